@@ -1,0 +1,803 @@
+/*
+ * morea_oracle.c -- the plain, slow, single-threaded CPU definition of MOREA's
+ * data-parallel hot path (arXiv 2303.04873), written from PAPER.md.
+ *
+ *   *** TEST INFRASTRUCTURE ONLY ***
+ *   Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ *   `--impl reference` leg may load or call this library.  It shares no code,
+ *   header, table or constant generator with the CUDA path under
+ *   paper_2303_04873_b200/, and it includes nothing from there.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fPIC -shared (no fast-math, no OpenMP, no
+ * SIMD intrinsics) so the fp64 results are reproducible.
+ *
+ * What it computes (citations are PAPER.md line numbers; readings O1..O13 are
+ * listed in DESIGN.md §3 and SURVEY.md §8(c)):
+ *   canonical fixed-point coordinates        O1  (paper silent)
+ *   signed-volume fold flags + severity      App. A.4, §4.3.1 L431   (O2)
+ *   voxel-centre sample sets, exactly-once   App. A.2 L739-742 + north_star   (O3)
+ *   piecewise-affine transform T, T'         App. A.2 "barycentric"      (O4)
+ *   trilinear interpolation, clamp           App. A.2 L744                    (O5)
+ *   h with exact zero/non-zero case split    §4.1.2 eq. L316-323              (O6)
+ *   f_intensity                              §4.1.2 eq. L316-317              (O7)
+ *   f_guidance, truncated distance maps      §4.1.3 eq. L338-342, App. A.3 L793-796 (O8)
+ *   f_magnitude, 10 edges incl. 4 spokes     §4.1.1 eq. L251-259              (O9)
+ *   partial evaluation (delta on dependents) §1, §4.2.1 L400-410        (O10)
+ *
+ * Everything that decides an integer (ownership, fold, the h case split, band
+ * membership) is decided exactly in integer arithmetic (int64 / __int128) or
+ * on identical fp32 values.  Values are fp64.  There is no blocking, fusion or
+ * reordering: every sample is visited by a per-voxel loop over each tet's
+ * bounding box, exactly as the definitions read.
+ *
+ * Parity pins for every function live in tests/test_oracle_*.py; the nearest
+ * point search used for the distance maps is an exact bucket search pinned to
+ * scipy.spatial.cKDTree and to brute force.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef __int128 i128;
+
+#define ORC_F_DOMAIN 1
+#define ORC_F_EMPTY 2
+
+/* Q.10 window (O1): Q in [-256*1024, 768*1024) on every axis. */
+#define QLO (-256LL * 1024LL)
+#define QHI (768LL * 1024LL)
+
+typedef struct {
+    double h_sum, g_sum, m_sum, severity;
+    int64_t n_samples;
+    int32_t folds, flags;
+} orc_acc;
+
+/* per-tet record returned by orc_eval_tets: 10 doubles */
+enum { PT_H = 0, PT_G, PT_NS, PT_NT, PT_M, PT_FOLD_S, PT_FOLD_T, PT_SEV, PT_DOMAIN, PT_PAD, PT_N };
+
+typedef struct {
+    int n[3];
+    int64_t V;
+    double sp[3];
+    float *I[2];
+    int K;
+    int64_t *coff[2];
+    float *cxyz[2];
+    double w[2][8 * 0 + 64]; /* pair weights |C_i|/|G| per side (K <= 64) */
+    double r;
+    int N, T;
+    float *base;
+    int32_t *tets;
+    float *cdelta;
+    int spoke_mode;
+    signed char *ref;
+    /* incidence CSR */
+    int32_t *inc_off, *inc;
+    /* lazy distance maps: memo[side][pair*V + v]; NaN = unknown, -1 = ">= r, not computed" */
+    float *memo[2];
+    /* bucket grid for exact nearest-point search */
+    int bsz, bn[3];
+    int32_t *boff[2][64];
+    int32_t *bidx[2][64];
+} orc_problem;
+
+/* ------------------------------------------------------------------ */
+/* O1: canonical coordinates  Q = round-half-even(1024 B + 1024 O) in fp64 */
+/* ------------------------------------------------------------------ */
+static int64_t canon(float b, float o) {
+    double v = 1024.0 * (double)b + 1024.0 * (double)o;
+    return (int64_t)nearbyint(v);
+}
+static int in_window(const int64_t q[3]) {
+    for (int a = 0; a < 3; a++)
+        if (q[a] < QLO || q[a] >= QHI) return 0;
+    return 1;
+}
+
+/* Q[side][k][axis] for the 4 vertices of tet t; returns 0 if any vertex is out of window */
+static int tet_coords(const orc_problem *P, const float *off, int t, int64_t Q[2][4][3]) {
+    int ok = 1;
+    for (int k = 0; k < 4; k++) {
+        int j = P->tets[4 * t + k];
+        for (int s = 0; s < 2; s++) {
+            for (int a = 0; a < 3; a++) {
+                float o = off ? off[6 * j + 3 * s + a] : 0.0f;
+                Q[s][k][a] = canon(P->base[3 * j + a], o);
+            }
+            if (!in_window(Q[s][k])) ok = 0;
+        }
+    }
+    return ok;
+}
+
+/* signed determinant det[Q1-Q0, Q2-Q0, Q3-Q0] (6 x signed volume, Q units^3), exact */
+static i128 det4(const int64_t Q[4][3]) {
+    i128 a[3], b[3], c[3];
+    for (int i = 0; i < 3; i++) {
+        a[i] = Q[1][i] - Q[0][i];
+        b[i] = Q[2][i] - Q[0][i];
+        c[i] = Q[3][i] - Q[0][i];
+    }
+    return a[0] * (b[1] * c[2] - b[2] * c[1]) - a[1] * (b[0] * c[2] - b[2] * c[0]) +
+           a[2] * (b[0] * c[1] - b[1] * c[0]);
+}
+static int sgn128(i128 v) { return (v > 0) - (v < 0); }
+
+/* ------------------------------------------------------------------ */
+/* O3: inward face normals and the exactly-once ownership predicate     */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    i128 n[4][3];    /* inward normal of the face opposite vertex k */
+    int64_t f0[4][3]; /* a vertex on that face */
+    i128 absdet;     /* |Delta| */
+} tet_faces;
+
+/* returns 0 if the tet is degenerate (Delta = 0): it owns nothing */
+static int make_faces(const int64_t Q[4][3], tet_faces *F) {
+    i128 d = det4(Q);
+    if (d == 0) return 0;
+    F->absdet = d < 0 ? -d : d;
+    for (int k = 0; k < 4; k++) {
+        int f[3], m = 0;
+        for (int j = 0; j < 4; j++)
+            if (j != k) f[m++] = j;
+        i128 u[3], v[3], w[3];
+        for (int a = 0; a < 3; a++) {
+            u[a] = Q[f[1]][a] - Q[f[0]][a];
+            v[a] = Q[f[2]][a] - Q[f[0]][a];
+            w[a] = Q[k][a] - Q[f[0]][a];
+        }
+        i128 n[3] = {u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2], u[0] * v[1] - u[1] * v[0]};
+        i128 s = n[0] * w[0] + n[1] * w[1] + n[2] * w[2]; /* = +-Delta */
+        for (int a = 0; a < 3; a++) {
+            F->n[k][a] = s > 0 ? n[a] : -n[a];
+            F->f0[k][a] = Q[f[0]][a];
+        }
+    }
+    return 1;
+}
+
+/* e_k(q) = n_k . (1024 q - f0_k): 4 x barycentric numerator, exact */
+static i128 face_eval(const tet_faces *F, int k, const int64_t q[3]) {
+    i128 e = 0;
+    for (int a = 0; a < 3; a++) e += F->n[k][a] * (i128)(1024 * q[a] - F->f0[k][a]);
+    return e;
+}
+/* lexpos(n): first non-zero component positive  (perturbation q + (eps, eps^2, eps^3)) */
+static int lexpos(const i128 n[3]) {
+    if (n[0] != 0) return n[0] > 0;
+    if (n[1] != 0) return n[1] > 0;
+    return n[2] > 0;
+}
+static int owns(const tet_faces *F, const int64_t q[3], i128 e[4]) {
+    for (int k = 0; k < 4; k++) {
+        e[k] = face_eval(F, k, q);
+        if (e[k] > 0) continue;
+        if (e[k] == 0 && lexpos(F->n[k])) continue;
+        return 0;
+    }
+    return 1;
+}
+
+/* lattice bbox of the tet clipped to the image: ceil(min Q/1024) .. floor(max Q/1024) */
+static int64_t floordiv(int64_t a, int64_t b) {
+    int64_t q = a / b;
+    if ((a % b != 0) && ((a < 0) != (b < 0))) q--;
+    return q;
+}
+static int64_t ceildiv(int64_t a, int64_t b) { return -floordiv(-a, b); }
+static void tet_bbox(const orc_problem *P, const int64_t Q[4][3], int64_t lo[3], int64_t hi[3]) {
+    for (int a = 0; a < 3; a++) {
+        int64_t mn = Q[0][a], mx = Q[0][a];
+        for (int k = 1; k < 4; k++) {
+            if (Q[k][a] < mn) mn = Q[k][a];
+            if (Q[k][a] > mx) mx = Q[k][a];
+        }
+        lo[a] = ceildiv(mn, 1024);
+        hi[a] = floordiv(mx, 1024);
+        if (lo[a] < 0) lo[a] = 0;
+        if (hi[a] > P->n[a] - 1) hi[a] = P->n[a] - 1;
+    }
+}
+
+static int64_t vidx(const orc_problem *P, int64_t x, int64_t y, int64_t z) {
+    return (z * P->n[1] + y) * P->n[0] + x;
+}
+
+/* ------------------------------------------------------------------ */
+/* O5: trilinear interpolation with clamp to the border (fp64)          */
+/* ------------------------------------------------------------------ */
+static double trilinear(const orc_problem *P, const float *vol, const double x[3]) {
+    int64_t i0[3];
+    double f[3];
+    for (int a = 0; a < 3; a++) {
+        double xc = x[a];
+        if (xc < 0.0) xc = 0.0;
+        if (xc > (double)(P->n[a] - 1)) xc = (double)(P->n[a] - 1);
+        int64_t fl = (int64_t)floor(xc);
+        if (fl > P->n[a] - 2) fl = P->n[a] - 2;
+        i0[a] = fl;
+        f[a] = xc - (double)fl;
+    }
+    double v = 0.0;
+    for (int dz = 0; dz < 2; dz++)
+        for (int dy = 0; dy < 2; dy++)
+            for (int dx = 0; dx < 2; dx++) {
+                double w = (dx ? f[0] : 1.0 - f[0]) * (dy ? f[1] : 1.0 - f[1]) * (dz ? f[2] : 1.0 - f[2]);
+                v += w * (double)vol[vidx(P, i0[0] + dx, i0[1] + dy, i0[2] + dz)];
+            }
+    return v;
+}
+
+/* ------------------------------------------------------------------ */
+/* O4 + O6: exact transform numerators and the exact contributing set  */
+/* ------------------------------------------------------------------ */
+/* Position on axis a is x_a = Pnum_a / M with M = 1024 |Delta| > 0 (exact rational).
+ * Contributing lattice indices of the clamped trilinear footprint on that axis:
+ *   x <= 0      -> {0}
+ *   x >= n-1    -> {n-1}
+ *   x integer   -> {x}
+ *   otherwise   -> {floor x, floor x + 1}                                   */
+static int axis_set(i128 Pnum, i128 M, int n, int64_t out[2]) {
+    if (Pnum <= 0) { out[0] = 0; return 1; }
+    if (Pnum >= (i128)(n - 1) * M) { out[0] = n - 1; return 1; }
+    i128 fl = Pnum / M; /* Pnum > 0, M > 0: truncation = floor */
+    if (Pnum % M == 0) { out[0] = (int64_t)fl; return 1; }
+    out[0] = (int64_t)fl;
+    out[1] = (int64_t)fl + 1;
+    return 2;
+}
+
+/* fg(b): some contributing corner has I > 0 (exactly) */
+static int fg_exact(const orc_problem *P, const float *vol, const i128 Pnum[3], i128 M) {
+    int64_t s[3][2];
+    int c[3];
+    for (int a = 0; a < 3; a++) c[a] = axis_set(Pnum[a], M, P->n[a], s[a]);
+    for (int k = 0; k < c[2]; k++)
+        for (int j = 0; j < c[1]; j++)
+            for (int i = 0; i < c[0]; i++)
+                if (vol[vidx(P, s[0][i], s[1][j], s[2][k])] > 0.0f) return 1;
+    return 0;
+}
+
+/* h(a, b) of PAPER.md §4.1.2 L318-322 with the case decided by (a > 0, fg) */
+static double h_of(double a, double b, int fg) {
+    if (a > 0.0 && fg) return (a - b) * (a - b);
+    if (a == 0.0 && !fg) return 0.0;
+    return 1.0;
+}
+
+/* ------------------------------------------------------------------ */
+/* O8: distance maps  D_i(q) = min_c || (q - c) . spacing ||  (fp64 -> fp32) */
+/* ------------------------------------------------------------------ */
+static double sqdist(const orc_problem *P, const int64_t q[3], const float *c) {
+    double dx = ((double)q[0] - (double)c[0]) * P->sp[0];
+    double dy = ((double)q[1] - (double)c[1]) * P->sp[1];
+    double dz = ((double)q[2] - (double)c[2]) * P->sp[2];
+    return dx * dx + dy * dy + dz * dz;
+}
+
+static int bucket_of(const orc_problem *P, double c, int a) {
+    int b = (int)floor((c + 1.0) / (double)P->bsz);
+    if (b < 0) b = 0;
+    if (b > P->bn[a] - 1) b = P->bn[a] - 1;
+    return b;
+}
+
+/* exact min over the pair's points of sqdist, searching buckets in Chebyshev
+ * rings around q's bucket; stops only once every unvisited point is provably
+ * farther than the best found (or farther than `limit2` if limit2 > 0). */
+static double nearest_sq(const orc_problem *P, int side, int pair, const int64_t q[3], double limit2) {
+    const float *pts = P->cxyz[side] + 3 * P->coff[side][pair];
+    const int32_t *off = P->boff[side][pair];
+    const int32_t *idx = P->bidx[side][pair];
+    int qb[3];
+    for (int a = 0; a < 3; a++) qb[a] = bucket_of(P, (double)q[a], a);
+    double smin = P->sp[0];
+    if (P->sp[1] < smin) smin = P->sp[1];
+    if (P->sp[2] < smin) smin = P->sp[2];
+    double best = INFINITY;
+    int maxring = P->bn[0];
+    if (P->bn[1] > maxring) maxring = P->bn[1];
+    if (P->bn[2] > maxring) maxring = P->bn[2];
+    for (int ring = 0; ring <= maxring; ring++) {
+        for (int bz = qb[2] - ring; bz <= qb[2] + ring; bz++) {
+            if (bz < 0 || bz >= P->bn[2]) continue;
+            for (int by = qb[1] - ring; by <= qb[1] + ring; by++) {
+                if (by < 0 || by >= P->bn[1]) continue;
+                for (int bx = qb[0] - ring; bx <= qb[0] + ring; bx++) {
+                    if (bx < 0 || bx >= P->bn[0]) continue;
+                    int cheb = abs(bx - qb[0]);
+                    if (abs(by - qb[1]) > cheb) cheb = abs(by - qb[1]);
+                    if (abs(bz - qb[2]) > cheb) cheb = abs(bz - qb[2]);
+                    if (cheb != ring) continue;
+                    int b = (bz * P->bn[1] + by) * P->bn[0] + bx;
+                    for (int32_t t = off[b]; t < off[b + 1]; t++) {
+                        double d2 = sqdist(P, q, pts + 3 * idx[t]);
+                        if (d2 < best) best = d2;
+                    }
+                }
+            }
+        }
+        /* any unvisited point lies >= ring*bsz voxels away along some axis
+         * (a point at the clamp border can only be farther) */
+        double lb = (double)ring * (double)P->bsz * smin;
+        double lb2 = lb * lb * (1.0 - 1e-9);
+        if (best <= lb2) break;
+        if (limit2 > 0.0 && lb2 >= limit2) break;
+    }
+    return best;
+}
+
+/* exact fp32 map value at voxel q for pair i on side s (memoised) */
+static float dmap_exact(orc_problem *P, int s, int i, const int64_t q[3]) {
+    int64_t v = vidx(P, q[0], q[1], q[2]);
+    float *m = &P->memo[s][(int64_t)i * P->V + v];
+    if (isnan(*m) || *m < 0.0f) {
+        double d2 = nearest_sq(P, s, i, q, 0.0);
+        *m = (float)sqrt(d2);
+    }
+    return *m;
+}
+
+/* band membership d = D_i(q) < r; returns 1 and sets *d if in band */
+static int band(orc_problem *P, int s, int i, const int64_t q[3], float *d) {
+    int64_t v = vidx(P, q[0], q[1], q[2]);
+    float *m = &P->memo[s][(int64_t)i * P->V + v];
+    if (isnan(*m)) {
+        /* any point with sqdist < (r(1+1e-6))^2 ?  if none, D >= r certainly */
+        double lim = P->r * (1.0 + 1e-6);
+        double d2 = nearest_sq(P, s, i, q, lim * lim);
+        if (d2 >= lim * lim) {
+            *m = -1.0f; /* marker: >= r, value not needed for the band */
+            return 0;
+        }
+        *m = (float)sqrt(nearest_sq(P, s, i, q, 0.0));
+    }
+    if (*m < 0.0f) return 0;
+    *d = *m;
+    return (double)*m < P->r;
+}
+
+static double trilinear_map(orc_problem *P, int s, int i, const double x[3]) {
+    int64_t i0[3];
+    double f[3];
+    for (int a = 0; a < 3; a++) {
+        double xc = x[a];
+        if (xc < 0.0) xc = 0.0;
+        if (xc > (double)(P->n[a] - 1)) xc = (double)(P->n[a] - 1);
+        int64_t fl = (int64_t)floor(xc);
+        if (fl > P->n[a] - 2) fl = P->n[a] - 2;
+        i0[a] = fl;
+        f[a] = xc - (double)fl;
+    }
+    double v = 0.0;
+    for (int dz = 0; dz < 2; dz++)
+        for (int dy = 0; dy < 2; dy++)
+            for (int dx = 0; dx < 2; dx++) {
+                double w = (dx ? f[0] : 1.0 - f[0]) * (dy ? f[1] : 1.0 - f[1]) * (dz ? f[2] : 1.0 - f[2]);
+                int64_t q[3] = {i0[0] + dx, i0[1] + dy, i0[2] + dz};
+                v += w * (double)dmap_exact(P, s, i, q);
+            }
+    return v;
+}
+
+/* ------------------------------------------------------------------ */
+/* O9: f_magnitude per tet: c_delta * sum over 10 edges (|e_s| - |e_t|)^2, mm */
+/* ------------------------------------------------------------------ */
+static double edge_len(const orc_problem *P, const int64_t Q[4][3], int kind, int u, int v) {
+    double s = 0.0;
+    for (int a = 0; a < 3; a++) {
+        double comp;
+        if (kind == 0) {
+            comp = (double)(Q[u][a] - Q[v][a]) / 1024.0;
+        } else {
+            /* spoke: vertex u -> centroid of the opposite face (SURVEY.md O9 / S:L201),
+             * (3 Q_u - sum of the other three) / 3 / 1024; spoke_mode 1 = tet centroid,
+             * which is 3/4 of that vector */
+            int64_t sum = 0;
+            for (int k = 0; k < 4; k++)
+                if (k != u) sum += Q[k][a];
+            comp = (double)(3 * Q[u][a] - sum) / 3072.0;
+            if (P->spoke_mode == 1) comp *= 0.75;
+        }
+        comp *= P->sp[a];
+        s += comp * comp;
+    }
+    return sqrt(s);
+}
+
+static double magnitude(const orc_problem *P, int t, const int64_t Q[2][4][3]) {
+    static const int E[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+    double m = 0.0;
+    for (int e = 0; e < 6; e++) {
+        double d = edge_len(P, Q[0], 0, E[e][0], E[e][1]) - edge_len(P, Q[1], 0, E[e][0], E[e][1]);
+        m += d * d;
+    }
+    for (int k = 0; k < 4; k++) {
+        double d = edge_len(P, Q[0], 1, k, 0) - edge_len(P, Q[1], 1, k, 0);
+        m += d * d;
+    }
+    return (double)P->cdelta[t] * m;
+}
+
+/* ------------------------------------------------------------------ */
+/* One tet, one side: visit every lattice point of its bbox, keep the owned */
+/* ones, accumulate h (O6/O7) and the guidance term (O8).               */
+/* ------------------------------------------------------------------ */
+static void tet_side_samples(orc_problem *P, int s, const int64_t Q[2][4][3], double *h_sum,
+                             double *g_sum, int64_t *n_owned, int32_t *owner_map, int tet_id) {
+    tet_faces F;
+    if (!make_faces(Q[s], &F)) return; /* degenerate: owns nothing */
+    int so = 1 - s;
+    const float *Iown = P->I[s], *Ioth = P->I[so];
+    i128 M = (i128)1024 * F.absdet;
+    i128 U[4][3];
+    for (int k = 0; k < 4; k++)
+        for (int a = 0; a < 3; a++) U[k][a] = (i128)(Q[so][k][a] - Q[s][k][a]);
+    int64_t lo[3], hi[3];
+    tet_bbox(P, Q[s], lo, hi);
+    for (int64_t z = lo[2]; z <= hi[2]; z++)
+        for (int64_t y = lo[1]; y <= hi[1]; y++)
+            for (int64_t x = lo[0]; x <= hi[0]; x++) {
+                int64_t q[3] = {x, y, z};
+                i128 e[4];
+                if (!owns(&F, q, e)) continue;
+                if (owner_map) {
+                    int64_t v = vidx(P, x, y, z);
+                    owner_map[v] = owner_map[v] == -1 ? tet_id : -2;
+                    continue;
+                }
+                (*n_owned)++;
+                /* O4: x = q + sum_k lambda_k U_k / 1024, lambda_k = e_k / |Delta| */
+                i128 Pnum[3];
+                double xp[3];
+                for (int a = 0; a < 3; a++) {
+                    i128 Nn = 0;
+                    for (int k = 0; k < 4; k++) Nn += e[k] * U[k][a];
+                    Pnum[a] = (i128)q[a] * M + Nn;
+                    xp[a] = (double)q[a] + (double)Nn / ((double)F.absdet * 1024.0);
+                }
+                double a_val = (double)Iown[vidx(P, x, y, z)];
+                double b_val = trilinear(P, Ioth, xp);
+                int fg = fg_exact(P, Ioth, Pnum, M);
+                *h_sum += h_of(a_val, b_val, fg);
+                /* O8: guidance over the pairs whose source-side distance is < r */
+                for (int i = 0; i < P->K; i++) {
+                    float d;
+                    if (!band(P, s, i, q, &d)) continue;
+                    double Dp = trilinear_map(P, so, i, xp);
+                    double dd = (double)d - Dp;
+                    *g_sum += P->w[s][i] * ((P->r - (double)d) / P->r) * dd * dd;
+                }
+            }
+}
+
+/* per-tet contributions (both sides) for one solution */
+static void tet_contrib(orc_problem *P, const float *off, int t, double rec[PT_N]) {
+    memset(rec, 0, sizeof(double) * PT_N);
+    int64_t Q[2][4][3];
+    if (!tet_coords(P, off, t, Q)) {
+        rec[PT_DOMAIN] = 1.0;
+        return;
+    }
+    for (int s = 0; s < 2; s++) {
+        i128 d = det4(Q[s]);
+        if (sgn128(d) != P->ref[t]) { /* O2: sign change, zero counts as a fold */
+            rec[s == 0 ? PT_FOLD_S : PT_FOLD_T] = 1.0;
+            double vol = (double)(d < 0 ? -d : d) / (6.0 * 1073741824.0);
+            rec[PT_SEV] += vol * P->sp[0] * P->sp[1] * P->sp[2];
+        }
+        int64_t n = 0;
+        tet_side_samples(P, s, Q, &rec[PT_H], &rec[PT_G], &n, NULL, t);
+        rec[s == 0 ? PT_NS : PT_NT] = (double)n;
+    }
+    rec[PT_M] = magnitude(P, t, Q);
+}
+
+/* ------------------------------------------------------------------ */
+/* Public entry points (ctypes)                                        */
+/* ------------------------------------------------------------------ */
+void orc_destroy(orc_problem *P);
+
+orc_problem *orc_create(int nx, int ny, int nz, const double *spacing, const float *I_s,
+                        const float *I_t, int K, const int64_t *cs_off, const float *cs_xyz,
+                        const int64_t *ct_off, const float *ct_xyz, double r_mm, int N,
+                        const float *base, int T, const int32_t *tets, const float *c_delta,
+                        int spoke_mode, int *status) {
+    *status = 0;
+    if (nx < 2 || ny < 2 || nz < 2 || K < 0 || K > 64 || N < 4 || T < 1) { *status = -1; return NULL; }
+    orc_problem *P = (orc_problem *)calloc(1, sizeof(orc_problem));
+    P->n[0] = nx; P->n[1] = ny; P->n[2] = nz;
+    P->V = (int64_t)nx * ny * nz;
+    for (int a = 0; a < 3; a++) P->sp[a] = spacing[a];
+    const float *Is[2] = {I_s, I_t};
+    const int64_t *co[2] = {cs_off, ct_off};
+    const float *cx[2] = {cs_xyz, ct_xyz};
+    for (int s = 0; s < 2; s++) {
+        P->I[s] = (float *)malloc(sizeof(float) * P->V);
+        memcpy(P->I[s], Is[s], sizeof(float) * P->V);
+        P->coff[s] = (int64_t *)malloc(sizeof(int64_t) * (K + 1));
+        memcpy(P->coff[s], co[s], sizeof(int64_t) * (K + 1));
+        int64_t M = co[s][K];
+        P->cxyz[s] = (float *)malloc(sizeof(float) * 3 * (M > 0 ? M : 1));
+        if (M > 0) memcpy(P->cxyz[s], cx[s], sizeof(float) * 3 * M);
+        /* w_i = |C_i| / |G_side| */
+        for (int i = 0; i < K; i++) P->w[s][i] = M > 0 ? (double)(co[s][i + 1] - co[s][i]) / (double)M : 0.0;
+        P->memo[s] = (float *)malloc(sizeof(float) * P->V * (K > 0 ? K : 1));
+        for (int64_t v = 0; v < P->V * (K > 0 ? K : 1); v++) P->memo[s][v] = NAN;
+    }
+    P->K = K;
+    /* r = 2.5 % of the image width (App. A.3) when not given */
+    P->r = r_mm > 0.0 ? r_mm : 0.025 * (double)nx * spacing[0];
+    P->N = N;
+    P->T = T;
+    P->base = (float *)malloc(sizeof(float) * 3 * N);
+    memcpy(P->base, base, sizeof(float) * 3 * N);
+    P->tets = (int32_t *)malloc(sizeof(int32_t) * 4 * T);
+    memcpy(P->tets, tets, sizeof(int32_t) * 4 * T);
+    P->cdelta = (float *)malloc(sizeof(float) * T);
+    for (int t = 0; t < T; t++) P->cdelta[t] = c_delta ? c_delta[t] : 1.0f;
+    P->spoke_mode = spoke_mode;
+    P->ref = (signed char *)malloc(T);
+    for (int t = 0; t < 4 * T; t++)
+        if (tets[t] < 0 || tets[t] >= N) { *status = -1; orc_destroy(P); return NULL; }
+    /* reference signs from the initial mesh (App. A.4) */
+    for (int t = 0; t < T; t++) {
+        int64_t Q[2][4][3];
+        if (!tet_coords(P, NULL, t, Q)) { *status = -3; orc_destroy(P); return NULL; }
+        int sg = sgn128(det4(Q[0]));
+        if (sg == 0) { *status = -3; orc_destroy(P); return NULL; }
+        P->ref[t] = (signed char)sg;
+    }
+    /* incidence CSR: tets incident to each point */
+    P->inc_off = (int32_t *)calloc(N + 1, sizeof(int32_t));
+    for (int t = 0; t < 4 * T; t++) P->inc_off[tets[t] + 1]++;
+    for (int j = 0; j < N; j++) P->inc_off[j + 1] += P->inc_off[j];
+    P->inc = (int32_t *)malloc(sizeof(int32_t) * 4 * T);
+    int32_t *fill = (int32_t *)calloc(N, sizeof(int32_t));
+    for (int t = 0; t < T; t++)
+        for (int k = 0; k < 4; k++) {
+            int j = tets[4 * t + k];
+            int dup = 0;
+            for (int32_t u = P->inc_off[j]; u < P->inc_off[j] + fill[j]; u++)
+                if (P->inc[u] == t) dup = 1;
+            if (!dup) P->inc[P->inc_off[j] + fill[j]++] = t;
+        }
+    /* compact (a tet listing a point twice is invalid anyway) */
+    free(fill);
+    /* bucket grid for the nearest-point search */
+    P->bsz = 4;
+    for (int a = 0; a < 3; a++) P->bn[a] = (P->n[a] + 2) / P->bsz + 1;
+    int nb = P->bn[0] * P->bn[1] * P->bn[2];
+    for (int s = 0; s < 2; s++)
+        for (int i = 0; i < K; i++) {
+            int64_t c0 = P->coff[s][i], c1 = P->coff[s][i + 1];
+            int32_t *off = (int32_t *)calloc(nb + 1, sizeof(int32_t));
+            int32_t *idx = (int32_t *)malloc(sizeof(int32_t) * (c1 - c0 + 1));
+            int *bid = (int *)malloc(sizeof(int) * (c1 - c0 + 1));
+            for (int64_t c = c0; c < c1; c++) {
+                const float *p = P->cxyz[s] + 3 * c;
+                int b = (bucket_of(P, p[2], 2) * P->bn[1] + bucket_of(P, p[1], 1)) * P->bn[0] +
+                        bucket_of(P, p[0], 0);
+                bid[c - c0] = b;
+                off[b + 1]++;
+            }
+            for (int b = 0; b < nb; b++) off[b + 1] += off[b];
+            int32_t *cur = (int32_t *)malloc(sizeof(int32_t) * (nb + 1));
+            memcpy(cur, off, sizeof(int32_t) * (nb + 1));
+            for (int64_t c = c0; c < c1; c++) idx[cur[bid[c - c0]]++] = (int32_t)(c - c0);
+            free(cur);
+            free(bid);
+            P->boff[s][i] = off;
+            P->bidx[s][i] = idx;
+        }
+    return P;
+}
+
+void orc_destroy(orc_problem *P) {
+    if (!P) return;
+    for (int s = 0; s < 2; s++) {
+        free(P->I[s]); free(P->coff[s]); free(P->cxyz[s]); free(P->memo[s]);
+        for (int i = 0; i < 64; i++) { free(P->boff[s][i]); free(P->bidx[s][i]); }
+    }
+    free(P->base); free(P->tets); free(P->cdelta); free(P->ref); free(P->inc_off); free(P->inc);
+    free(P);
+}
+
+/* per-tet records (PT_N doubles each) for the tets in `sub` (or all when sub == NULL) */
+int orc_eval_tets(orc_problem *P, const float *offsets_one, int n_sub, const int32_t *sub, double *out) {
+    int n = sub ? n_sub : P->T;
+    for (int i = 0; i < n; i++) tet_contrib(P, offsets_one, sub ? sub[i] : i, out + (int64_t)PT_N * i);
+    return 0;
+}
+
+static void acc_objectives(const orc_problem *P, const orc_acc *acc, double obj[3]) {
+    if ((acc->flags & (ORC_F_DOMAIN | ORC_F_EMPTY)) || acc->n_samples == 0) {
+        obj[0] = obj[1] = obj[2] = NAN;
+        return;
+    }
+    obj[0] = acc->m_sum / (10.0 * (double)P->T);          /* L258 */
+    obj[1] = acc->h_sum / (double)acc->n_samples;          /* L317 */
+    obj[2] = acc->g_sum / (double)acc->n_samples;          /* L339 */
+}
+
+static int any_out_of_window(const orc_problem *P, const float *off) {
+    for (int j = 0; j < P->N; j++)
+        for (int s = 0; s < 2; s++) {
+            int64_t q[3];
+            for (int a = 0; a < 3; a++) q[a] = canon(P->base[3 * j + a], off[6 * j + 3 * s + a]);
+            if (!in_window(q)) return 1;
+        }
+    return 0;
+}
+
+/* full evaluation of one solution (sum over all tets in index order) */
+int orc_eval(orc_problem *P, const float *offsets_one, double obj[3], orc_acc *acc) {
+    memset(acc, 0, sizeof(*acc));
+    double rec[PT_N];
+    for (int t = 0; t < P->T; t++) {
+        tet_contrib(P, offsets_one, t, rec);
+        acc->h_sum += rec[PT_H];
+        acc->g_sum += rec[PT_G];
+        acc->m_sum += rec[PT_M];
+        acc->severity += rec[PT_SEV];
+        acc->n_samples += (int64_t)rec[PT_NS] + (int64_t)rec[PT_NT];
+        acc->folds += (int32_t)rec[PT_FOLD_S] + (int32_t)rec[PT_FOLD_T];
+    }
+    if (any_out_of_window(P, offsets_one)) acc->flags |= ORC_F_DOMAIN;
+    if (acc->n_samples == 0) acc->flags |= ORC_F_EMPTY;
+    acc_objectives(P, acc, obj);
+    return 0;
+}
+
+/* O10: partial evaluation of one group S for one solution.
+ * D = union of the tets incident to S; acc' = acc - sum_D old + sum_D new. */
+int orc_eval_partial(orc_problem *P, const float *base_offsets_one, const orc_acc *base_acc,
+                     int n_changed, const int32_t *changed, const float *new_vals, double obj[3],
+                     orc_acc *acc) {
+    char *in_d = (char *)calloc(P->T, 1);
+    for (int i = 0; i < n_changed; i++) {
+        int j = changed[i];
+        if (j < 0 || j >= P->N) { free(in_d); return -1; }
+        for (int32_t u = P->inc_off[j]; u < P->inc_off[j + 1]; u++) in_d[P->inc[u]] = 1;
+    }
+    float *nw = (float *)malloc(sizeof(float) * 6 * P->N);
+    memcpy(nw, base_offsets_one, sizeof(float) * 6 * P->N);
+    for (int i = 0; i < n_changed; i++)
+        for (int c = 0; c < 6; c++) nw[6 * changed[i] + c] = new_vals[6 * i + c];
+    *acc = *base_acc;
+    double ro[PT_N], rn[PT_N];
+    int dom_new = 0;
+    for (int t = 0; t < P->T; t++) {
+        if (!in_d[t]) continue;
+        tet_contrib(P, base_offsets_one, t, ro);
+        tet_contrib(P, nw, t, rn);
+        acc->h_sum += rn[PT_H] - ro[PT_H];
+        acc->g_sum += rn[PT_G] - ro[PT_G];
+        acc->m_sum += rn[PT_M] - ro[PT_M];
+        acc->severity += rn[PT_SEV] - ro[PT_SEV];
+        acc->n_samples += (int64_t)(rn[PT_NS] + rn[PT_NT]) - (int64_t)(ro[PT_NS] + ro[PT_NT]);
+        acc->folds += (int32_t)(rn[PT_FOLD_S] + rn[PT_FOLD_T]) - (int32_t)(ro[PT_FOLD_S] + ro[PT_FOLD_T]);
+        if (rn[PT_DOMAIN] != 0.0) dom_new = 1;
+    }
+    acc->flags = (base_acc->flags & ORC_F_DOMAIN) | (dom_new ? ORC_F_DOMAIN : 0);
+    for (int i = 0; i < n_changed; i++)
+        for (int s = 0; s < 2; s++) {
+            int64_t q[3];
+            for (int a = 0; a < 3; a++) q[a] = canon(P->base[3 * changed[i] + a], new_vals[6 * i + 3 * s + a]);
+            if (!in_window(q)) acc->flags |= ORC_F_DOMAIN;
+        }
+    if (acc->n_samples == 0) acc->flags |= ORC_F_EMPTY;
+    acc_objectives(P, acc, obj);
+    free(in_d);
+    free(nw);
+    return 0;
+}
+
+/* fold flags per (side, tet) + count and severity (O2; row a9) */
+int orc_check_folds(orc_problem *P, const float *offsets_one, int32_t *count, double *severity,
+                    uint8_t *flags /* 2*T or NULL */) {
+    *count = 0;
+    *severity = 0.0;
+    for (int t = 0; t < P->T; t++) {
+        int64_t Q[2][4][3];
+        if (!tet_coords(P, offsets_one, t, Q)) {
+            if (flags) flags[t] = flags[P->T + t] = 0;
+            continue;
+        }
+        for (int s = 0; s < 2; s++) {
+            i128 d = det4(Q[s]);
+            int f = sgn128(d) != P->ref[t];
+            if (flags) flags[(int64_t)s * P->T + t] = (uint8_t)f;
+            if (f) {
+                (*count)++;
+                *severity += (double)(d < 0 ? -d : d) / (6.0 * 1073741824.0) * P->sp[0] * P->sp[1] * P->sp[2];
+            }
+        }
+    }
+    return 0;
+}
+
+/* owner of every voxel on one side: tet id, -1 none, -2 more than one (O3) */
+int orc_owner_map(orc_problem *P, const float *offsets_one, int side, int32_t *owner) {
+    for (int64_t v = 0; v < P->V; v++) owner[v] = -1;
+    for (int t = 0; t < P->T; t++) {
+        int64_t Q[2][4][3];
+        if (!tet_coords(P, offsets_one, t, Q)) continue;
+        tet_side_samples(P, side, Q, NULL, NULL, NULL, owner, t);
+    }
+    return 0;
+}
+
+/* full fp32 distance map of pair i on side s (exact nearest-point distances) */
+int orc_distance_map(orc_problem *P, int s, int i, float *out) {
+    for (int64_t z = 0; z < P->n[2]; z++)
+        for (int64_t y = 0; y < P->n[1]; y++)
+            for (int64_t x = 0; x < P->n[0]; x++) {
+                int64_t q[3] = {x, y, z};
+                out[vidx(P, x, y, z)] = dmap_exact(P, s, i, q);
+            }
+    return 0;
+}
+
+/* debug: one sample of tet t on side s at lattice point q.
+ * out = {owned, x, y, z (fp64 transformed position), a, b, fg, h,
+ *        floor/integer code per axis (3 values: 2*set_size + (first index sign))} */
+int orc_sample_debug(orc_problem *P, const float *offsets_one, int t, int s, const int64_t *q,
+                     double *out, int64_t *sets /* 3 x 3: count, idx0, idx1 */) {
+    int64_t Q[2][4][3];
+    memset(out, 0, sizeof(double) * 8);
+    if (!tet_coords(P, offsets_one, t, Q)) return -1;
+    tet_faces F;
+    if (!make_faces(Q[s], &F)) return -2;
+    i128 e[4];
+    int o = owns(&F, q, e);
+    out[0] = o;
+    /* evaluate the affine map even when not owned (barycentrics may be negative) */
+    for (int k = 0; k < 4; k++) e[k] = face_eval(&F, k, q);
+    int so = 1 - s;
+    i128 M = (i128)1024 * F.absdet, Pnum[3];
+    double xp[3];
+    for (int a = 0; a < 3; a++) {
+        i128 Nn = 0;
+        for (int k = 0; k < 4; k++) Nn += e[k] * (i128)(Q[so][k][a] - Q[s][k][a]);
+        Pnum[a] = (i128)q[a] * M + Nn;
+        xp[a] = (double)q[a] + (double)Nn / ((double)F.absdet * 1024.0);
+        out[1 + a] = xp[a];
+        int64_t st[2] = {0, 0};
+        int c = axis_set(Pnum[a], M, P->n[a], st);
+        sets[3 * a + 0] = c;
+        sets[3 * a + 1] = st[0];
+        sets[3 * a + 2] = c == 2 ? st[1] : -1;
+    }
+    int inimg = q[0] >= 0 && q[0] < P->n[0] && q[1] >= 0 && q[1] < P->n[1] && q[2] >= 0 && q[2] < P->n[2];
+    out[4] = inimg ? (double)P->I[s][vidx(P, q[0], q[1], q[2])] : NAN;
+    out[5] = trilinear(P, P->I[so], xp);
+    out[6] = fg_exact(P, P->I[so], Pnum, M);
+    out[7] = inimg ? h_of(out[4], out[5], (int)out[6]) : NAN;
+    return 0;
+}
+
+/* exported helpers for the pin tests (pure functions of their arguments) */
+double orc_h(double a, double b, int fg) { return h_of(a, b, fg); }
+double orc_trilinear_raw(int nx, int ny, int nz, const float *vol, double x, double y, double z) {
+    orc_problem tmp;
+    memset(&tmp, 0, sizeof(tmp));
+    tmp.n[0] = nx; tmp.n[1] = ny; tmp.n[2] = nz;
+    double p[3] = {x, y, z};
+    return trilinear(&tmp, vol, p);
+}
+int orc_signed_det(const int64_t *Q12, int64_t *hi, uint64_t *lo) {
+    int64_t Q[4][3];
+    memcpy(Q, Q12, sizeof(Q));
+    i128 d = det4(Q);
+    *hi = (int64_t)(d >> 64);
+    *lo = (uint64_t)d;
+    return sgn128(d);
+}
+int64_t orc_canon(float b, float o) { return canon(b, o); }
+int orc_ref_sign(const orc_problem *P, int t) { return P->ref[t]; }
+double orc_r(const orc_problem *P) { return P->r; }
