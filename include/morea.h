@@ -1,0 +1,192 @@
+/*
+ * morea.h -- C-ABI of the B200-native MOREA hot path (arXiv 2303.04873).
+ *
+ * Batched evaluation of dual-dynamic tetrahedral-mesh deformations over a whole
+ * MO-RV-GOMEA population: f_magnitude (§4.1.1, eq. L257-259),
+ * f_intensity (§4.1.2, eq. L316-323), f_guidance (§4.1.3, eq. L338-342;
+ * App. A.3) and signed-volume fold detection (§4.1.4; App. A.4
+ * L806-810), as full evaluations and as GOMEA partial evaluations over the
+ * tetrahedra that depend on a changed FOS point set (§1, §4.2.1
+ * L399-410).  The readings of the paper that fix every ambiguous detail are
+ * listed in DESIGN.md §3 (O1..O13); the short forms are repeated per call.
+ *
+ * Conventions common to every call
+ *  - Positions are in voxel-index units: voxel (i,j,k) has its centre at
+ *    (i,j,k).  Volumes are float32, x-fastest (index (k*ny + j)*nx + i).
+ *  - Every buffer is caller-owned.  Unless a call says otherwise, an array
+ *    argument may be HOST memory (pageable or pinned) or DEVICE memory of the
+ *    context's device; the library detects which (cudaPointerGetAttributes).
+ *    Host inputs are staged to device scratch inside the call; when any
+ *    output is host memory the call synchronises the context stream before
+ *    returning.  When every pointer is device memory the call is asynchronous
+ *    and stream-ordered on the context stream.
+ *  - A context is bound to one device and is not thread-safe.  Multi-GPU use
+ *    is one context per process/rank; the library itself makes no NCCL calls.
+ *  - Return value: MOREA_OK (0) or a negative MOREA_E* code; the message is
+ *    available from morea_last_error().  Per-solution conditions are FLAGS in
+ *    morea_acc.flags, never errors (a batch never fails for one solution).
+ */
+#ifndef MOREA_H
+#define MOREA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes ---- */
+#define MOREA_OK 0
+#define MOREA_EINVAL (-1)  /* bad shape/index/value, negative or NaN intensity */
+#define MOREA_ESTATE (-2)  /* eval before morea_load_images / morea_set_mesh */
+#define MOREA_EDOMAIN (-3) /* base point outside the Q.10 window or degenerate base tet */
+#define MOREA_ECUDA (-4)   /* CUDA runtime error (message has the CUDA error string) */
+#define MOREA_ENOMEM (-5)  /* device allocation failed */
+
+/* ---- per-solution flags (morea_acc.flags) ---- */
+#define MOREA_F_DOMAIN 1 /* some point outside the Q.10 window: objectives are NaN */
+#define MOREA_F_EMPTY 2  /* no samples (n_samples == 0): objectives are NaN */
+
+/* ---- morea_set_mesh options ---- */
+#define MOREA_SPOKE_FACE_CENTROID 0 /* spoke = vertex -> centroid of the opposite face (O9, default) */
+#define MOREA_SPOKE_TET_CENTROID 1  /* spoke = tet centroid -> vertex (3/4 of the above) */
+
+/* Q.10 window (reading O1): canonical coordinates Q = round-half-even(1024*B +
+ * 1024*O) must satisfy -256*1024 <= Q < 768*1024 on every axis. */
+#define MOREA_WINDOW_LO_VOX (-256)
+#define MOREA_WINDOW_HI_VOX 768
+
+typedef struct morea_ctx morea_ctx;
+
+/* Per-solution accumulator (48 bytes).  Objectives derive from it as
+ *   f_magnitude = m_sum / (10 T)      (L258)
+ *   f_intensity = h_sum / n_samples   (L317, n_samples = |P_s| + |P_t|)
+ *   f_guidance  = g_sum / n_samples   (L339)
+ * folds = number of (tet, side) pairs whose exact signed volume has another
+ * sign than the tet's reference sign (0 counts as a fold; App. A.4,
+ * "either of the two meshes" §4.3.1); severity = sum of |signed volume|
+ * in mm^3 over those pairs (L810).  folds > 0 means infeasible: objectives are
+ * still written but voxels may be owned twice (or not at all). */
+typedef struct {
+    double h_sum, g_sum, m_sum, severity;
+    int64_t n_samples;
+    int32_t folds, flags;
+} morea_acc;
+
+/* Create a context on `cuda_device`.  `cuda_stream` (a cudaStream_t of that
+ * device) is used for all work; NULL creates a context-owned non-blocking
+ * stream.  Returns MOREA_ECUDA if the device is unusable. */
+int morea_create(int cuda_device, void *cuda_stream, morea_ctx **out);
+void morea_destroy(morea_ctx *ctx);
+/* Message of the last failed call ("" if none).  Owned by the context. */
+const char *morea_last_error(const morea_ctx *ctx);
+/* The stream the context launches on (cudaStream_t as void*). */
+void *morea_stream(const morea_ctx *ctx);
+
+/* Load the two volumes and the contour guidance (one-off per problem).
+ *  nx,ny,nz >= 2, <= 768; spacing_mm[3] > 0 (physical voxel size; lengths,
+ *    distances, r and severities are in mm).
+ *  I_s, I_t: V = nx*ny*nz float32 each, finite, >= 0, background exactly 0
+ *    (h's zero/non-zero cases, L318-322; reading O6).
+ *  n_pairs K in [0, 8]: pairs <C_s, C_t>_i of contour point sets (L332-333).
+ *    cs_off/ct_off: K+1 int64 CSR offsets (non-decreasing, cs_off[0] = 0) into
+ *    cs_xyz/ct_xyz: float32 xyz triples in voxel units.  Weights per side are
+ *    |C_i| / |G_side| (L340).
+ *  r_mm: truncation radius of the guidance term (App. A.3); <= 0 means
+ *    0.025 * nx * spacing_mm[0] ("2.5% of the width of the image").
+ * Builds on the device, in fp64 and exactly reproducibly: the distance maps
+ * D_i^side(q) = min_c ||(q - c) * spacing|| (L793, brute force over all points,
+ * rounded once to fp32) and the narrow-band masks bit i = [D_i^side(q) < r].
+ * Synchronises the context stream. */
+int morea_load_images(morea_ctx *ctx, int nx, int ny, int nz, const double spacing_mm[3],
+                      const float *I_s, const float *I_t, int n_pairs, const int64_t *cs_off,
+                      const float *cs_xyz, const int64_t *ct_off, const float *ct_xyz,
+                      double r_mm);
+
+/* Set the dual-dynamic mesh topology and its base positions (L397).
+ *  base_xyz: N*3 float32 voxel units; tets: T*4 int32 point ids in [0, N);
+ *  c_delta: T float32 elasticity factors (L253) or NULL for 1.0;
+ *  spoke_mode: MOREA_SPOKE_FACE_CENTROID or MOREA_SPOKE_TET_CENTROID (O9).
+ * Reference signs are the exact signs of the base tets (App. A.4); a base
+ * point outside the Q.10 window or a zero-volume base tet is MOREA_EDOMAIN.
+ * Requires morea_load_images first.  Synchronises the context stream. */
+int morea_set_mesh(morea_ctx *ctx, int n_points, const float *base_xyz, int n_tets,
+                   const int32_t *tets, const float *c_delta, int spoke_mode);
+
+/* Full evaluation of `pop` solutions.
+ *  offsets: pop*N*6 float32, per point (src dx,dy,dz, tgt dx,dy,dz): the point
+ *    is at base + offset on each side (the genotype of L528, "transform-both"
+ *    L2003).
+ *  obj: pop*3 float64 (f_magnitude, f_intensity, f_guidance) or NULL;
+ *  acc: pop morea_acc or NULL;
+ *  tet_cache: NULL or pop*T*4 float64 receiving per-tet contributions
+ *    {h, g, n_samples, m} summed over both sides -- the "old" values a later
+ *    morea_eval_partial can reuse instead of recomputing them.
+ * Samples are the voxel centres owned by each tet on each side under the exact
+ * exactly-once rule (O3); a sample q of side s maps to x = T(q) by the tet's
+ * barycentric coordinates (O4) and contributes h(I_s(q), trilinear(I_t, x))
+ * (O5, O6) and, for each pair with D_i^s(q) < r, w_i (r - d)/r (d - D_i^t(x))^2
+ * (O8); symmetrically for side t. */
+int morea_eval_full(morea_ctx *ctx, int pop, const float *offsets, double *obj, morea_acc *acc,
+                    double *tet_cache);
+
+/* Partial (delta) evaluation of n_groups changed point sets per solution
+ * (O10).  For group g, S_g = changed_pts[grp_off[g] .. grp_off[g+1]) (point
+ * ids, no duplicates inside a group) and D_g = the tets incident to S_g.  The
+ * result for (solution k, group g) is
+ *     acc' = base_acc[k] - sum_{D_g} contrib(base) + sum_{D_g} contrib(new)
+ * where "new" replaces the offsets of S_g by
+ *     new_vals[(k*S + grp_off[g] + i)*6 + c],  S = grp_off[n_groups].
+ * Groups are independent (each delta is taken against the base alone), so
+ * groups may overlap; a colour class (disjoint D_g, L409-410) is the intended
+ * use.  grp_off / changed_pts are HOST arrays (the static FOS structure; the
+ * dependent-tet plan is built on the host and cached).  base_acc must be the
+ * accumulator of base_offsets (caller's contract).
+ *  tet_cache: NULL (old contributions are recomputed: 2x the work) or the
+ *    pop*T*4 array written by morea_eval_full for base_offsets (bitwise equal
+ *    results either way).
+ *  obj: pop*n_groups*3, acc: pop*n_groups (index k*n_groups + g), either NULL.
+ *  dep_cache_out: NULL or pop*ND*4 float64, ND = sum_g |D_g|: the new per-tet
+ *    contributions {h, g, n, m} in group order, tets ascending within a group
+ *    (see morea_partial_deps for the tet ids).
+ * flags' = (base flags & DOMAIN) | DOMAIN if a new point leaves the window |
+ * EMPTY if n_samples' == 0. */
+int morea_eval_partial(morea_ctx *ctx, int pop, const float *base_offsets,
+                       const morea_acc *base_acc, int n_groups, const int32_t *grp_off,
+                       const int32_t *changed_pts, const float *new_vals, const double *tet_cache,
+                       double *obj, morea_acc *acc, double *dep_cache_out);
+
+/* The dependent tets of the plan of the last morea_eval_partial call: writes
+ * up to `cap` tet ids (group order, ascending within a group) into `tets` (host)
+ * and the n_groups+1 offsets into `dep_off` (host).  Returns ND (>= 0). */
+int morea_partial_deps(morea_ctx *ctx, int cap, int32_t *tets, int32_t *dep_off);
+
+/* Fold check only (row a9): per solution the number of folded (tet, side) pairs
+ * and their summed severity (mm^3); tet_flags (NULL or pop*2*T uint8, index
+ * (k*2 + side)*T + t) gets 1 for a folded pair.  fold_count/severity may be
+ * NULL.  No voxel work. */
+int morea_check_folds(morea_ctx *ctx, int pop, const float *offsets, int32_t *fold_count,
+                      double *severity, uint8_t *tet_flags);
+
+/* Test hook (not on the hot path): owning tet of every voxel of one side for
+ * one solution, with the same rasterizer the evaluation uses.  owner: V int32,
+ * tet id, -1 = no owner, -2 = more than one owner.  offsets_one: N*6. */
+int morea_owner_map(morea_ctx *ctx, const float *offsets_one, int side, int32_t *owner);
+
+/* Test hook: the fp32 distance map D_pair^side (V floats) built by
+ * morea_load_images. */
+int morea_distance_map(morea_ctx *ctx, int side, int pair, float *out);
+
+/* Profiling of the evaluation kernel (bench.py): when enabled, every launch of
+ * the rasterize/evaluate kernel is bracketed by CUDA events on the context
+ * stream and its algorithmic work is counted.  morea_prof_read synchronises
+ * and returns: launches, summed kernel milliseconds, sampled voxels, band
+ * entries, tet-side items.  Reading resets the counters. */
+int morea_prof_enable(morea_ctx *ctx, int on);
+int morea_prof_read(morea_ctx *ctx, int64_t *launches, double *ms, int64_t *samples,
+                    int64_t *band_entries, int64_t *items);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOREA_H */

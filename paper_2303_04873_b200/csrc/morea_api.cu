@@ -1,0 +1,764 @@
+// morea_api.cu -- host side of the C-ABI declared in include/morea.h.
+//
+// Validation, Q.10 canonicalisation of the base mesh and reference signs
+// (App. A.4), incidence CSR and dependent-tet plans for partial
+// evaluation (§4.2.1), host/device pointer staging, stream handling
+// and kernel launches.  No arithmetic of the objectives happens here: every
+// step of an evaluation runs in morea_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "morea.h"
+#include "morea_internal.h"
+
+using namespace morea;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct Plan {
+  bool valid = false;
+  std::vector<int32_t> key_off, key_pts;
+  int G = 0, S = 0, n_entries = 0;
+  std::vector<int32_t> dep_tets, dep_off;  // canonical order
+  DevBuf entry_tet, entry_out, entry_slots, group_off, grp_off, changed;
+};
+
+}  // namespace
+
+struct morea_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int n_sm = 148, blocks_per_sm = 1;
+  // images
+  bool have_images = false;
+  int nx = 0, ny = 0, nz = 0, K = 0;
+  long long V = 0;
+  double sp[3] = {1, 1, 1};
+  double r = 0;
+  double w[2][kMaxPairs] = {};
+  DevBuf I[2], band[2], dmap[2], wts;
+  // mesh
+  bool have_mesh = false;
+  int N = 0, T = 0, spoke_mode = 0;
+  DevBuf base, tets, cdelta, ref;
+  std::vector<float> h_base;
+  std::vector<int32_t> h_tets, inc_off, inc;
+  std::vector<double> tet_size;
+  DevBuf full_entry_tet, full_entry_out, full_group_off;
+  // scratch
+  DevBuf rec, counter, stats;
+  DevBuf st_off, st_nv, st_cache_in, st_base_acc, st_obj, st_acc, st_cache_out, st_i32, st_f64,
+      st_u8;
+  Plan plan;
+  // profiling
+  bool prof = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+  long long prof_launches = 0;
+};
+
+namespace {
+
+int fail(morea_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CK(call)                                                                            \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      int code_ = (e_ == cudaErrorMemoryAllocation) ? MOREA_ENOMEM : MOREA_ECUDA;           \
+      return fail(ctx, code_, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,    \
+                  __LINE__);                                                                \
+    }                                                                                       \
+  } while (0)
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Device view of an input: the pointer itself if it is device memory,
+// otherwise an async copy into `st` (pageable sources are consumed before the
+// call returns, so the caller may reuse them immediately).
+cudaError_t in_dev(morea_ctx* ctx, const void* p, size_t bytes, DevBuf& st, const void** out) {
+  if (!p || bytes == 0) {
+    *out = p;
+    return cudaSuccess;
+  }
+  if (is_device_ptr(p)) {
+    *out = p;
+    return cudaSuccess;
+  }
+  cudaError_t e = st.ensure(bytes);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(st.p, p, bytes, cudaMemcpyHostToDevice, ctx->stream);
+  *out = st.p;
+  return e;
+}
+
+struct OutView {
+  void* user = nullptr;
+  void* dev = nullptr;
+  size_t bytes = 0;
+  bool copy = false;
+};
+
+cudaError_t out_dev(void* p, size_t bytes, DevBuf& st, OutView& v) {
+  v.user = p;
+  v.bytes = bytes;
+  v.copy = false;
+  v.dev = p;
+  if (!p || bytes == 0) return cudaSuccess;
+  if (is_device_ptr(p)) return cudaSuccess;
+  cudaError_t e = st.ensure(bytes);
+  if (e != cudaSuccess) return e;
+  v.dev = st.p;
+  v.copy = true;
+  return cudaSuccess;
+}
+
+// Copy staged outputs back and synchronise if any output was host memory.
+cudaError_t finish_outputs(morea_ctx* ctx, OutView* v, int n) {
+  bool any = false;
+  for (int i = 0; i < n; i++) {
+    if (!v[i].copy) continue;
+    cudaError_t e = cudaMemcpyAsync(v[i].user, v[i].dev, v[i].bytes, cudaMemcpyDeviceToHost,
+                                    ctx->stream);
+    if (e != cudaSuccess) return e;
+    any = true;
+  }
+  if (any) return cudaStreamSynchronize(ctx->stream);
+  return cudaSuccess;
+}
+
+// Host copy of a small array that may live on either side.
+template <class T>
+cudaError_t to_host(morea_ctx* ctx, const T* p, size_t n, std::vector<T>& out) {
+  out.resize(n);
+  if (n == 0) return cudaSuccess;
+  if (is_device_ptr(p)) {
+    cudaError_t e = cudaMemcpyAsync(out.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost,
+                                    ctx->stream);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(ctx->stream);
+  }
+  std::memcpy(out.data(), p, n * sizeof(T));
+  return cudaSuccess;
+}
+
+// O1 on the host, used only for the base mesh (reference signs / validation):
+// same fp64 operations as the device canon_q with a zero offset.
+long long canon_host(float b) { return (long long)std::nearbyint(1024.0 * (double)b + 1024.0 * 0.0); }
+
+__int128 det_host(const long long Q[4][3]) {
+  __int128 a[3], b[3], c[3];
+  for (int i = 0; i < 3; i++) {
+    a[i] = Q[1][i] - Q[0][i];
+    b[i] = Q[2][i] - Q[0][i];
+    c[i] = Q[3][i] - Q[0][i];
+  }
+  return a[0] * (b[1] * c[2] - b[2] * c[1]) - a[1] * (b[0] * c[2] - b[2] * c[0]) +
+         a[2] * (b[0] * c[1] - b[1] * c[0]);
+}
+
+Volumes volumes_of(const morea_ctx* c) {
+  Volumes v;
+  v.nx = c->nx; v.ny = c->ny; v.nz = c->nz; v.V = c->V;
+  for (int a = 0; a < 3; a++) v.sp[a] = c->sp[a];
+  for (int s = 0; s < 2; s++) {
+    v.I[s] = c->I[s].as<float>();
+    v.band[s] = c->K > 0 ? c->band[s].as<unsigned char>() : nullptr;
+    v.dmap[s] = c->K > 0 ? c->dmap[s].as<float>() : nullptr;
+  }
+  v.K = c->K;
+  v.r = c->r;
+  v.w = c->wts.as<double>();
+  return v;
+}
+
+MeshDev mesh_of(const morea_ctx* c) {
+  MeshDev m;
+  m.N = c->N; m.T = c->T;
+  m.base = c->base.as<float>();
+  m.tets = c->tets.as<int4>();
+  m.cdelta = c->cdelta.as<float>();
+  m.ref = c->ref.as<signed char>();
+  m.spoke_mode = c->spoke_mode;
+  return m;
+}
+
+int eval_grid(morea_ctx* ctx, long long n_items) {
+  long long g = (long long)ctx->n_sm * ctx->blocks_per_sm;
+  long long need = (n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  return (int)std::max<long long>(1, std::min(g, need));
+}
+
+cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
+  cudaError_t e = ctx->counter.ensure(sizeof(unsigned long long));
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream);
+  if (e != cudaSuccess) return e;
+  a.counter = ctx->counter.as<unsigned long long>();
+  a.stats = ctx->prof ? ctx->stats.as<unsigned long long>() : nullptr;
+  const long long n_items = (long long)a.n_entries * a.P;
+  if (n_items == 0) return cudaSuccess;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->prof) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, ctx->stream);
+  }
+  e = launch_eval(a, eval_grid(ctx, n_items), ctx->stream);
+  if (ctx->prof) {
+    cudaEventRecord(e1, ctx->stream);
+    ctx->evs.emplace_back(e0, e1);
+    ctx->prof_launches++;
+  }
+  return e;
+}
+
+// Build (or reuse) the dependent-tet plan of a partial request (host, O10).
+int build_plan(morea_ctx* ctx, int G, const int32_t* grp_off_in, const int32_t* changed_in) {
+  std::vector<int32_t> off, pts;
+  CK(to_host(ctx, grp_off_in, (size_t)G + 1, off));
+  if (off[0] != 0) return fail(ctx, MOREA_EINVAL, "grp_off[0] must be 0");
+  for (int g = 0; g < G; g++)
+    if (off[g + 1] < off[g]) return fail(ctx, MOREA_EINVAL, "grp_off must be non-decreasing");
+  const int S = off[G];
+  CK(to_host(ctx, changed_in, (size_t)S, pts));
+  Plan& P = ctx->plan;
+  if (P.valid && P.key_off == off && P.key_pts == pts) return MOREA_OK;
+  P.valid = false;
+  std::vector<int> stamp(ctx->N, -1), slot_of(ctx->N, -1), tstamp(ctx->T, -1);
+  std::vector<int32_t> dep_tets, dep_off(1, 0);
+  struct Ent { int tet, out; int4 slots; };
+  std::vector<Ent> ents;
+  for (int g = 0; g < G; g++) {
+    std::vector<int32_t> D;
+    for (int i = off[g]; i < off[g + 1]; i++) {
+      const int j = pts[i];
+      if (j < 0 || j >= ctx->N) return fail(ctx, MOREA_EINVAL, "changed point %d out of range", j);
+      if (stamp[j] == g) return fail(ctx, MOREA_EINVAL, "point %d twice in group %d", j, g);
+      stamp[j] = g;
+      slot_of[j] = i;
+      for (int u = ctx->inc_off[j]; u < ctx->inc_off[j + 1]; u++) {
+        const int t = ctx->inc[u];
+        if (tstamp[t] != g) {
+          tstamp[t] = g;
+          D.push_back(t);
+        }
+      }
+    }
+    std::sort(D.begin(), D.end());
+    for (int t : D) {
+      int s4[4];
+      for (int k = 0; k < 4; k++) {
+        const int j = ctx->h_tets[4 * t + k];
+        s4[k] = stamp[j] == g ? slot_of[j] : -1;
+      }
+      ents.push_back({t, (int)dep_tets.size(), make_int4(s4[0], s4[1], s4[2], s4[3])});
+      dep_tets.push_back(t);
+    }
+    dep_off.push_back((int32_t)dep_tets.size());
+  }
+  // schedule: largest tets first (stable), so the queue drains evenly
+  std::vector<int> order(ents.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return ctx->tet_size[ents[a].tet] > ctx->tet_size[ents[b].tet];
+  });
+  std::vector<int> et(ents.size()), eo(ents.size());
+  std::vector<int4> es(ents.size());
+  for (size_t i = 0; i < order.size(); i++) {
+    et[i] = ents[order[i]].tet;
+    eo[i] = ents[order[i]].out;
+    es[i] = ents[order[i]].slots;
+  }
+  const size_t ne = ents.size();
+  CK(P.entry_tet.ensure(ne * sizeof(int)));
+  CK(P.entry_out.ensure(ne * sizeof(int)));
+  CK(P.entry_slots.ensure(ne * sizeof(int4)));
+  CK(P.group_off.ensure((G + 1) * sizeof(int)));
+  CK(P.grp_off.ensure((G + 1) * sizeof(int)));
+  CK(P.changed.ensure(std::max(S, 1) * sizeof(int)));
+  if (ne) {
+    CK(cudaMemcpyAsync(P.entry_tet.p, et.data(), ne * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(P.entry_out.p, eo.data(), ne * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(P.entry_slots.p, es.data(), ne * sizeof(int4), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  CK(cudaMemcpyAsync(P.group_off.p, dep_off.data(), (G + 1) * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(P.grp_off.p, off.data(), (G + 1) * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  if (S) CK(cudaMemcpyAsync(P.changed.p, pts.data(), S * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  // the host vectors above are pageable: the copies have consumed them on return
+  CK(cudaStreamSynchronize(ctx->stream));
+  P.key_off = off;
+  P.key_pts = pts;
+  P.G = G;
+  P.S = S;
+  P.n_entries = (int)ne;
+  P.dep_tets = dep_tets;
+  P.dep_off = dep_off;
+  P.valid = true;
+  return MOREA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int morea_create(int cuda_device, void* cuda_stream, morea_ctx** out) {
+  if (!out) return MOREA_EINVAL;
+  *out = nullptr;
+  morea_ctx* ctx = new morea_ctx();
+  ctx->device = cuda_device;
+  cudaError_t e = cudaSetDevice(cuda_device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return MOREA_ECUDA;
+  }
+  if (cuda_stream) {
+    ctx->stream = (cudaStream_t)cuda_stream;
+  } else {
+    e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete ctx;
+      return MOREA_ECUDA;
+    }
+    ctx->own_stream = true;
+  }
+  cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, cuda_device);
+  ctx->blocks_per_sm = eval_blocks_per_sm();
+  if (ctx->stats.ensure(4 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMemset(ctx->stats.p, 0, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+    delete ctx;
+    return MOREA_ECUDA;
+  }
+  *out = ctx;
+  return MOREA_OK;
+}
+
+void morea_destroy(morea_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& p : ctx->evs) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
+                    &ctx->dmap[1], &ctx->wts, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
+                    &ctx->full_entry_tet, &ctx->full_entry_out, &ctx->full_group_off, &ctx->rec,
+                    &ctx->counter, &ctx->stats, &ctx->st_off, &ctx->st_nv, &ctx->st_cache_in,
+                    &ctx->st_base_acc, &ctx->st_obj, &ctx->st_acc, &ctx->st_cache_out,
+                    &ctx->st_i32, &ctx->st_f64, &ctx->st_u8, &ctx->plan.entry_tet,
+                    &ctx->plan.entry_out, &ctx->plan.entry_slots, &ctx->plan.group_off,
+                    &ctx->plan.grp_off, &ctx->plan.changed};
+  for (DevBuf* b : bufs) b->release();
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* morea_last_error(const morea_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void* morea_stream(const morea_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spacing_mm[3],
+                      const float* I_s, const float* I_t, int n_pairs, const int64_t* cs_off,
+                      const float* cs_xyz, const int64_t* ct_off, const float* ct_xyz,
+                      double r_mm) {
+  if (!ctx) return MOREA_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  if (nx < 2 || ny < 2 || nz < 2 || nx > 768 || ny > 768 || nz > 768)
+    return fail(ctx, MOREA_EINVAL, "dims must be in [2, 768], got %d x %d x %d", nx, ny, nz);
+  if (!spacing_mm || !I_s || !I_t) return fail(ctx, MOREA_EINVAL, "null spacing or volume");
+  std::vector<double> sp;
+  CK(to_host(ctx, spacing_mm, 3, sp));
+  for (int a = 0; a < 3; a++)
+    if (!(sp[a] > 0.0) || !std::isfinite(sp[a])) return fail(ctx, MOREA_EINVAL, "spacing must be > 0");
+  if (n_pairs < 0 || n_pairs > kMaxPairs)
+    return fail(ctx, MOREA_EINVAL, "n_pairs must be in [0, %d]", kMaxPairs);
+  ctx->have_images = false;
+  ctx->have_mesh = false;
+  ctx->plan.valid = false;
+  const long long V = (long long)nx * ny * nz;
+  ctx->nx = nx; ctx->ny = ny; ctx->nz = nz; ctx->V = V;
+  for (int a = 0; a < 3; a++) ctx->sp[a] = sp[a];
+  const float* Iin[2] = {I_s, I_t};
+  CK(ctx->st_i32.ensure(sizeof(int)));
+  CK(cudaMemsetAsync(ctx->st_i32.p, 0, sizeof(int), ctx->stream));
+  for (int s = 0; s < 2; s++) {
+    CK(ctx->I[s].ensure(V * sizeof(float)));
+    CK(cudaMemcpyAsync(ctx->I[s].p, Iin[s], V * sizeof(float), cudaMemcpyDefault, ctx->stream));
+    CK(launch_validate_volume(ctx->I[s].as<float>(), V, ctx->st_i32.as<int>(), ctx->stream));
+  }
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, ctx->st_i32.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (bad) return fail(ctx, MOREA_EINVAL, "intensities must be finite and >= 0");
+  // contours
+  const int K = n_pairs;
+  ctx->K = K;
+  ctx->r = r_mm > 0.0 ? r_mm : 0.025 * (double)nx * sp[0];  // App. A.3
+  const int64_t* offs[2] = {cs_off, ct_off};
+  const float* xyz[2] = {cs_xyz, ct_xyz};
+  std::memset(ctx->w, 0, sizeof(ctx->w));
+  for (int s = 0; s < 2 && K > 0; s++) {
+    std::vector<int64_t> off;
+    if (!offs[s]) return fail(ctx, MOREA_EINVAL, "null contour offsets");
+    CK(to_host(ctx, offs[s], (size_t)K + 1, off));
+    if (off[0] != 0) return fail(ctx, MOREA_EINVAL, "contour offsets must start at 0");
+    for (int i = 0; i < K; i++)
+      if (off[i + 1] < off[i]) return fail(ctx, MOREA_EINVAL, "contour offsets must be non-decreasing");
+    const int64_t M = off[K];
+    if (M > 0 && !xyz[s]) return fail(ctx, MOREA_EINVAL, "null contour points");
+    for (int i = 0; i < K; i++) ctx->w[s][i] = M > 0 ? (double)(off[i + 1] - off[i]) / (double)M : 0.0;
+    DevBuf pts, doff;
+    CK(pts.ensure(std::max<int64_t>(M, 1) * 3 * sizeof(float)));
+    CK(doff.ensure((K + 1) * sizeof(long long)));
+    if (M > 0) CK(cudaMemcpyAsync(pts.p, xyz[s], M * 3 * sizeof(float), cudaMemcpyDefault, ctx->stream));
+    CK(cudaMemcpyAsync(doff.p, off.data(), (K + 1) * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+    CK(ctx->dmap[s].ensure((size_t)K * V * sizeof(float)));
+    CK(ctx->band[s].ensure(V));
+    CK(launch_distance_maps(pts.as<float>(), doff.as<long long>(), K, nx, ny, nz, ctx->sp,
+                            ctx->dmap[s].as<float>(), ctx->stream));
+    CK(launch_band_mask(ctx->dmap[s].as<float>(), K, V, ctx->r, ctx->band[s].as<unsigned char>(),
+                        ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    pts.release();
+    doff.release();
+  }
+  CK(ctx->wts.ensure(sizeof(ctx->w)));
+  CK(cudaMemcpyAsync(ctx->wts.p, ctx->w, sizeof(ctx->w), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->have_images = true;
+  return MOREA_OK;
+}
+
+int morea_set_mesh(morea_ctx* ctx, int n_points, const float* base_xyz, int n_tets,
+                   const int32_t* tets, const float* c_delta, int spoke_mode) {
+  if (!ctx) return MOREA_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->have_images) return fail(ctx, MOREA_ESTATE, "morea_load_images must come first");
+  if (n_points < 4 || n_tets < 1 || !base_xyz || !tets)
+    return fail(ctx, MOREA_EINVAL, "need >= 4 points and >= 1 tet");
+  if (spoke_mode != MOREA_SPOKE_FACE_CENTROID && spoke_mode != MOREA_SPOKE_TET_CENTROID)
+    return fail(ctx, MOREA_EINVAL, "bad spoke_mode");
+  ctx->have_mesh = false;
+  ctx->plan.valid = false;
+  std::vector<float> b, cd;
+  std::vector<int32_t> t;
+  CK(to_host(ctx, base_xyz, (size_t)n_points * 3, b));
+  CK(to_host(ctx, tets, (size_t)n_tets * 4, t));
+  if (c_delta) {
+    CK(to_host(ctx, c_delta, (size_t)n_tets, cd));
+  } else {
+    cd.assign(n_tets, 1.0f);
+  }
+  for (int i = 0; i < 4 * n_tets; i++)
+    if (t[i] < 0 || t[i] >= n_points) return fail(ctx, MOREA_EINVAL, "tet index %d out of range", t[i]);
+  for (int i = 0; i < n_tets; i++)
+    if (!std::isfinite(cd[i])) return fail(ctx, MOREA_EINVAL, "c_delta must be finite");
+  std::vector<long long> Q((size_t)n_points * 3);
+  for (int j = 0; j < n_points; j++)
+    for (int a = 0; a < 3; a++) {
+      if (!std::isfinite(b[3 * j + a])) return fail(ctx, MOREA_EINVAL, "base point %d not finite", j);
+      Q[3 * j + a] = canon_host(b[3 * j + a]);
+      if (Q[3 * j + a] < kQLo || Q[3 * j + a] >= kQHi)
+        return fail(ctx, MOREA_EDOMAIN, "base point %d outside the Q.10 window", j);
+    }
+  std::vector<signed char> ref(n_tets);
+  std::vector<double> size(n_tets);
+  for (int i = 0; i < n_tets; i++) {
+    long long q[4][3];
+    for (int k = 0; k < 4; k++)
+      for (int a = 0; a < 3; a++) q[k][a] = Q[3 * t[4 * i + k] + a];
+    __int128 d = det_host(q);
+    if (d == 0) return fail(ctx, MOREA_EDOMAIN, "base tet %d has zero volume", i);
+    ref[i] = d > 0 ? 1 : -1;  // reference signs, App. A.4
+    size[i] = std::fabs((double)d);
+  }
+  // incidence CSR (tets incident to each point, ascending)
+  std::vector<int32_t> inc_off(n_points + 1, 0), inc;
+  for (int i = 0; i < n_tets; i++) {
+    int v[4] = {t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3]};
+    for (int k = 0; k < 4; k++) {
+      bool dup = false;
+      for (int l = 0; l < k; l++) dup = dup || v[l] == v[k];
+      if (!dup) inc_off[v[k] + 1]++;
+    }
+  }
+  for (int j = 0; j < n_points; j++) inc_off[j + 1] += inc_off[j];
+  inc.resize(inc_off[n_points]);
+  std::vector<int32_t> fill(inc_off.begin(), inc_off.end() - 1);
+  for (int i = 0; i < n_tets; i++) {
+    int v[4] = {t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3]};
+    for (int k = 0; k < 4; k++) {
+      bool dup = false;
+      for (int l = 0; l < k; l++) dup = dup || v[l] == v[k];
+      if (!dup) inc[fill[v[k]]++] = i;
+    }
+  }
+  ctx->N = n_points;
+  ctx->T = n_tets;
+  ctx->spoke_mode = spoke_mode;
+  ctx->h_base = b;
+  ctx->h_tets = t;
+  ctx->inc_off = inc_off;
+  ctx->inc = inc;
+  ctx->tet_size = size;
+  std::vector<int> order(n_tets), outs(n_tets);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int c) { return size[a] > size[c]; });
+  for (int i = 0; i < n_tets; i++) outs[i] = order[i];
+  const int goff[2] = {0, n_tets};
+  CK(ctx->base.ensure(b.size() * sizeof(float)));
+  CK(ctx->tets.ensure(t.size() * sizeof(int32_t)));
+  CK(ctx->cdelta.ensure(cd.size() * sizeof(float)));
+  CK(ctx->ref.ensure(ref.size()));
+  CK(ctx->full_entry_tet.ensure(n_tets * sizeof(int)));
+  CK(ctx->full_entry_out.ensure(n_tets * sizeof(int)));
+  CK(ctx->full_group_off.ensure(2 * sizeof(int)));
+  CK(cudaMemcpyAsync(ctx->base.p, b.data(), b.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->tets.p, t.data(), t.size() * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->cdelta.p, cd.data(), cd.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->ref.p, ref.data(), ref.size(), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->full_entry_tet.p, order.data(), n_tets * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->full_entry_out.p, outs.data(), n_tets * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->full_group_off.p, goff, 2 * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->have_mesh = true;
+  return MOREA_OK;
+}
+
+static int check_ready(morea_ctx* ctx) {
+  if (!ctx) return MOREA_EINVAL;
+  if (!ctx->have_images || !ctx->have_mesh)
+    return fail(ctx, MOREA_ESTATE, "load images and set the mesh before evaluating");
+  return MOREA_OK;
+}
+
+int morea_eval_full(morea_ctx* ctx, int pop, const float* offsets, double* obj, morea_acc* acc,
+                    double* tet_cache) {
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  if (pop < 0 || (pop > 0 && !offsets)) return fail(ctx, MOREA_EINVAL, "bad pop / offsets");
+  if (pop == 0) return MOREA_OK;
+  const int N = ctx->N, T = ctx->T;
+  const float* off = nullptr;
+  CK(in_dev(ctx, offsets, (size_t)pop * N * 6 * sizeof(float), ctx->st_off, (const void**)&off));
+  OutView ov[3];
+  CK(out_dev(obj, (size_t)pop * 3 * sizeof(double), ctx->st_obj, ov[0]));
+  CK(out_dev(acc, (size_t)pop * sizeof(morea_acc), ctx->st_acc, ov[1]));
+  CK(out_dev(tet_cache, (size_t)pop * T * 4 * sizeof(double), ctx->st_cache_out, ov[2]));
+  CK(ctx->rec.ensure((size_t)pop * T * sizeof(Rec)));
+  EvalArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.vol = volumes_of(ctx);
+  a.mesh = mesh_of(ctx);
+  a.P = pop;
+  a.offsets = off;
+  a.n_entries = T;
+  a.entry_tet = ctx->full_entry_tet.as<int>();
+  a.entry_out = ctx->full_entry_out.as<int>();
+  a.entry_slots = nullptr;
+  a.new_vals = nullptr;
+  a.S_total = 0;
+  a.partial = 0;
+  a.cache_in = nullptr;
+  a.cache_out = (double*)ov[2].dev;
+  a.rec = ctx->rec.as<Rec>();
+  a.n_out = T;
+  CK(run_eval(ctx, a));
+  CK(launch_reduce(pop, 1, T, ctx->full_group_off.as<int>(), ctx->rec.as<Rec>(), nullptr, 0, T, N,
+                   ctx->base.as<float>(), off, nullptr, nullptr, nullptr, 0, (double*)ov[0].dev,
+                   ov[1].dev, ctx->stream));
+  CK(finish_outputs(ctx, ov, 3));
+  return MOREA_OK;
+}
+
+int morea_eval_partial(morea_ctx* ctx, int pop, const float* base_offsets,
+                       const morea_acc* base_acc, int n_groups, const int32_t* grp_off,
+                       const int32_t* changed_pts, const float* new_vals, const double* tet_cache,
+                       double* obj, morea_acc* acc, double* dep_cache_out) {
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  if (pop < 0 || n_groups < 0 || !grp_off) return fail(ctx, MOREA_EINVAL, "bad pop / groups");
+  if (pop > 0 && (!base_offsets || !base_acc)) return fail(ctx, MOREA_EINVAL, "null base inputs");
+  rc = build_plan(ctx, n_groups, grp_off, changed_pts);
+  if (rc) return rc;
+  if (pop == 0 || n_groups == 0) return MOREA_OK;
+  const Plan& P = ctx->plan;
+  if (P.S > 0 && !new_vals) return fail(ctx, MOREA_EINVAL, "null new_vals");
+  const int N = ctx->N, T = ctx->T, G = n_groups;
+  const float *off = nullptr, *nv = nullptr;
+  const double* cin = nullptr;
+  const morea_acc* bacc = nullptr;
+  CK(in_dev(ctx, base_offsets, (size_t)pop * N * 6 * sizeof(float), ctx->st_off, (const void**)&off));
+  CK(in_dev(ctx, new_vals, (size_t)pop * P.S * 6 * sizeof(float), ctx->st_nv, (const void**)&nv));
+  CK(in_dev(ctx, tet_cache, (size_t)pop * T * 4 * sizeof(double), ctx->st_cache_in, (const void**)&cin));
+  CK(in_dev(ctx, base_acc, (size_t)pop * sizeof(morea_acc), ctx->st_base_acc, (const void**)&bacc));
+  OutView ov[3];
+  CK(out_dev(obj, (size_t)pop * G * 3 * sizeof(double), ctx->st_obj, ov[0]));
+  CK(out_dev(acc, (size_t)pop * G * sizeof(morea_acc), ctx->st_acc, ov[1]));
+  CK(out_dev(dep_cache_out, (size_t)pop * P.n_entries * 4 * sizeof(double), ctx->st_cache_out, ov[2]));
+  CK(ctx->rec.ensure((size_t)pop * std::max(P.n_entries, 1) * sizeof(Rec)));
+  EvalArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.vol = volumes_of(ctx);
+  a.mesh = mesh_of(ctx);
+  a.P = pop;
+  a.offsets = off;
+  a.n_entries = P.n_entries;
+  a.entry_tet = P.entry_tet.as<int>();
+  a.entry_out = P.entry_out.as<int>();
+  a.entry_slots = P.entry_slots.as<int4>();
+  a.new_vals = nv;
+  a.S_total = P.S;
+  a.partial = 1;
+  a.cache_in = cin;
+  a.cache_out = (double*)ov[2].dev;
+  a.rec = ctx->rec.as<Rec>();
+  a.n_out = P.n_entries;
+  CK(run_eval(ctx, a));
+  CK(launch_reduce(pop, G, P.n_entries, P.group_off.as<int>(), ctx->rec.as<Rec>(), bacc, 1, T, N,
+                   ctx->base.as<float>(), off, P.changed.as<int>(), P.grp_off.as<int>(), nv, P.S,
+                   (double*)ov[0].dev, ov[1].dev, ctx->stream));
+  CK(finish_outputs(ctx, ov, 3));
+  return MOREA_OK;
+}
+
+int morea_partial_deps(morea_ctx* ctx, int cap, int32_t* tets, int32_t* dep_off) {
+  if (!ctx) return MOREA_EINVAL;
+  if (!ctx->plan.valid) return fail(ctx, MOREA_ESTATE, "no partial plan yet");
+  const Plan& P = ctx->plan;
+  if (tets)
+    for (int i = 0; i < std::min<int>(cap, (int)P.dep_tets.size()); i++) tets[i] = P.dep_tets[i];
+  if (dep_off)
+    for (int g = 0; g <= P.G; g++) dep_off[g] = P.dep_off[g];
+  return (int)P.dep_tets.size();
+}
+
+int morea_check_folds(morea_ctx* ctx, int pop, const float* offsets, int32_t* fold_count,
+                      double* severity, uint8_t* tet_flags) {
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  if (pop < 0 || (pop > 0 && !offsets)) return fail(ctx, MOREA_EINVAL, "bad pop / offsets");
+  if (pop == 0) return MOREA_OK;
+  const float* off = nullptr;
+  CK(in_dev(ctx, offsets, (size_t)pop * ctx->N * 6 * sizeof(float), ctx->st_off, (const void**)&off));
+  OutView ov[3];
+  CK(out_dev(fold_count, (size_t)pop * sizeof(int32_t), ctx->st_i32, ov[0]));
+  CK(out_dev(severity, (size_t)pop * sizeof(double), ctx->st_f64, ov[1]));
+  CK(out_dev(tet_flags, (size_t)pop * 2 * ctx->T, ctx->st_u8, ov[2]));
+  CK(launch_check_folds(mesh_of(ctx), ctx->sp, pop, off, (int*)ov[0].dev, (double*)ov[1].dev,
+                        (unsigned char*)ov[2].dev, ctx->stream));
+  CK(finish_outputs(ctx, ov, 3));
+  return MOREA_OK;
+}
+
+int morea_owner_map(morea_ctx* ctx, const float* offsets_one, int side, int32_t* owner) {
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  if (!offsets_one || !owner || (side != 0 && side != 1)) return fail(ctx, MOREA_EINVAL, "bad args");
+  const float* off = nullptr;
+  CK(in_dev(ctx, offsets_one, (size_t)ctx->N * 6 * sizeof(float), ctx->st_off, (const void**)&off));
+  OutView ov[1];
+  CK(out_dev(owner, (size_t)ctx->V * sizeof(int32_t), ctx->st_i32, ov[0]));
+  CK(launch_owner_map(volumes_of(ctx), mesh_of(ctx), off, side, (int*)ov[0].dev, ctx->stream));
+  CK(finish_outputs(ctx, ov, 1));
+  return MOREA_OK;
+}
+
+int morea_distance_map(morea_ctx* ctx, int side, int pair, float* out) {
+  if (!ctx) return MOREA_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->have_images) return fail(ctx, MOREA_ESTATE, "no images");
+  if (side < 0 || side > 1 || pair < 0 || pair >= ctx->K || !out) return fail(ctx, MOREA_EINVAL, "bad args");
+  CK(cudaMemcpyAsync(out, ctx->dmap[side].as<float>() + (size_t)pair * ctx->V, ctx->V * sizeof(float),
+                     cudaMemcpyDefault, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MOREA_OK;
+}
+
+int morea_prof_enable(morea_ctx* ctx, int on) {
+  if (!ctx) return MOREA_EINVAL;
+  ctx->prof = on != 0;
+  return MOREA_OK;
+}
+
+int morea_prof_read(morea_ctx* ctx, int64_t* launches, double* ms, int64_t* samples,
+                    int64_t* band_entries, int64_t* items) {
+  if (!ctx) return MOREA_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double tot = 0.0;
+  for (auto& p : ctx->evs) {
+    float m = 0.f;
+    cudaEventElapsedTime(&m, p.first, p.second);
+    tot += m;
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  ctx->evs.clear();
+  unsigned long long st[4] = {0, 0, 0, 0};
+  CK(cudaMemcpy(st, ctx->stats.p, sizeof(st), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(ctx->stats.p, 0, sizeof(st)));
+  if (launches) *launches = ctx->prof_launches;
+  if (ms) *ms = tot;
+  if (samples) *samples = (int64_t)st[0];
+  if (band_entries) *band_entries = (int64_t)st[1];
+  if (items) *items = (int64_t)st[2];
+  ctx->prof_launches = 0;
+  return MOREA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,241 @@
+"""Thin Python binding of libmorea.so (include/morea.h).
+
+Argument marshalling only: every step of an evaluation runs in the sm_100a
+kernels behind the C-ABI.  Arrays may be torch tensors (CUDA or CPU) or numpy
+arrays; their data pointers are handed to the library, which detects host vs
+device memory itself.  There is no CPU fallback: if libmorea.so is missing the
+import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmorea.so")
+
+MOREA_OK = 0
+ERRORS = {-1: "EINVAL", -2: "ESTATE", -3: "EDOMAIN", -4: "ECUDA", -5: "ENOMEM"}
+F_DOMAIN = 1
+F_EMPTY = 2
+SPOKE_FACE_CENTROID = 0
+SPOKE_TET_CENTROID = 1
+
+ACC_DTYPE = np.dtype([("h_sum", "<f8"), ("g_sum", "<f8"), ("m_sum", "<f8"), ("severity", "<f8"),
+                      ("n_samples", "<i8"), ("folds", "<i4"), ("flags", "<i4")])
+assert ACC_DTYPE.itemsize == 48
+
+EXPORTS = ["morea_create", "morea_destroy", "morea_last_error", "morea_stream", "morea_load_images",
+           "morea_set_mesh", "morea_eval_full", "morea_eval_partial", "morea_partial_deps",
+           "morea_check_folds", "morea_owner_map", "morea_distance_map", "morea_prof_enable",
+           "morea_prof_read"]
+
+
+class MoreaError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"morea error {code} ({ERRORS.get(code, '?')}): {msg}")
+        self.code = code
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with "
+                          "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, f64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+    L.morea_create.argtypes = [i32, vp, ctypes.POINTER(vp)]
+    L.morea_destroy.argtypes = [vp]
+    L.morea_destroy.restype = None
+    L.morea_last_error.argtypes = [vp]
+    L.morea_last_error.restype = ctypes.c_char_p
+    L.morea_stream.argtypes = [vp]
+    L.morea_stream.restype = vp
+    L.morea_load_images.argtypes = [vp, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, f64]
+    L.morea_set_mesh.argtypes = [vp, i32, vp, i32, vp, vp, i32]
+    L.morea_eval_full.argtypes = [vp, i32, vp, vp, vp, vp]
+    L.morea_eval_partial.argtypes = [vp, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp]
+    L.morea_partial_deps.argtypes = [vp, i32, vp, vp]
+    L.morea_check_folds.argtypes = [vp, i32, vp, vp, vp, vp]
+    L.morea_owner_map.argtypes = [vp, vp, i32, vp]
+    L.morea_distance_map.argtypes = [vp, i32, i32, vp]
+    L.morea_prof_enable.argtypes = [vp, i32]
+    L.morea_prof_read.argtypes = [vp] + [ctypes.POINTER(i64), ctypes.POINTER(f64)] + \
+        [ctypes.POINTER(i64)] * 3
+    return L
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _ptr(a):
+    """Data pointer of a torch tensor / numpy array (None -> NULL).  Must be contiguous."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr()
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _np(a, dtype):
+    return np.ascontiguousarray(np.asarray(a), dtype=dtype)
+
+
+def _is_torch(a):
+    return hasattr(a, "data_ptr") and not isinstance(a, np.ndarray)
+
+
+class Context:
+    """One evaluator instance bound to one CUDA device (include/morea.h)."""
+
+    def __init__(self, device: int = 0, stream=None):
+        h = ctypes.c_void_p()
+        s = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        rc = _lib.morea_create(int(device), s, ctypes.byref(h))
+        if rc != MOREA_OK:
+            raise MoreaError(rc, "morea_create failed (no usable CUDA device?)")
+        self.h = h
+        self.device = device
+        self.N = self.T = self.V = self.K = 0
+        self.dims = None
+        self._last_G = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.morea_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, rc):
+        if rc != MOREA_OK:
+            raise MoreaError(rc, _lib.morea_last_error(self.h).decode())
+
+    @property
+    def stream_handle(self):
+        return _lib.morea_stream(self.h)
+
+    # ------------------------------------------------------------------ setup
+    def load_images(self, dims, spacing, I_s, I_t, cs_off, cs_xyz, ct_off, ct_xyz, r_mm=0.0):
+        nx, ny, nz = (int(d) for d in dims)
+        sp = _np(spacing, np.float64)
+        Is = I_s if _is_torch(I_s) else _np(I_s, np.float32)
+        It = I_t if _is_torch(I_t) else _np(I_t, np.float32)
+        cso, cto = _np(cs_off, np.int64), _np(ct_off, np.int64)
+        csx = cs_xyz if _is_torch(cs_xyz) else _np(cs_xyz, np.float32)
+        ctx_ = ct_xyz if _is_torch(ct_xyz) else _np(ct_xyz, np.float32)
+        K = len(cso) - 1
+        self._check(_lib.morea_load_images(self.h, nx, ny, nz, _ptr(sp), _ptr(Is), _ptr(It), K,
+                                           _ptr(cso), _ptr(csx), _ptr(cto), _ptr(ctx_),
+                                           float(r_mm)))
+        self.dims = (nx, ny, nz)
+        self.V = nx * ny * nz
+        self.K = K
+
+    def set_mesh(self, base, tets, c_delta=None, spoke_mode=SPOKE_FACE_CENTROID):
+        b = base if _is_torch(base) else _np(base, np.float32)
+        t = tets if _is_torch(tets) else _np(tets, np.int32)
+        c = None if c_delta is None else (c_delta if _is_torch(c_delta) else _np(c_delta, np.float32))
+        N = int(b.shape[0])
+        T = int(t.shape[0])
+        self._check(_lib.morea_set_mesh(self.h, N, _ptr(b), T, _ptr(t), _ptr(c), int(spoke_mode)))
+        self.N, self.T = N, T
+
+    @classmethod
+    def from_workload(cls, w, device=0, stream=None):
+        ctx = cls(device, stream)
+        ctx.load_images(w.dims, w.spacing, w.I_s, w.I_t, w.cs_off, w.cs_xyz, w.ct_off, w.ct_xyz,
+                        w.r_mm)
+        ctx.set_mesh(w.base, w.tets, w.c_delta)
+        return ctx
+
+    # ------------------------------------------------------------------ evaluation
+    def eval_full(self, offsets, obj=None, acc=None, tet_cache=None):
+        """offsets: (P, N, 6) float32 (device or host).  Outputs are written into
+        the given arrays (device or host); returns (obj, acc, tet_cache)."""
+        P = int(offsets.shape[0])
+        self._check(_lib.morea_eval_full(self.h, P, _ptr(offsets), _ptr(obj), _ptr(acc),
+                                         _ptr(tet_cache)))
+        return obj, acc, tet_cache
+
+    def eval_partial(self, base_offsets, base_acc, grp_off, changed, new_vals, tet_cache=None,
+                     obj=None, acc=None, dep_cache_out=None):
+        P = int(base_offsets.shape[0])
+        go = _np(grp_off, np.int32)
+        ch = _np(changed, np.int32)
+        G = len(go) - 1
+        self._last_G = G
+        self._check(_lib.morea_eval_partial(self.h, P, _ptr(base_offsets), _ptr(base_acc), G,
+                                            _ptr(go), _ptr(ch), _ptr(new_vals), _ptr(tet_cache),
+                                            _ptr(obj), _ptr(acc), _ptr(dep_cache_out)))
+        return obj, acc, dep_cache_out
+
+    def partial_deps(self):
+        n = _lib.morea_partial_deps(self.h, 0, None, None)
+        if n < 0:
+            self._check(n)
+        tets = np.zeros(max(n, 1), np.int32)
+        off = np.zeros(self._last_G + 1, np.int32)
+        _lib.morea_partial_deps(self.h, n, _ptr(tets), _ptr(off))
+        return tets[:n], off
+
+    def check_folds(self, offsets, fold_count=None, severity=None, tet_flags=None):
+        P = int(offsets.shape[0])
+        self._check(_lib.morea_check_folds(self.h, P, _ptr(offsets), _ptr(fold_count),
+                                           _ptr(severity), _ptr(tet_flags)))
+        return fold_count, severity, tet_flags
+
+    def owner_map(self, offsets_one, side, owner=None):
+        if owner is None:
+            owner = np.empty(self.V, np.int32)
+        o = offsets_one if _is_torch(offsets_one) else _np(offsets_one, np.float32)
+        self._check(_lib.morea_owner_map(self.h, _ptr(o), int(side), _ptr(owner)))
+        return owner
+
+    def distance_map(self, side, pair, out=None):
+        if out is None:
+            out = np.empty(self.V, np.float32)
+        self._check(_lib.morea_distance_map(self.h, int(side), int(pair), _ptr(out)))
+        return out
+
+    # ------------------------------------------------------------------ profiling
+    def prof_enable(self, on=True):
+        self._check(_lib.morea_prof_enable(self.h, 1 if on else 0))
+
+    def prof_read(self):
+        la, sa, ba, it = (ctypes.c_int64() for _ in range(4))
+        ms = ctypes.c_double()
+        self._check(_lib.morea_prof_read(self.h, ctypes.byref(la), ctypes.byref(ms),
+                                         ctypes.byref(sa), ctypes.byref(ba), ctypes.byref(it)))
+        return dict(launches=la.value, ms=ms.value, samples=sa.value, band_entries=ba.value,
+                    items=it.value)
+
+
+# ---------------------------------------------------------------------------- helpers
+def acc_to_numpy(acc):
+    """Decode an accumulator buffer (torch (P,6) int64 / uint8 bytes / numpy) to ACC_DTYPE."""
+    if _is_torch(acc):
+        acc = acc.detach().cpu().contiguous().numpy()
+    return np.ascontiguousarray(acc).view(np.uint8).reshape(-1).view(ACC_DTYPE)
+
+
+def empty_outputs(P, T=None, G=1, device="cuda", cache=False, torch=None):
+    """Device output buffers (torch) for P solutions x G groups."""
+    if torch is None:
+        import torch
+    obj = torch.empty((P * G, 3), dtype=torch.float64, device=device)
+    acc = torch.empty((P * G, 6), dtype=torch.int64, device=device)
+    tc = torch.empty((P, T, 4), dtype=torch.float64, device=device) if cache else None
+    return obj, acc, tc

@@ -522,7 +522,7 @@ def partial_request(w: Workload, plan, kind="class", class_index=0, seed=31, sig
     fixed6 = np.concatenate([w.fixed_axes, w.fixed_axes], axis=1)[changed]  # (S, 6)
     noise = rng.normal(size=(w.P, len(changed), 6)) * sigma
     new_vals = w.offsets[:, changed, :].astype(np.float64) + np.where(fixed6[None], 0.0, noise)
-    return grp_off, changed, new_vals.astype(np.float32)
+    return grp_off, changed, np.ascontiguousarray(new_vals, dtype=np.float32)
 
 
 def random_tiny_mesh(dims, n_inner, seed):
