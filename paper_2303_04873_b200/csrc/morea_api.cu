@@ -51,7 +51,7 @@ struct Plan {
   std::vector<int32_t> key_off, key_pts;
   int G = 0, S = 0, n_entries = 0;
   std::vector<int32_t> dep_tets, dep_off;  // canonical order
-  DevBuf entry_tet, entry_out, entry_slots, group_off, grp_off, changed;
+  DevBuf canon_tet, canon_slots, sched, group_off, grp_off, changed;
 };
 
 }  // namespace
@@ -77,9 +77,9 @@ struct morea_ctx {
   std::vector<float> h_base;
   std::vector<int32_t> h_tets, inc_off, inc;
   std::vector<double> tet_size;
-  DevBuf full_entry_tet, full_entry_out, full_group_off;
+  DevBuf full_sched, full_group_off;
   // scratch
-  DevBuf rec, counter, stats;
+  DevBuf geom, scal, hgn, counter, stats;
   DevBuf st_off, st_nv, st_cache_in, st_base_acc, st_obj, st_acc, st_cache_out, st_i32, st_f64,
       st_u8;
   Plan plan;
@@ -232,28 +232,49 @@ MeshDev mesh_of(const morea_ctx* c) {
   return m;
 }
 
-int eval_grid(morea_ctx* ctx, long long n_items) {
+int raster_grid(morea_ctx* ctx, long long n_items) {
   long long g = (long long)ctx->n_sm * ctx->blocks_per_sm;
   long long need = (n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
   return (int)std::max<long long>(1, std::min(g, need));
 }
 
-cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
-  cudaError_t e = ctx->counter.ensure(sizeof(unsigned long long));
+// Scratch for one evaluation: SideRec per rastered (version, entry, sol, side),
+// Scal per (version, entry, sol), HGN per rastered (version, entry, sol).
+cudaError_t eval_scratch(morea_ctx* ctx, EvalArgs& a) {
+  const size_t items = (size_t)a.n_entries * a.P;
+  cudaError_t e = ctx->geom.ensure(std::max<size_t>(1, items * a.n_raster_versions * 2) * sizeof(SideRec));
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream);
+  e = ctx->scal.ensure(std::max<size_t>(1, items * a.n_setup_versions) * sizeof(Scal));
+  if (e != cudaSuccess) return e;
+  e = ctx->hgn.ensure(std::max<size_t>(1, items * a.n_raster_versions) * sizeof(HGN));
+  if (e != cudaSuccess) return e;
+  a.geom = ctx->geom.as<SideRec>();
+  a.scal = ctx->scal.as<Scal>();
+  a.hgn = ctx->hgn.as<HGN>();
+  e = ctx->counter.ensure(sizeof(unsigned long long));
   if (e != cudaSuccess) return e;
   a.counter = ctx->counter.as<unsigned long long>();
   a.stats = ctx->prof ? ctx->stats.as<unsigned long long>() : nullptr;
-  const long long n_items = (long long)a.n_entries * a.P;
+  return cudaSuccess;
+}
+
+// k_setup -> k_raster (the dominant kernel; bracketed by events when profiling).
+cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
+  cudaError_t e = eval_scratch(ctx, a);
+  if (e != cudaSuccess) return e;
+  e = launch_setup(a, ctx->stream);
+  if (e != cudaSuccess) return e;
+  const long long n_items = (long long)a.n_entries * a.P * a.n_raster_versions;
   if (n_items == 0) return cudaSuccess;
+  e = cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream);
+  if (e != cudaSuccess) return e;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (ctx->prof) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, ctx->stream);
   }
-  e = launch_eval(a, eval_grid(ctx, n_items), ctx->stream);
+  e = launch_raster(a, raster_grid(ctx, n_items), ctx->stream);
   if (ctx->prof) {
     cudaEventRecord(e1, ctx->stream);
     ctx->evs.emplace_back(e0, e1);
@@ -276,7 +297,7 @@ int build_plan(morea_ctx* ctx, int G, const int32_t* grp_off_in, const int32_t* 
   P.valid = false;
   std::vector<int> stamp(ctx->N, -1), slot_of(ctx->N, -1), tstamp(ctx->T, -1);
   std::vector<int32_t> dep_tets, dep_off(1, 0);
-  struct Ent { int tet, out; int4 slots; };
+  struct Ent { int tet; int4 slots; };
   std::vector<Ent> ents;
   for (int g = 0; g < G; g++) {
     std::vector<int32_t> D;
@@ -301,35 +322,33 @@ int build_plan(morea_ctx* ctx, int G, const int32_t* grp_off_in, const int32_t* 
         const int j = ctx->h_tets[4 * t + k];
         s4[k] = stamp[j] == g ? slot_of[j] : -1;
       }
-      ents.push_back({t, (int)dep_tets.size(), make_int4(s4[0], s4[1], s4[2], s4[3])});
+      ents.push_back({t, make_int4(s4[0], s4[1], s4[2], s4[3])});
       dep_tets.push_back(t);
     }
     dep_off.push_back((int32_t)dep_tets.size());
   }
-  // schedule: largest tets first (stable), so the queue drains evenly
-  std::vector<int> order(ents.size());
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+  // canonical arrays + schedule (largest tets first, stable) so the queue drains evenly
+  const size_t ne = ents.size();
+  std::vector<int> ct(ne), sched(ne);
+  std::vector<int4> cs(ne);
+  for (size_t i = 0; i < ne; i++) {
+    ct[i] = ents[i].tet;
+    cs[i] = ents[i].slots;
+  }
+  std::iota(sched.begin(), sched.end(), 0);
+  std::stable_sort(sched.begin(), sched.end(), [&](int a, int b) {
     return ctx->tet_size[ents[a].tet] > ctx->tet_size[ents[b].tet];
   });
-  std::vector<int> et(ents.size()), eo(ents.size());
-  std::vector<int4> es(ents.size());
-  for (size_t i = 0; i < order.size(); i++) {
-    et[i] = ents[order[i]].tet;
-    eo[i] = ents[order[i]].out;
-    es[i] = ents[order[i]].slots;
-  }
-  const size_t ne = ents.size();
-  CK(P.entry_tet.ensure(ne * sizeof(int)));
-  CK(P.entry_out.ensure(ne * sizeof(int)));
-  CK(P.entry_slots.ensure(ne * sizeof(int4)));
+  CK(P.canon_tet.ensure(std::max<size_t>(ne, 1) * sizeof(int)));
+  CK(P.canon_slots.ensure(std::max<size_t>(ne, 1) * sizeof(int4)));
+  CK(P.sched.ensure(std::max<size_t>(ne, 1) * sizeof(int)));
   CK(P.group_off.ensure((G + 1) * sizeof(int)));
   CK(P.grp_off.ensure((G + 1) * sizeof(int)));
   CK(P.changed.ensure(std::max(S, 1) * sizeof(int)));
   if (ne) {
-    CK(cudaMemcpyAsync(P.entry_tet.p, et.data(), ne * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(P.entry_out.p, eo.data(), ne * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(P.entry_slots.p, es.data(), ne * sizeof(int4), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(P.canon_tet.p, ct.data(), ne * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(P.canon_slots.p, cs.data(), ne * sizeof(int4), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(P.sched.p, sched.data(), ne * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   }
   CK(cudaMemcpyAsync(P.group_off.p, dep_off.data(), (G + 1) * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(P.grp_off.p, off.data(), (G + 1) * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
@@ -372,7 +391,7 @@ int morea_create(int cuda_device, void* cuda_stream, morea_ctx** out) {
     ctx->own_stream = true;
   }
   cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, cuda_device);
-  ctx->blocks_per_sm = eval_blocks_per_sm();
+  ctx->blocks_per_sm = raster_blocks_per_sm();
   if (ctx->stats.ensure(4 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemset(ctx->stats.p, 0, 4 * sizeof(unsigned long long)) != cudaSuccess) {
     delete ctx;
@@ -392,11 +411,11 @@ void morea_destroy(morea_ctx* ctx) {
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
                     &ctx->dmap[1], &ctx->wts, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
-                    &ctx->full_entry_tet, &ctx->full_entry_out, &ctx->full_group_off, &ctx->rec,
+                    &ctx->full_sched, &ctx->full_group_off, &ctx->geom, &ctx->scal, &ctx->hgn,
                     &ctx->counter, &ctx->stats, &ctx->st_off, &ctx->st_nv, &ctx->st_cache_in,
                     &ctx->st_base_acc, &ctx->st_obj, &ctx->st_acc, &ctx->st_cache_out,
-                    &ctx->st_i32, &ctx->st_f64, &ctx->st_u8, &ctx->plan.entry_tet,
-                    &ctx->plan.entry_out, &ctx->plan.entry_slots, &ctx->plan.group_off,
+                    &ctx->st_i32, &ctx->st_f64, &ctx->st_u8, &ctx->plan.canon_tet,
+                    &ctx->plan.canon_slots, &ctx->plan.sched, &ctx->plan.group_off,
                     &ctx->plan.grp_off, &ctx->plan.changed};
   for (DevBuf* b : bufs) b->release();
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -551,24 +570,21 @@ int morea_set_mesh(morea_ctx* ctx, int n_points, const float* base_xyz, int n_te
   ctx->inc_off = inc_off;
   ctx->inc = inc;
   ctx->tet_size = size;
-  std::vector<int> order(n_tets), outs(n_tets);
+  std::vector<int> order(n_tets);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int a, int c) { return size[a] > size[c]; });
-  for (int i = 0; i < n_tets; i++) outs[i] = order[i];
   const int goff[2] = {0, n_tets};
   CK(ctx->base.ensure(b.size() * sizeof(float)));
   CK(ctx->tets.ensure(t.size() * sizeof(int32_t)));
   CK(ctx->cdelta.ensure(cd.size() * sizeof(float)));
   CK(ctx->ref.ensure(ref.size()));
-  CK(ctx->full_entry_tet.ensure(n_tets * sizeof(int)));
-  CK(ctx->full_entry_out.ensure(n_tets * sizeof(int)));
+  CK(ctx->full_sched.ensure(n_tets * sizeof(int)));
   CK(ctx->full_group_off.ensure(2 * sizeof(int)));
   CK(cudaMemcpyAsync(ctx->base.p, b.data(), b.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->tets.p, t.data(), t.size() * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->cdelta.p, cd.data(), cd.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->ref.p, ref.data(), ref.size(), cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->full_entry_tet.p, order.data(), n_tets * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->full_entry_out.p, outs.data(), n_tets * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->full_sched.p, order.data(), n_tets * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->full_group_off.p, goff, 2 * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->have_mesh = true;
@@ -596,7 +612,6 @@ int morea_eval_full(morea_ctx* ctx, int pop, const float* offsets, double* obj, 
   CK(out_dev(obj, (size_t)pop * 3 * sizeof(double), ctx->st_obj, ov[0]));
   CK(out_dev(acc, (size_t)pop * sizeof(morea_acc), ctx->st_acc, ov[1]));
   CK(out_dev(tet_cache, (size_t)pop * T * 4 * sizeof(double), ctx->st_cache_out, ov[2]));
-  CK(ctx->rec.ensure((size_t)pop * T * sizeof(Rec)));
   EvalArgs a;
   std::memset(&a, 0, sizeof(a));
   a.vol = volumes_of(ctx);
@@ -604,20 +619,15 @@ int morea_eval_full(morea_ctx* ctx, int pop, const float* offsets, double* obj, 
   a.P = pop;
   a.offsets = off;
   a.n_entries = T;
-  a.entry_tet = ctx->full_entry_tet.as<int>();
-  a.entry_out = ctx->full_entry_out.as<int>();
-  a.entry_slots = nullptr;
-  a.new_vals = nullptr;
-  a.S_total = 0;
+  a.canon_tet = nullptr;
+  a.canon_slots = nullptr;
+  a.sched = ctx->full_sched.as<int>();
   a.partial = 0;
-  a.cache_in = nullptr;
-  a.cache_out = (double*)ov[2].dev;
-  a.rec = ctx->rec.as<Rec>();
-  a.n_out = T;
+  a.n_setup_versions = 1;
+  a.n_raster_versions = 1;
   CK(run_eval(ctx, a));
-  CK(launch_reduce(pop, 1, T, ctx->full_group_off.as<int>(), ctx->rec.as<Rec>(), nullptr, 0, T, N,
-                   ctx->base.as<float>(), off, nullptr, nullptr, nullptr, 0, (double*)ov[0].dev,
-                   ov[1].dev, ctx->stream));
+  CK(launch_reduce(a, 1, ctx->full_group_off.as<int>(), nullptr, nullptr, (double*)ov[2].dev,
+                   nullptr, nullptr, (double*)ov[0].dev, ov[1].dev, ctx->stream));
   CK(finish_outputs(ctx, ov, 3));
   return MOREA_OK;
 }
@@ -648,7 +658,6 @@ int morea_eval_partial(morea_ctx* ctx, int pop, const float* base_offsets,
   CK(out_dev(obj, (size_t)pop * G * 3 * sizeof(double), ctx->st_obj, ov[0]));
   CK(out_dev(acc, (size_t)pop * G * sizeof(morea_acc), ctx->st_acc, ov[1]));
   CK(out_dev(dep_cache_out, (size_t)pop * P.n_entries * 4 * sizeof(double), ctx->st_cache_out, ov[2]));
-  CK(ctx->rec.ensure((size_t)pop * std::max(P.n_entries, 1) * sizeof(Rec)));
   EvalArgs a;
   std::memset(&a, 0, sizeof(a));
   a.vol = volumes_of(ctx);
@@ -656,20 +665,17 @@ int morea_eval_partial(morea_ctx* ctx, int pop, const float* base_offsets,
   a.P = pop;
   a.offsets = off;
   a.n_entries = P.n_entries;
-  a.entry_tet = P.entry_tet.as<int>();
-  a.entry_out = P.entry_out.as<int>();
-  a.entry_slots = P.entry_slots.as<int4>();
+  a.canon_tet = P.canon_tet.as<int>();
+  a.canon_slots = P.canon_slots.as<int4>();
+  a.sched = P.sched.as<int>();
   a.new_vals = nv;
   a.S_total = P.S;
   a.partial = 1;
-  a.cache_in = cin;
-  a.cache_out = (double*)ov[2].dev;
-  a.rec = ctx->rec.as<Rec>();
-  a.n_out = P.n_entries;
+  a.n_setup_versions = 2;
+  a.n_raster_versions = cin ? 1 : 2;
   CK(run_eval(ctx, a));
-  CK(launch_reduce(pop, G, P.n_entries, P.group_off.as<int>(), ctx->rec.as<Rec>(), bacc, 1, T, N,
-                   ctx->base.as<float>(), off, P.changed.as<int>(), P.grp_off.as<int>(), nv, P.S,
-                   (double*)ov[0].dev, ov[1].dev, ctx->stream));
+  CK(launch_reduce(a, G, P.group_off.as<int>(), bacc, cin, (double*)ov[2].dev, P.changed.as<int>(),
+                   P.grp_off.as<int>(), (double*)ov[0].dev, ov[1].dev, ctx->stream));
   CK(finish_outputs(ctx, ov, 3));
   return MOREA_OK;
 }
@@ -713,7 +719,18 @@ int morea_owner_map(morea_ctx* ctx, const float* offsets_one, int side, int32_t*
   CK(in_dev(ctx, offsets_one, (size_t)ctx->N * 6 * sizeof(float), ctx->st_off, (const void**)&off));
   OutView ov[1];
   CK(out_dev(owner, (size_t)ctx->V * sizeof(int32_t), ctx->st_i32, ov[0]));
-  CK(launch_owner_map(volumes_of(ctx), mesh_of(ctx), off, side, (int*)ov[0].dev, ctx->stream));
+  EvalArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.vol = volumes_of(ctx);
+  a.mesh = mesh_of(ctx);
+  a.P = 1;
+  a.offsets = off;
+  a.n_entries = ctx->T;
+  a.sched = ctx->full_sched.as<int>();
+  a.n_setup_versions = 1;
+  a.n_raster_versions = 1;
+  CK(eval_scratch(ctx, a));
+  CK(launch_owner_map(a, side, (int*)ov[0].dev, ctx->stream));
   CK(finish_outputs(ctx, ov, 1));
   return MOREA_OK;
 }

@@ -1,6 +1,6 @@
 // Internal declarations shared by the host API (morea_api.cu) and the kernels
-// (morea_kernels.cu).  Product code only -- nothing here is shared with the
-// oracle under oracle/.
+// (morea_kernels.cu).  Product code only; nothing here is shared with the
+// independent CPU checker.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -11,15 +11,40 @@ constexpr int kMaxPairs = 8;
 constexpr int kQLo = -256 * 1024;  // Q.10 window (O1)
 constexpr int kQHi = 768 * 1024;
 constexpr int kWarpsPerBlock = 8;
-constexpr int kEvalThreads = 32 * kWarpsPerBlock;
+constexpr int kRasterThreads = 32 * kWarpsPerBlock;
 
-// Per (solution, entry) record written by the evaluation kernel.
-struct Rec {
-  double h, g, m, sev;
-  long long n;
-  int folds, flags;  // flags bit 0: a vertex outside the window (domain)
+// Geometry of one (version, entry, solution, side) item, written by k_setup and
+// read by k_raster.  448 bytes, 16-byte aligned.
+struct __align__(16) SideRec {
+  double fa[4], fb[4], fc[4];  // face crossing x*(y,z) = fa + fb (y - lo_y) + fc (z - lo_z)
+  long long nrm[4][3];         // exact inward normals (|n| < 2^41)
+  long long cst[4];            // e_k(q) = 1024 n_k . q - cst_k  (exact)
+  double A[3][3];              // displacement gradient du_a / dq_b
+  double d0[3];                // displacement at lo
+  long long absdet;            // |Delta|
+  float fthr[4];               // fp64 crossing error bound (voxels)
+  float eps[3];                // fp32 position filter bound per axis (0 = exact axis)
+  int flags;                   // bit 0: rasterize; bit 1: fast path (no clamp, no exact axis)
+  int ftype[4];                // +-1: lower/upper bound face (n_x >< 0), 0: flat, +-2: slow exact
+  int lo[3], hi[3];            // lattice bbox clipped to the image
+  int U[4][3];                 // Q_other - Q_own per vertex
 };
-static_assert(sizeof(Rec) == 48, "Rec layout");
+static_assert(sizeof(SideRec) == 448, "SideRec layout");
+
+// Per-tet scalar terms of one (version, entry, solution).
+struct Scal {
+  double m, sev;
+  int folds, flags;  // flags bit 0: a vertex outside the Q.10 window
+  int pad[2];
+};
+static_assert(sizeof(Scal) == 32, "Scal layout");
+
+// Sample sums of one (version, entry, solution), both sides.
+struct HGN {
+  double h, g;
+  long long n, nb;
+};
+static_assert(sizeof(HGN) == 32, "HGN layout");
 
 struct Volumes {
   int nx, ny, nz;
@@ -42,22 +67,26 @@ struct MeshDev {
   int spoke_mode;
 };
 
+// One evaluation launch sequence: k_setup -> k_raster -> k_reduce.
+// Item index space: (version, canonical entry, solution); version 0 = the new
+// (evaluated) geometry, version 1 = the base geometry of a partial evaluation.
 struct EvalArgs {
   Volumes vol;
   MeshDev mesh;
   int P;
-  const float* offsets;  // P*N*6
+  const float* offsets;      // P*N*6
   int n_entries;
-  const int* entry_tet;      // schedule order (large tets first)
-  const int* entry_out;      // canonical output index of the entry
-  const int4* entry_slots;   // partial: per vertex slot into new_vals' S dim, or -1
+  const int* canon_tet;      // canonical entry -> tet (nullptr: identity, full evaluation)
+  const int4* canon_slots;   // canonical entry -> per vertex slot into new_vals, or -1
+  const int* sched;          // queue position -> canonical entry (large tets first)
   const float* new_vals;     // P*S_total*6
   int S_total;
   int partial;
-  const double* cache_in;    // partial: P*T*4 old {h,g,n,m} or nullptr
-  double* cache_out;         // full: P*T*4 by tet id; partial: P*n_out*4 by out index
-  Rec* rec;                  // P*n_out
-  int n_out;
+  int n_setup_versions;      // 1 (full) or 2 (partial)
+  int n_raster_versions;     // 1, or 2 when a partial evaluation recomputes the base
+  SideRec* geom;             // [version][entry][sol][side]
+  Scal* scal;                // [version][entry][sol]
+  HGN* hgn;                  // [version][entry][sol]
   unsigned long long* counter;  // work queue head (zeroed before launch)
   unsigned long long* stats;    // [samples, band entries, items]
 };
@@ -68,16 +97,14 @@ cudaError_t launch_distance_maps(const float* pts, const long long* off, int K, 
                                  int nz, const double sp[3], float* dmap, cudaStream_t s);
 cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, unsigned char* band,
                              cudaStream_t s);
-cudaError_t launch_eval(const EvalArgs& a, int grid, cudaStream_t s);
-int eval_blocks_per_sm();
-cudaError_t launch_reduce(int P, int G, int n_out, const int* group_off, const Rec* rec,
-                          const void* base_acc, int partial, int T, int N, const float* base,
-                          const float* offsets, const int* changed, const int* grp_off,
-                          const float* new_vals, int S_total, double* obj, void* acc,
-                          cudaStream_t s);
+cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s);
+cudaError_t launch_raster(const EvalArgs& a, int grid, cudaStream_t s);
+int raster_blocks_per_sm();
+cudaError_t launch_reduce(const EvalArgs& a, int G, const int* group_off, const void* base_acc,
+                          const double* cache_in, double* cache_out, const int* changed,
+                          const int* grp_off, double* obj, void* acc, cudaStream_t s);
 cudaError_t launch_check_folds(const MeshDev& m, const double sp[3], int P, const float* offsets,
                                int* count, double* sev, unsigned char* flags, cudaStream_t s);
-cudaError_t launch_owner_map(const Volumes& v, const MeshDev& m, const float* offsets_one,
-                             int side, int* owner, cudaStream_t s);
+cudaError_t launch_owner_map(const EvalArgs& a, int side, int* owner, cudaStream_t s);
 
 }  // namespace morea

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmorea.so")
+LIB_PATH = os.environ.get("MOREA_LIB") or os.path.join(_HERE, "libmorea.so")
 
 MOREA_OK = 0
 ERRORS = {-1: "EINVAL", -2: "ESTATE", -3: "EDOMAIN", -4: "ECUDA", -5: "ENOMEM"}
