@@ -183,6 +183,8 @@ int morea_distance_map(morea_ctx *ctx, int side, int pair, float *out);
  * and returns: launches, summed kernel milliseconds, sampled voxels, band
  * entries, tet-side items.  Reading resets the counters. */
 int morea_prof_enable(morea_ctx *ctx, int on);
+/* Number of kernels this context has launched since it was created. */
+int64_t morea_kernel_launches(const morea_ctx *ctx);
 int morea_prof_read(morea_ctx *ctx, int64_t *launches, double *ms, int64_t *samples,
                     int64_t *band_entries, int64_t *items);
 

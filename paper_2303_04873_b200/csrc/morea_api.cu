@@ -87,6 +87,7 @@ struct morea_ctx {
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
   long long prof_launches = 0;
+  long long kernels = 0;  // every kernel launch of this context
 };
 
 namespace {
@@ -263,6 +264,7 @@ cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
   cudaError_t e = eval_scratch(ctx, a);
   if (e != cudaSuccess) return e;
   e = launch_setup(a, ctx->stream);
+  ctx->kernels++;
   if (e != cudaSuccess) return e;
   const long long n_items = (long long)a.n_entries * a.P * a.n_raster_versions;
   if (n_items == 0) return cudaSuccess;
@@ -275,6 +277,7 @@ cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
     cudaEventRecord(e0, ctx->stream);
   }
   e = launch_raster(a, raster_grid(ctx, n_items), ctx->stream);
+  ctx->kernels++;
   if (ctx->prof) {
     cudaEventRecord(e1, ctx->stream);
     ctx->evs.emplace_back(e0, e1);
@@ -628,6 +631,7 @@ int morea_eval_full(morea_ctx* ctx, int pop, const float* offsets, double* obj, 
   CK(run_eval(ctx, a));
   CK(launch_reduce(a, 1, ctx->full_group_off.as<int>(), nullptr, nullptr, (double*)ov[2].dev,
                    nullptr, nullptr, (double*)ov[0].dev, ov[1].dev, ctx->stream));
+  ctx->kernels++;
   CK(finish_outputs(ctx, ov, 3));
   return MOREA_OK;
 }
@@ -676,6 +680,7 @@ int morea_eval_partial(morea_ctx* ctx, int pop, const float* base_offsets,
   CK(run_eval(ctx, a));
   CK(launch_reduce(a, G, P.group_off.as<int>(), bacc, cin, (double*)ov[2].dev, P.changed.as<int>(),
                    P.grp_off.as<int>(), (double*)ov[0].dev, ov[1].dev, ctx->stream));
+  ctx->kernels++;
   CK(finish_outputs(ctx, ov, 3));
   return MOREA_OK;
 }
@@ -706,6 +711,7 @@ int morea_check_folds(morea_ctx* ctx, int pop, const float* offsets, int32_t* fo
   CK(out_dev(tet_flags, (size_t)pop * 2 * ctx->T, ctx->st_u8, ov[2]));
   CK(launch_check_folds(mesh_of(ctx), ctx->sp, pop, off, (int*)ov[0].dev, (double*)ov[1].dev,
                         (unsigned char*)ov[2].dev, ctx->stream));
+  ctx->kernels++;
   CK(finish_outputs(ctx, ov, 3));
   return MOREA_OK;
 }
@@ -731,6 +737,7 @@ int morea_owner_map(morea_ctx* ctx, const float* offsets_one, int side, int32_t*
   a.n_raster_versions = 1;
   CK(eval_scratch(ctx, a));
   CK(launch_owner_map(a, side, (int*)ov[0].dev, ctx->stream));
+  ctx->kernels += 3;
   CK(finish_outputs(ctx, ov, 1));
   return MOREA_OK;
 }
@@ -745,6 +752,8 @@ int morea_distance_map(morea_ctx* ctx, int side, int pair, float* out) {
   CK(cudaStreamSynchronize(ctx->stream));
   return MOREA_OK;
 }
+
+int64_t morea_kernel_launches(const morea_ctx* ctx) { return ctx ? ctx->kernels : -1; }
 
 int morea_prof_enable(morea_ctx* ctx, int on) {
   if (!ctx) return MOREA_EINVAL;

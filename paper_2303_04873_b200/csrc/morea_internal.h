@@ -14,22 +14,25 @@ constexpr int kWarpsPerBlock = 8;
 constexpr int kRasterThreads = 32 * kWarpsPerBlock;
 
 // Geometry of one (version, entry, solution, side) item, written by k_setup and
-// read by k_raster.  448 bytes, 16-byte aligned.
+// read by k_raster.  384 bytes, 16-byte aligned.  The fp32 fields
+// are roundings of exact (or fp64) values; each comes with an error bound so the
+// rasterizer can detect when only the exact integer fields can decide.
 struct __align__(16) SideRec {
-  double fa[4], fb[4], fc[4];  // face crossing x*(y,z) = fa + fb (y - lo_y) + fc (z - lo_z)
-  long long nrm[4][3];         // exact inward normals (|n| < 2^41)
-  long long cst[4];            // e_k(q) = 1024 n_k . q - cst_k  (exact)
-  double A[3][3];              // displacement gradient du_a / dq_b
-  double d0[3];                // displacement at lo
-  long long absdet;            // |Delta|
-  float fthr[4];               // fp64 crossing error bound (voxels)
-  float eps[3];                // fp32 position filter bound per axis (0 = exact axis)
-  int flags;                   // bit 0: rasterize; bit 1: fast path (no clamp, no exact axis)
-  int ftype[4];                // +-1: lower/upper bound face (n_x >< 0), 0: flat, +-2: slow exact
-  int lo[3], hi[3];            // lattice bbox clipped to the image
-  int U[4][3];                 // Q_other - Q_own per vertex
+  float fa[4], fb[4], fc[4];  // face crossing x*(y,z) = fa + fb (y - lo_y) + fc (z - lo_z)
+  float fthr[4];              // bound on the fp32 crossing error (voxels)
+  int ftype[4];               // +-1: lower/upper bound face (n_x >< 0), 0: flat, +-2: exact search
+  long long nrm[4][3];        // exact inward normals (|n| < 2^41)
+  long long cst[4];           // e_k(q) = 1024 n_k . q - cst_k  (exact)
+  float A[3][3];              // displacement gradient du_a / dq_b
+  float d0[3];                // displacement at lo
+  float eps[3];               // fp32 position filter bound per axis (0 = exact axis)
+  int flags;                  // bit 0: rasterize; bit 1: no exact axis
+  float vy[4], vz[4];         // vertex y, z (voxel units, exact) for per-slice y ranges
+  int lo[3], hi[3];           // lattice bbox clipped to the image
+  int U[4][3];                // Q_other - Q_own per vertex
+  long long absdet;           // |Delta|
 };
-static_assert(sizeof(SideRec) == 448, "SideRec layout");
+static_assert(sizeof(SideRec) == 384, "SideRec layout");
 
 // Per-tet scalar terms of one (version, entry, solution).
 struct Scal {

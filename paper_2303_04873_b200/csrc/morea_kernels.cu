@@ -103,8 +103,11 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
     G.hi[a] = min(floordiv1024(mx), dims[a] - 1);
     if (G.lo[a] > G.hi[a]) return;  // no lattice point of the image inside
   }
+  const double Ly = (double)(G.hi[1] - G.lo[1]), Lz = (double)(G.hi[2] - G.lo[2]);
 #pragma unroll
   for (int k = 0; k < 4; k++) {
+    G.vy[k] = (float)Q[k][1] * (1.0f / 1024.0f);  // exact: |Q| < 2^20
+    G.vz[k] = (float)Q[k][2] * (1.0f / 1024.0f);
     const int f0 = (k == 0) ? 1 : 0;
     const int f1 = (k <= 1) ? 2 : 1;
     const int f2 = (k <= 2) ? 3 : 2;
@@ -117,76 +120,71 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
     G.cst[k] = n0 * (i64)Q[f0][0] + n1 * (i64)Q[f0][1] + n2 * (i64)Q[f0][2];
 #pragma unroll
     for (int a = 0; a < 3; a++) G.U[k][a] = Qo[k][a] - Q[k][a];
-    // row crossing x*(y, z): 1024 (n0 x + n1 y + n2 z) = cst
+    // row crossing x*(y, z): 1024 (n0 x + n1 y + n2 z) = cst, evaluated in fp32 per row
     if (n0 != 0) {
-      G.ftype[k] = n0 > 0 ? 1 : -1;
       const i128 num = (i128)G.cst[k] - (i128)1024 * ((i128)n1 * G.lo[1] + (i128)n2 * G.lo[2]);
-      G.fa[k] = (double)num / (1024.0 * (double)n0);
-      G.fb[k] = -(double)n1 / (double)n0;
-      G.fc[k] = -(double)n2 / (double)n0;
-      const double mag = fabs(G.fa[k]) + fabs(G.fb[k]) * (double)(G.hi[1] - G.lo[1]) +
-                         fabs(G.fc[k]) * (double)(G.hi[2] - G.lo[2]) + 1.0;
-      G.fthr[k] = (float)ldexp(mag, -44);  // >> the few-ulp fp64 error of the crossing
-      if (G.fthr[k] >= 0.25f) G.ftype[k] *= 2;  // nearly x-parallel face: exact search per row
+      const double fa = (double)num / (1024.0 * (double)n0);
+      const double fb = -(double)n1 / (double)n0, fc = -(double)n2 / (double)n0;
+      G.fa[k] = (float)fa;
+      G.fb[k] = (float)fb;
+      G.fc[k] = (float)fc;
+      // fp32 rounding of 3 coefficients + 2 fma: < 2^-22 (|fa| + |fb| Ly + |fc| Lz); 4x margin
+      const double thr = ldexp(fabs(fa) + fabs(fb) * Ly + fabs(fc) * Lz + 1.0, -20);
+      G.fthr[k] = (float)thr;
+      G.ftype[k] = (n0 > 0 ? 1 : -1) * (thr >= 0.25 ? 2 : 1);
     } else {
       G.ftype[k] = 0;
-      G.fa[k] = G.fb[k] = G.fc[k] = 0.0;
+      G.fa[k] = G.fb[k] = G.fc[k] = 0.0f;
       G.fthr[k] = 0.0f;
     }
   }
   // O4: displacement u(p) = sum_k lambda_k(p) U_k / 1024, lambda_k = e_k / |Delta|.
   // Gradient du_a/dp_b = sum_k n_kb U_ka / |Delta|; value at lo from exact e_k(lo).
   const double inv_det = 1.0 / (double)G.absdet;
+  const double L[3] = {(double)(G.hi[0] - G.lo[0]), Ly, Lz};
   i64 elo[4];
 #pragma unroll
   for (int k = 0; k < 4; k++)
     elo[k] = 1024 * (G.nrm[k][0] * G.lo[0] + G.nrm[k][1] * G.lo[1] + G.nrm[k][2] * G.lo[2]) - G.cst[k];
-  bool fast = true;
+  bool any_exact = false;
 #pragma unroll
   for (int a = 0; a < 3; a++) {
     bool exact = true;
+    double Aab[3];
 #pragma unroll
     for (int b = 0; b < 3; b++) {
       i128 num = 0;
 #pragma unroll
       for (int k = 0; k < 4; k++) num += (i128)G.nrm[k][b] * (i128)G.U[k][a];
       if (num != 0) exact = false;
-      G.A[a][b] = (double)num * inv_det;
+      Aab[b] = (double)num * inv_det;
+      G.A[a][b] = (float)Aab[b];
     }
-    double dmin, dmax;
     if (exact) {
-      // every vertex moves by the same U_a: x_a = q_a + U_a / 1024 exactly
-      G.d0[a] = (double)G.U[0][a] * (1.0 / 1024.0);
+      // every vertex moves by the same U_a: x_a = q_a + U_a / 1024 exactly (fp32-exact)
+      G.d0[a] = (float)G.U[0][a] * (1.0f / 1024.0f);
       G.eps[a] = 0.0f;
-      fast = false;
-      dmin = dmax = G.d0[a];
+      any_exact = true;
     } else {
       i128 N = 0;
 #pragma unroll
       for (int k = 0; k < 4; k++) N += (i128)elo[k] * (i128)G.U[k][a];
-      G.d0[a] = (double)N / (1024.0 * (double)G.absdet);
-      dmin = 1e300;
-      dmax = -1e300;
-      double amax = 0.0;
+      const double d0 = (double)N / (1024.0 * (double)G.absdet);
+      G.d0[a] = (float)d0;
+      double amax = fabs(d0);
 #pragma unroll
-      for (int c = 0; c < 8; c++) {
-        const double v = G.d0[a] + G.A[a][0] * (double)((c & 1) ? G.hi[0] - G.lo[0] : 0) +
-                         G.A[a][1] * (double)((c & 2) ? G.hi[1] - G.lo[1] : 0) +
-                         G.A[a][2] * (double)((c & 4) ? G.hi[2] - G.lo[2] : 0);
-        const double xq = v + (double)((c >> a) & 1 ? G.hi[a] : G.lo[a]);
-        dmin = fmin(dmin, xq);
-        dmax = fmax(dmax, xq);
+      for (int c = 1; c < 8; c++) {
+        const double v = d0 + Aab[0] * ((c & 1) ? L[0] : 0.0) + Aab[1] * ((c & 2) ? L[1] : 0.0) +
+                         Aab[2] * ((c & 4) ? L[2] : 0.0);
         amax = fmax(amax, fabs(v));
       }
-      // fp32 error of d = fma(A_x, k, d_row) + frac: <= 2^-24 (2 |u|max + 2 |A_x| L + 1);
-      // eps = 2x that
-      const double bound = amax + fabs(G.A[a][0]) * (double)(G.hi[0] - G.lo[0]) + 1.0;
-      G.eps[a] = (float)ldexp(bound, -22);
-      // fast path only if every position of the bbox stays strictly inside [0, n-1]
-      if (!(dmin > 1e-3 && dmax < (double)(dims[a] - 1) - 1e-3)) fast = false;
+      // fp32 error of d = fma(A_x0, k, d_row(fp32 fma chain)) and of frac(d):
+      // <= 2^-24 (5 (|u|max + sum_b |A_ab| L_b) + 1); eps = 3x that
+      const double bound = amax + fabs(Aab[0]) * L[0] + fabs(Aab[1]) * L[1] + fabs(Aab[2]) * L[2] + 1.0;
+      G.eps[a] = (float)ldexp(bound, -19);
     }
   }
-  G.flags = 1 | (fast ? 2 : 0);
+  G.flags = 1 | (any_exact ? 0 : 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -313,7 +311,7 @@ __device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, int
   const int lo = R.lo[0], hi = R.hi[0];
   xl = lo;
   xh = hi;
-  const double dy = (double)(y - R.lo[1]), dz = (double)(z - R.lo[2]);
+  const float dy = (float)(y - R.lo[1]), dz = (float)(z - R.lo[2]);
 #pragma unroll
   for (int k = 0; k < 4; k++) {
     const int t = R.ftype[k];
@@ -323,10 +321,11 @@ __device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, int
       if (!own) xh = lo - 1;
       continue;
     }
-    double xs = fma(R.fc[k], dz, fma(R.fb[k], dy, R.fa[k]));
-    xs = fmin(fmax(xs, (double)lo - 4.5), (double)hi + 4.5);
-    if (t == 2 || t == -2) {  // exact monotone search (rare; e is monotone in x)
-      int x = (int)rint(xs);
+    float xs = fmaf(R.fc[k], dz, fmaf(R.fb[k], dy, R.fa[k]));
+    xs = fminf(fmaxf(xs, (float)lo - 4.5f), (float)hi + 4.5f);
+    const float xr = rintf(xs);
+    if (t == 2 || t == -2) {  // exact monotone search (rare: nearly x-parallel face)
+      int x = (int)xr;
       if (t > 0) {  // smallest x in [lo, hi+1] with e >= 0
         x = min(max(x, lo), hi + 1);
         while (x > lo && face_e(R, k, x - 1, y, z) >= 0) --x;
@@ -340,11 +339,10 @@ __device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, int
       }
       continue;
     }
-    const double xr = rint(xs);
     int xi;
-    if (fabs(xs - xr) > (double)R.fthr[k]) {
-      xi = (int)ceil(xs) - (t < 0 ? 1 : 0);  // lower: smallest x > x*; upper: largest x < x*
-    } else {
+    if (fabsf(xs - xr) > R.fthr[k]) {
+      xi = (int)ceilf(xs) - (t < 0 ? 1 : 0);  // lower: smallest x > x*; upper: largest x < x*
+    } else {  // x* within the error bound of the integer c: decide exactly
       const int c = (int)xr;
       const i64 e = face_e(R, k, c, y, z);
       xi = t > 0 ? (e >= 0 ? c : c + 1) : (e > 0 ? c : c - 1);
@@ -354,65 +352,111 @@ __device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, int
   }
 }
 
+// Conservative y range of the tet's cross-section with the plane z (exact
+// vertex coordinates; edge intersections in fp32 with a 1e-3 voxel margin).
+__device__ __forceinline__ void slice_y_range(const SideRec& R, int z, int& ylo, int& yhi) {
+  float ymin = 3.0e38f, ymax = -3.0e38f;
+  const float zf = (float)z;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+#pragma unroll
+    for (int j = i + 1; j < 4; j++) {
+      const float zi = R.vz[i], zj = R.vz[j];
+      const float lo = fminf(zi, zj), hi = fmaxf(zi, zj);
+      if (zf < lo || zf > hi) continue;
+      float y0, y1;
+      if (hi > lo) {
+        const float t = (zf - zi) / (zj - zi);
+        y0 = y1 = fmaf(t, R.vy[j] - R.vy[i], R.vy[i]);
+      } else {
+        y0 = R.vy[i];
+        y1 = R.vy[j];
+      }
+      ymin = fminf(ymin, fminf(y0, y1));
+      ymax = fmaxf(ymax, fmaxf(y0, y1));
+    }
+  }
+  ylo = max(R.lo[1], (int)ceilf(fmaxf(ymin - 1e-3f, -1.0e6f)));
+  yhi = min(R.hi[1], (int)floorf(fminf(ymax + 1e-3f, 1.0e6f)));
+}
+
 struct WarpSmem {
   SideRec R;
   int4 row_i[32];    // (exclusive prefix, linear index of row start, xl, y | z << 16)
   float4 row_d[32];  // fp32 displacement at the row start
 };
 
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(FULLMASK, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// index of the first lane whose inclusive prefix exceeds idx (idx < total)
+__device__ __forceinline__ int warp_search(int incl, int idx) {
+  int pos = 0;
+#pragma unroll
+  for (int b = 16; b; b >>= 1) {
+    const int v = __shfl_sync(FULLMASK, incl, pos + b - 1);
+    if (v <= idx) pos += b;
+  }
+  return pos;
+}
+
 // Generic rasterizer: f(row_info, row_disp, k) for every owned sample of the
-// side, 32 samples per warp step.  All lanes of the warp must call it.
+// side.  Rows are enumerated per z-slice over the slice's y range, 32 rows per
+// step (lanes compute the exact x-intervals), then the flattened samples of
+// those rows are swept 32 at a time.  All lanes of the warp must call it.
 template <class F>
 __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, WarpSmem& S, int lane,
                                        F& f) {
-  const int nyb = R.hi[1] - R.lo[1] + 1, nzb = R.hi[2] - R.lo[2] + 1;
-  const int nrows = nyb * nzb;
-  for (int r0 = 0; r0 < nrows; r0 += 32) {
-    const int r = r0 + lane;
-    int len = 0, xl = 0, y = 0, z = 0;
-    float4 drow = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < nrows) {
-      const int zz = r / nyb;
-      y = R.lo[1] + (r - zz * nyb);
-      z = R.lo[2] + zz;
-      int xh;
-      row_interval(R, y, z, xl, xh);
-      len = max(0, xh - xl + 1);
-      if (len) {
-        const double ox = (double)(xl - R.lo[0]), oy = (double)(y - R.lo[1]),
-                     oz = (double)(z - R.lo[2]);
-        drow.x = (float)fma(R.A[0][2], oz, fma(R.A[0][1], oy, fma(R.A[0][0], ox, R.d0[0])));
-        drow.y = (float)fma(R.A[1][2], oz, fma(R.A[1][1], oy, fma(R.A[1][0], ox, R.d0[1])));
-        drow.z = (float)fma(R.A[2][2], oz, fma(R.A[2][1], oy, fma(R.A[2][0], ox, R.d0[2])));
+  for (int z0 = R.lo[2]; z0 <= R.hi[2]; z0 += 32) {
+    const int zl = z0 + lane;
+    int ylo = 0, yhi = -1;
+    if (zl <= R.hi[2]) slice_y_range(R, zl, ylo, yhi);
+    const int cnt = max(0, yhi - ylo + 1);
+    const int zincl = warp_incl_scan(cnt, lane);
+    const int nrows = __shfl_sync(FULLMASK, zincl, 31);
+    for (int r0 = 0; r0 < nrows; r0 += 32) {
+      const int r = r0 + lane;
+      const int zp = warp_search(zincl, min(r, nrows - 1));
+      const int zinc = __shfl_sync(FULLMASK, zincl, zp);
+      const int zcnt = __shfl_sync(FULLMASK, cnt, zp);
+      const int zylo = __shfl_sync(FULLMASK, ylo, zp);
+      int len = 0, xl = 0;
+      const int z = z0 + zp;
+      const int y = zylo + (r - (zinc - zcnt));
+      float4 drow = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < nrows) {
+        int xh;
+        row_interval(R, y, z, xl, xh);
+        len = max(0, xh - xl + 1);
+        const float ox = (float)(xl - R.lo[0]), oy = (float)(y - R.lo[1]), oz = (float)(z - R.lo[2]);
+        drow.x = fmaf(R.A[0][2], oz, fmaf(R.A[0][1], oy, fmaf(R.A[0][0], ox, R.d0[0])));
+        drow.y = fmaf(R.A[1][2], oz, fmaf(R.A[1][1], oy, fmaf(R.A[1][0], ox, R.d0[1])));
+        drow.z = fmaf(R.A[2][2], oz, fmaf(R.A[2][1], oy, fmaf(R.A[2][0], ox, R.d0[2])));
       }
-    }
-    int incl = len;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(FULLMASK, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(FULLMASK, incl, 31);
-    if (total == 0) continue;
-    __syncwarp();
-    S.row_i[lane] = make_int4(incl - len, (z * ny + y) * nx + xl, xl, y | (z << 16));
-    S.row_d[lane] = drow;
-    __syncwarp();
-    for (int s0 = 0; s0 < total; s0 += 32) {
-      const int idx = s0 + lane;
-      int pos = 0;
-#pragma unroll
-      for (int b = 16; b; b >>= 1) {
-        const int v = __shfl_sync(FULLMASK, incl, pos + b - 1);
-        if (v <= idx) pos += b;
+      const int incl = warp_incl_scan(len, lane);
+      const int total = __shfl_sync(FULLMASK, incl, 31);
+      if (total == 0) continue;
+      __syncwarp();
+      S.row_i[lane] = make_int4(incl - len, (z * ny + y) * nx + xl, xl, y | (z << 16));
+      S.row_d[lane] = drow;
+      __syncwarp();
+      for (int s0 = 0; s0 < total; s0 += 32) {
+        const int idx = s0 + lane;
+        const int pos = warp_search(incl, idx);
+        if (idx < total) {
+          const int4 ri = S.row_i[pos];
+          const float4 rd = S.row_d[pos];
+          f(ri, rd, idx - ri.x);
+        }
       }
-      if (idx < total) {
-        const int4 ri = S.row_i[pos];
-        const float4 rd = S.row_d[pos];
-        f(ri, rd, idx - ri.x);
-      }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 
@@ -460,28 +504,10 @@ __device__ __noinline__ bool exact_fg(const SideRec& R, int qx, int qy, int qz, 
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 
-// Per-axis clamp of the fp32 position (O5) for the general path: i0 in [0, n-2],
-// weight f in [0, 1]; x <= 0 -> (0, 0); x >= n-1 -> (n-2, 1); else floor/frac.
-__device__ __forceinline__ void axis_clamp(int q, float d, int n, float eps, int& i0, float& f,
-                                           bool& amb) {
-  const float fl = floorf(d);
-  float fr = d - fl;
-  amb = (eps > 0.0f) && ((fr < eps) || (fr > 1.0f - eps));
-  const int ix = q + (int)fl;
-  if (ix < 0 || (ix == 0 && fr == 0.0f)) {
-    i0 = 0; fr = 0.0f;
-  } else if (ix >= n - 1) {
-    i0 = n - 2; fr = 1.0f;
-  } else {
-    i0 = ix;
-  }
-  f = fr;
-}
-
-// a5 + a6: one sample of one side.  FAST: every position of the item is
-// strictly inside the image and no axis is exact, so all 8 corners have a
-// positive weight unless the position is within eps of a lattice plane.
-template <bool FAST>
+// a5 + a6: one sample of one side.  NOEXACT: no axis of the item is an exact
+// translation axis, so a position farther than eps from every lattice plane has
+// all 8 corners of positive weight when it is inside [0, n-1] (checked per sample).
+template <bool NOEXACT>
 struct Sample {
   const SideRec& R;
   const float* __restrict__ Iown;
@@ -502,23 +528,22 @@ struct Sample {
     const int qx = ri.z + k, qy = ri.w & 0xffff, qz = ri.w >> 16;
     const int lin = ri.y + k;
     const float a = __ldg(&Iown[lin]);
+    const unsigned bm0 = band ? (unsigned)__ldg(&band[lin]) : 0u;
     const float dx = fmaf(ax, (float)k, rd.x);
     const float dy = fmaf(ay, (float)k, rd.y);
     const float dz = fmaf(az, (float)k, rd.z);
-    int i0x, i0y, i0z;
-    float fx, fy, fz;
-    bool amb;
-    if (FAST) {
-      const float flx = floorf(dx), fly = floorf(dy), flz = floorf(dz);
-      fx = dx - flx; fy = dy - fly; fz = dz - flz;
-      i0x = qx + (int)flx; i0y = qy + (int)fly; i0z = qz + (int)flz;
-      amb = (fx < ex) | (fx > 1.0f - ex) | (fy < ey) | (fy > 1.0f - ey) | (fz < ez) | (fz > 1.0f - ez);
-    } else {
-      bool bx, by, bz;
-      axis_clamp(qx, dx, nx, ex, i0x, fx, bx);
-      axis_clamp(qy, dy, ny, ey, i0y, fy, by);
-      axis_clamp(qz, dz, nz, ez, i0z, fz, bz);
-      amb = bx | by | bz;
+    const float flx = floorf(dx), fly = floorf(dy), flz = floorf(dz);
+    float fx = dx - flx, fy = dy - fly, fz = dz - flz;
+    int i0x = qx + (int)flx, i0y = qy + (int)fly, i0z = qz + (int)flz;
+    bool amb = (fx < ex) | (fx > 1.0f - ex) | (fy < ey) | (fy > 1.0f - ey) | (fz < ez) | (fz > 1.0f - ez);
+    amb = amb && NOEXACT;
+    const bool inside = ((unsigned)i0x < (unsigned)(nx - 1)) & ((unsigned)i0y < (unsigned)(ny - 1)) &
+                        ((unsigned)i0z < (unsigned)(nz - 1));
+    if (!inside) {
+      // O5 clamp: x <= 0 -> corner 0 (f = 0); x >= n-1 -> corner n-1 (i0 = n-2, f = 1)
+      if (i0x < 0 || (i0x == 0 && fx == 0.f)) { i0x = 0; fx = 0.f; } else if (i0x >= nx - 1) { i0x = nx - 2; fx = 1.f; }
+      if (i0y < 0 || (i0y == 0 && fy == 0.f)) { i0y = 0; fy = 0.f; } else if (i0y >= ny - 1) { i0y = ny - 2; fy = 1.f; }
+      if (i0z < 0 || (i0z == 0 && fz == 0.f)) { i0z = 0; fz = 0.f; } else if (i0z >= nz - 1) { i0z = nz - 2; fz = 1.f; }
     }
     const int sy = nx, sz = nx * ny;
     const int base = (i0z * ny + i0y) * nx + i0x;
@@ -531,7 +556,7 @@ struct Sample {
     bool fg;
     if (amb) {
       fg = exact_fg(R, qx, qy, qz, dx, dy, dz, Ioth, nx, ny, nz);
-    } else if (FAST) {
+    } else if (NOEXACT && inside) {
       // all 8 corners contribute; values are >= 0, so the sum is > 0 iff one is
       fg = ((c000 + c100) + (c010 + c110)) + ((c001 + c101) + (c011 + c111)) > 0.f;
     } else {
@@ -554,24 +579,22 @@ struct Sample {
     }
     h_sum += (double)h;
     n += 1;
-    if (band) {
-      unsigned bm = __ldg(&band[lin]);
-      while (bm) {
-        const int i = __ffs(bm) - 1;
-        bm &= bm - 1;
-        nb += 1;
-        const float* Do = dmap_oth + (long long)i * V;
-        const float d = __ldg(&dmap_own[(long long)i * V + lin]);
-        const float e000 = __ldg(&Do[base]), e100 = __ldg(&Do[base + 1]);
-        const float e010 = __ldg(&Do[base + sy]), e110 = __ldg(&Do[base + sy + 1]);
-        const float e001 = __ldg(&Do[base + sz]), e101 = __ldg(&Do[base + sz + 1]);
-        const float e011 = __ldg(&Do[base + sz + sy]), e111 = __ldg(&Do[base + sz + sy + 1]);
-        const float Dp = lerpf(lerpf(lerpf(e000, e100, fx), lerpf(e010, e110, fx), fy),
-                               lerpf(lerpf(e001, e101, fx), lerpf(e011, e111, fx), fy), fz);
-        const double dd = (double)d - (double)Dp;
-        // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit)
-        g_sum += __ldg(&w[i]) * ((r - (double)d) * inv_r) * dd * dd;
-      }
+    unsigned bm = bm0;
+    while (bm) {
+      const int i = __ffs(bm) - 1;
+      bm &= bm - 1;
+      nb += 1;
+      const float* Do = dmap_oth + (long long)i * V;
+      const float d = __ldg(&dmap_own[(long long)i * V + lin]);
+      const float e000 = __ldg(&Do[base]), e100 = __ldg(&Do[base + 1]);
+      const float e010 = __ldg(&Do[base + sy]), e110 = __ldg(&Do[base + sy + 1]);
+      const float e001 = __ldg(&Do[base + sz]), e101 = __ldg(&Do[base + sz + 1]);
+      const float e011 = __ldg(&Do[base + sz + sy]), e111 = __ldg(&Do[base + sz + sy + 1]);
+      const float Dp = lerpf(lerpf(lerpf(e000, e100, fx), lerpf(e010, e110, fx), fy),
+                             lerpf(lerpf(e001, e101, fx), lerpf(e011, e111, fx), fy), fz);
+      const double dd = (double)d - (double)Dp;
+      // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit)
+      g_sum += __ldg(&w[i]) * ((r - (double)d) * inv_r) * dd * dd;
     }
   }
 };
@@ -601,7 +624,7 @@ __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int l
                                             double& h_sum, double& g_sum, int& n, int& nb) {
   const SideRec& R = S.R;
   Sample<FAST> f{R, V.I[s], V.I[1 - s], V.band[s], V.dmap[s], V.dmap[1 - s], (int)V.V, V.nx, V.ny,
-                 V.nz, (float)R.A[0][0], (float)R.A[1][0], (float)R.A[2][0], R.eps[0], R.eps[1],
+                 V.nz, R.A[0][0], R.A[1][0], R.A[2][0], R.eps[0], R.eps[1],
                  R.eps[2], V.r, 1.0 / V.r, V.w + s * kMaxPairs, 0.0, 0.0, 0, 0};
   raster(R, V.nx, V.ny, S, lane, f);
   h_sum += f.h_sum;

@@ -30,7 +30,7 @@ assert ACC_DTYPE.itemsize == 48
 EXPORTS = ["morea_create", "morea_destroy", "morea_last_error", "morea_stream", "morea_load_images",
            "morea_set_mesh", "morea_eval_full", "morea_eval_partial", "morea_partial_deps",
            "morea_check_folds", "morea_owner_map", "morea_distance_map", "morea_prof_enable",
-           "morea_prof_read"]
+           "morea_prof_read", "morea_kernel_launches"]
 
 
 class MoreaError(RuntimeError):
@@ -61,6 +61,8 @@ def _load():
     L.morea_owner_map.argtypes = [vp, vp, i32, vp]
     L.morea_distance_map.argtypes = [vp, i32, i32, vp]
     L.morea_prof_enable.argtypes = [vp, i32]
+    L.morea_kernel_launches.argtypes = [vp]
+    L.morea_kernel_launches.restype = i64
     L.morea_prof_read.argtypes = [vp] + [ctypes.POINTER(i64), ctypes.POINTER(f64)] + \
         [ctypes.POINTER(i64)] * 3
     return L
@@ -211,6 +213,9 @@ class Context:
         return out
 
     # ------------------------------------------------------------------ profiling
+    def kernel_launches(self):
+        return int(_lib.morea_kernel_launches(self.h))
+
     def prof_enable(self, on=True):
         self._check(_lib.morea_prof_enable(self.h, 1 if on else 0))
 
