@@ -74,8 +74,11 @@ typedef struct {
 } morea_acc;
 
 /* Create a context on `cuda_device`.  `cuda_stream` (a cudaStream_t of that
- * device) is used for all work; NULL creates a context-owned non-blocking
- * stream.  Returns MOREA_ECUDA if the device is unusable. */
+ * device) is used for all work; NULL creates a context-owned stream that is
+ * ordered with the legacy default stream (cudaStreamDefault flags), so inputs
+ * written there before a call are visible to it.  With a caller stream the
+ * caller orders its producers on that stream.  Returns MOREA_ECUDA if the
+ * device is unusable. */
 int morea_create(int cuda_device, void *cuda_stream, morea_ctx **out);
 void morea_destroy(morea_ctx *ctx);
 /* Message of the last failed call ("" if none).  Owned by the context. */

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -61,7 +62,7 @@ struct morea_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   std::string err;
-  int n_sm = 148, blocks_per_sm = 1;
+  int n_sm = 148, blocks_per_sm = 1, blocks_per_sm_tex = 1;
   // images
   bool have_images = false;
   int nx = 0, ny = 0, nz = 0, K = 0;
@@ -69,7 +70,13 @@ struct morea_ctx {
   double sp[3] = {1, 1, 1};
   double r = 0;
   double w[2][kMaxPairs] = {};
-  DevBuf I[2], band[2], dmap[2], wts;
+  DevBuf I[2], band[2], dmap[2], wts, tex_handles;
+  // texture-gather copies (tall 2D arrays) of I_s, I_t and the maps
+  bool use_tex = false;
+  cudaArray_t arrI[2] = {nullptr, nullptr};
+  cudaTextureObject_t texI[2] = {0, 0};
+  std::vector<cudaArray_t> arrD;
+  std::vector<cudaTextureObject_t> texD;
   // mesh
   bool have_mesh = false;
   int N = 0, T = 0, spoke_mode = 0;
@@ -219,6 +226,10 @@ Volumes volumes_of(const morea_ctx* c) {
   v.K = c->K;
   v.r = c->r;
   v.w = c->wts.as<double>();
+  v.use_tex = c->use_tex ? 1 : 0;
+  v.texI[0] = c->texI[0];
+  v.texI[1] = c->texI[1];
+  v.texD = c->use_tex ? c->tex_handles.as<unsigned long long>() : nullptr;
   return v;
 }
 
@@ -234,7 +245,7 @@ MeshDev mesh_of(const morea_ctx* c) {
 }
 
 int raster_grid(morea_ctx* ctx, long long n_items) {
-  long long g = (long long)ctx->n_sm * ctx->blocks_per_sm;
+  long long g = (long long)ctx->n_sm * (ctx->use_tex ? ctx->blocks_per_sm_tex : ctx->blocks_per_sm);
   long long need = (n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
   return (int)std::max<long long>(1, std::min(g, need));
 }
@@ -369,6 +380,80 @@ int build_plan(morea_ctx* ctx, int G, const int32_t* grp_off_in, const int32_t* 
   return MOREA_OK;
 }
 
+void release_textures(morea_ctx* ctx) {
+  for (int s = 0; s < 2; s++) {
+    if (ctx->texI[s]) cudaDestroyTextureObject(ctx->texI[s]);
+    if (ctx->arrI[s]) cudaFreeArray(ctx->arrI[s]);
+    ctx->texI[s] = 0;
+    ctx->arrI[s] = nullptr;
+  }
+  for (auto t : ctx->texD)
+    if (t) cudaDestroyTextureObject(t);
+  for (auto a : ctx->arrD)
+    if (a) cudaFreeArray(a);
+  ctx->texD.clear();
+  ctx->arrD.clear();
+  ctx->use_tex = false;
+}
+
+// A float volume (nx x ny x nz, x-fastest, device) as a tall 2D gather texture:
+// texel (x, y + ny z).  Point sampling, clamp, unnormalised coordinates.
+cudaError_t make_gather_texture(morea_ctx* ctx, const float* dev, cudaArray_t* arr,
+                                cudaTextureObject_t* tex) {
+  cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
+  const size_t W = ctx->nx, H = (size_t)ctx->ny * ctx->nz;
+  cudaError_t e = cudaMallocArray(arr, &fd, W, H, cudaArrayTextureGather);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy2DToArrayAsync(*arr, 0, 0, dev, W * sizeof(float), W * sizeof(float), H,
+                               cudaMemcpyDeviceToDevice, ctx->stream);
+  if (e != cudaSuccess) return e;
+  cudaResourceDesc rd;
+  std::memset(&rd, 0, sizeof(rd));
+  rd.resType = cudaResourceTypeArray;
+  rd.res.array.array = *arr;
+  cudaTextureDesc td;
+  std::memset(&td, 0, sizeof(td));
+  td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
+  td.filterMode = cudaFilterModePoint;
+  td.readMode = cudaReadModeElementType;
+  td.normalizedCoords = 0;
+  return cudaCreateTextureObject(tex, &rd, &td, nullptr);
+}
+
+// Enable the texture-gather path when the tall 2D layout fits the gather limits.
+cudaError_t build_textures(morea_ctx* ctx) {
+  release_textures(ctx);
+  const char* off = std::getenv("MOREA_NO_TEX");
+  if (off && off[0] && off[0] != '0') return cudaSuccess;
+  int gw = 0, gh = 0;
+  cudaDeviceGetAttribute(&gw, cudaDevAttrMaxTexture2DGatherWidth, ctx->device);
+  cudaDeviceGetAttribute(&gh, cudaDevAttrMaxTexture2DGatherHeight, ctx->device);
+  if ((long long)ctx->nx > gw || (long long)ctx->ny * ctx->nz > gh) return cudaSuccess;
+  for (int s = 0; s < 2; s++) {
+    cudaError_t e = make_gather_texture(ctx, ctx->I[s].as<float>(), &ctx->arrI[s], &ctx->texI[s]);
+    if (e != cudaSuccess) return e;
+  }
+  std::vector<unsigned long long> h(2 * kMaxPairs, 0ull);
+  for (int s = 0; s < 2; s++)
+    for (int i = 0; i < ctx->K; i++) {
+      cudaArray_t a = nullptr;
+      cudaTextureObject_t t = 0;
+      cudaError_t e = make_gather_texture(ctx, ctx->dmap[s].as<float>() + (size_t)i * ctx->V, &a, &t);
+      if (e != cudaSuccess) return e;
+      ctx->arrD.push_back(a);
+      ctx->texD.push_back(t);
+      h[s * kMaxPairs + i] = (unsigned long long)t;
+    }
+  cudaError_t e = ctx->tex_handles.ensure(h.size() * sizeof(unsigned long long));
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(ctx->tex_handles.p, h.data(), h.size() * sizeof(unsigned long long),
+                      cudaMemcpyHostToDevice, ctx->stream);
+  if (e != cudaSuccess) return e;
+  e = cudaStreamSynchronize(ctx->stream);
+  if (e == cudaSuccess) ctx->use_tex = true;
+  return e;
+}
+
 }  // namespace
 
 extern "C" {
@@ -386,7 +471,9 @@ int morea_create(int cuda_device, void* cuda_stream, morea_ctx** out) {
   if (cuda_stream) {
     ctx->stream = (cudaStream_t)cuda_stream;
   } else {
-    e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    // blocking stream: implicitly ordered after work on the legacy default stream,
+    // so inputs produced there (e.g. torch copies) are complete before our kernels run
+    e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault);
     if (e != cudaSuccess) {
       delete ctx;
       return MOREA_ECUDA;
@@ -394,7 +481,8 @@ int morea_create(int cuda_device, void* cuda_stream, morea_ctx** out) {
     ctx->own_stream = true;
   }
   cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, cuda_device);
-  ctx->blocks_per_sm = raster_blocks_per_sm();
+  ctx->blocks_per_sm = raster_blocks_per_sm(false);
+  ctx->blocks_per_sm_tex = raster_blocks_per_sm(true);
   if (ctx->stats.ensure(4 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemset(ctx->stats.p, 0, 4 * sizeof(unsigned long long)) != cudaSuccess) {
     delete ctx;
@@ -408,12 +496,13 @@ void morea_destroy(morea_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  release_textures(ctx);
   for (auto& p : ctx->evs) {
     cudaEventDestroy(p.first);
     cudaEventDestroy(p.second);
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
-                    &ctx->dmap[1], &ctx->wts, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
+                    &ctx->dmap[1], &ctx->wts, &ctx->tex_handles, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
                     &ctx->full_sched, &ctx->full_group_off, &ctx->geom, &ctx->scal, &ctx->hgn,
                     &ctx->counter, &ctx->stats, &ctx->st_off, &ctx->st_nv, &ctx->st_cache_in,
                     &ctx->st_base_acc, &ctx->st_obj, &ctx->st_acc, &ctx->st_cache_out,
@@ -497,6 +586,7 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
   CK(ctx->wts.ensure(sizeof(ctx->w)));
   CK(cudaMemcpyAsync(ctx->wts.p, ctx->w, sizeof(ctx->w), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  CK(build_textures(ctx));
   ctx->have_images = true;
   return MOREA_OK;
 }

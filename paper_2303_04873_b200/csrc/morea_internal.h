@@ -59,6 +59,11 @@ struct Volumes {
   int K;
   double r;
   const double* w;  // device: w[side * kMaxPairs + i] = |C_i| / |G_side|
+  // texture-gather path: I_s / I_t and the maps as tall 2D textures (texel (x, y + ny z)),
+  // gathered 2x2 per slice (tld4); 0 / nullptr when the volume exceeds the gather limits
+  unsigned long long texI[2];
+  const unsigned long long* texD;  // [side * kMaxPairs + i]
+  int use_tex;
 };
 
 struct MeshDev {
@@ -102,7 +107,7 @@ cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, un
                              cudaStream_t s);
 cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s);
 cudaError_t launch_raster(const EvalArgs& a, int grid, cudaStream_t s);
-int raster_blocks_per_sm();
+int raster_blocks_per_sm(bool tex);
 cudaError_t launch_reduce(const EvalArgs& a, int G, const int* group_off, const void* base_acc,
                           const double* cache_in, double* cache_out, const int* changed,
                           const int* grp_off, double* obj, void* acc, cudaStream_t s);

@@ -507,7 +507,7 @@ __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(
 // a5 + a6: one sample of one side.  NOEXACT: no axis of the item is an exact
 // translation axis, so a position farther than eps from every lattice plane has
 // all 8 corners of positive weight when it is inside [0, n-1] (checked per sample).
-template <bool NOEXACT>
+template <bool NOEXACT, bool TEX>
 struct Sample {
   const SideRec& R;
   const float* __restrict__ Iown;
@@ -523,6 +523,27 @@ struct Sample {
   const double* w;   // pair weights of this side
   double h_sum, g_sum;
   int n, nb;
+  unsigned long long tex_oth;          // gather texture of the other volume
+  const unsigned long long* tex_moth;  // gather textures of the other side's maps
+
+  // the 8 corners (i0 .. i0+1)^3: two 2x2 texture gathers (tld4) or 8 loads
+  __device__ __forceinline__ void corners(const float* __restrict__ vol, unsigned long long tex,
+                                          int base, int i0x, int i0y, int i0z, float c[8]) const {
+    if (TEX) {
+      const float u = (float)(i0x + 1), v = (float)(i0z * ny + i0y + 1);
+      const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v, 0);
+      const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v + (float)ny, 0);
+      // gather order: (x0,y1) (x1,y1) (x1,y0) (x0,y0)
+      c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
+      c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
+    } else {
+      const int sy = nx, sz = nx * ny;
+      c[0] = __ldg(&vol[base]); c[1] = __ldg(&vol[base + 1]);
+      c[2] = __ldg(&vol[base + sy]); c[3] = __ldg(&vol[base + sy + 1]);
+      c[4] = __ldg(&vol[base + sz]); c[5] = __ldg(&vol[base + sz + 1]);
+      c[6] = __ldg(&vol[base + sz + sy]); c[7] = __ldg(&vol[base + sz + sy + 1]);
+    }
+  }
 
   __device__ __forceinline__ void operator()(const int4& ri, const float4& rd, int k) {
     const int qx = ri.z + k, qy = ri.w & 0xffff, qz = ri.w >> 16;
@@ -545,12 +566,11 @@ struct Sample {
       if (i0y < 0 || (i0y == 0 && fy == 0.f)) { i0y = 0; fy = 0.f; } else if (i0y >= ny - 1) { i0y = ny - 2; fy = 1.f; }
       if (i0z < 0 || (i0z == 0 && fz == 0.f)) { i0z = 0; fz = 0.f; } else if (i0z >= nz - 1) { i0z = nz - 2; fz = 1.f; }
     }
-    const int sy = nx, sz = nx * ny;
     const int base = (i0z * ny + i0y) * nx + i0x;
-    const float c000 = __ldg(&Ioth[base]), c100 = __ldg(&Ioth[base + 1]);
-    const float c010 = __ldg(&Ioth[base + sy]), c110 = __ldg(&Ioth[base + sy + 1]);
-    const float c001 = __ldg(&Ioth[base + sz]), c101 = __ldg(&Ioth[base + sz + 1]);
-    const float c011 = __ldg(&Ioth[base + sz + sy]), c111 = __ldg(&Ioth[base + sz + sy + 1]);
+    float cc[8];
+    corners(Ioth, tex_oth, base, i0x, i0y, i0z, cc);
+    const float c000 = cc[0], c100 = cc[1], c010 = cc[2], c110 = cc[3];
+    const float c001 = cc[4], c101 = cc[5], c011 = cc[6], c111 = cc[7];
     const float b = lerpf(lerpf(lerpf(c000, c100, fx), lerpf(c010, c110, fx), fy),
                           lerpf(lerpf(c001, c101, fx), lerpf(c011, c111, fx), fy), fz);
     bool fg;
@@ -579,17 +599,19 @@ struct Sample {
     }
     h_sum += (double)h;
     n += 1;
-    unsigned bm = bm0;
-    while (bm) {
-      const int i = __ffs(bm) - 1;
-      bm &= bm - 1;
+    // pairs in a warp-uniform order: a texture instruction needs the same handle on
+    // every executing lane, so loop over the OR of the active lanes' band bits
+    unsigned wbm = __reduce_or_sync(__activemask(), bm0);
+    while (wbm) {
+      const int i = __ffs(wbm) - 1;
+      wbm &= wbm - 1;
+      if (!((bm0 >> i) & 1u)) continue;
       nb += 1;
-      const float* Do = dmap_oth + (long long)i * V;
       const float d = __ldg(&dmap_own[(long long)i * V + lin]);
-      const float e000 = __ldg(&Do[base]), e100 = __ldg(&Do[base + 1]);
-      const float e010 = __ldg(&Do[base + sy]), e110 = __ldg(&Do[base + sy + 1]);
-      const float e001 = __ldg(&Do[base + sz]), e101 = __ldg(&Do[base + sz + 1]);
-      const float e011 = __ldg(&Do[base + sz + sy]), e111 = __ldg(&Do[base + sz + sy + 1]);
+      float ee[8];
+      corners(dmap_oth + (long long)i * V, TEX ? __ldg(&tex_moth[i]) : 0ull, base, i0x, i0y, i0z, ee);
+      const float e000 = ee[0], e100 = ee[1], e010 = ee[2], e110 = ee[3];
+      const float e001 = ee[4], e101 = ee[5], e011 = ee[6], e111 = ee[7];
       const float Dp = lerpf(lerpf(lerpf(e000, e100, fx), lerpf(e010, e110, fx), fy),
                              lerpf(lerpf(e001, e101, fx), lerpf(e011, e111, fx), fy), fz);
       const double dd = (double)d - (double)Dp;
@@ -619,13 +641,14 @@ __device__ __forceinline__ void load_rec(WarpSmem& S, const SideRec* src, int la
   __syncwarp();
 }
 
-template <bool FAST>
+template <bool FAST, bool TEX>
 __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int lane, int s,
                                             double& h_sum, double& g_sum, int& n, int& nb) {
   const SideRec& R = S.R;
-  Sample<FAST> f{R, V.I[s], V.I[1 - s], V.band[s], V.dmap[s], V.dmap[1 - s], (int)V.V, V.nx, V.ny,
-                 V.nz, R.A[0][0], R.A[1][0], R.A[2][0], R.eps[0], R.eps[1],
-                 R.eps[2], V.r, 1.0 / V.r, V.w + s * kMaxPairs, 0.0, 0.0, 0, 0};
+  Sample<FAST, TEX> f{R, V.I[s], V.I[1 - s], V.band[s], V.dmap[s], V.dmap[1 - s], (int)V.V, V.nx,
+                      V.ny, V.nz, R.A[0][0], R.A[1][0], R.A[2][0], R.eps[0], R.eps[1],
+                      R.eps[2], V.r, 1.0 / V.r, V.w + s * kMaxPairs, 0.0, 0.0, 0, 0,
+                      TEX ? V.texI[1 - s] : 0ull, TEX ? V.texD + (1 - s) * kMaxPairs : nullptr};
   raster(R, V.nx, V.ny, S, lane, f);
   h_sum += f.h_sum;
   g_sum += f.g_sum;
@@ -636,6 +659,7 @@ __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int l
 // ---------------------------------------------------------------------------
 // k_raster: persistent warps over the item queue (a4 + a5 + a6 + per-tet a7).
 // ---------------------------------------------------------------------------
+template <bool TEX>
 __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(const EvalArgs A) {
   __shared__ WarpSmem smem[kWarpsPerBlock];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -661,8 +685,8 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
       load_rec(S, &A.geom[2 * i + s], lane);
       const int fl = S.R.flags;
       if (!(fl & 1)) continue;
-      if (fl & 2) raster_side<true>(A.vol, S, lane, s, h_sum, g_sum, n, nb);
-      else raster_side<false>(A.vol, S, lane, s, h_sum, g_sum, n, nb);
+      if (fl & 2) raster_side<true, TEX>(A.vol, S, lane, s, h_sum, g_sum, n, nb);
+      else raster_side<false, TEX>(A.vol, S, lane, s, h_sum, g_sum, n, nb);
     }
     HGN out;
     out.h = warp_sum_d(h_sum);
@@ -683,15 +707,17 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
   }
 }
 
-int raster_blocks_per_sm() {
+int raster_blocks_per_sm(bool tex) {
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_raster, kRasterThreads, 0) != cudaSuccess)
-    return 1;
+  cudaError_t e = tex ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_raster<true>, kRasterThreads, 0)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_raster<false>, kRasterThreads, 0);
+  if (e != cudaSuccess) return 1;
   return nb > 0 ? nb : 1;
 }
 
 cudaError_t launch_raster(const EvalArgs& a, int grid, cudaStream_t s) {
-  k_raster<<<grid, kRasterThreads, 0, s>>>(a);
+  if (a.vol.use_tex) k_raster<true><<<grid, kRasterThreads, 0, s>>>(a);
+  else k_raster<false><<<grid, kRasterThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
