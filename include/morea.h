@@ -90,7 +90,9 @@ void *morea_stream(const morea_ctx *ctx);
  *  nx,ny,nz >= 2, <= 768; spacing_mm[3] > 0 (physical voxel size; lengths,
  *    distances, r and severities are in mm).
  *  I_s, I_t: V = nx*ny*nz float32 each, finite, >= 0, background exactly 0
- *    (h's zero/non-zero cases, L318-322; reading O6).
+ *    (h's zero/non-zero cases, L318-322; reading O6); non-zero values must be
+ *    >= 2^-40 (~9.1e-13) so the fp32 interpolant of a non-zero footprint cannot
+ *    underflow to 0 (the exact case split relies on it).
  *  n_pairs K in [0, 8]: pairs <C_s, C_t>_i of contour point sets (L332-333).
  *    cs_off/ct_off: K+1 int64 CSR offsets (non-decreasing, cs_off[0] = 0) into
  *    cs_xyz/ct_xyz: float32 xyz triples in voxel units.  Weights per side are

@@ -550,7 +550,7 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, ctx->st_i32.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  if (bad) return fail(ctx, MOREA_EINVAL, "intensities must be finite and >= 0");
+  if (bad) return fail(ctx, MOREA_EINVAL, "intensities must be finite, and 0 or in [2^-40, inf)");
   // contours
   const int K = n_pairs;
   ctx->K = K;

@@ -28,7 +28,7 @@
 #include "morea_internal.h"
 
 #ifndef MOREA_RASTER_MINB
-#define MOREA_RASTER_MINB 3  // resident 256-thread blocks per SM the register budget targets
+#define MOREA_RASTER_MINB 4  // resident 256-thread blocks per SM the register budget targets
 #endif
 
 namespace morea {
@@ -384,6 +384,7 @@ struct WarpSmem {
   SideRec R;
   int4 row_i[32];    // (exclusive prefix, linear index of row start, xl, y | z << 16)
   float4 row_d[32];  // fp32 displacement at the row start
+  float4 row_p[32];  // row start as floats: (xl, y, z, z * ny + y)
 };
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -406,13 +407,17 @@ __device__ __forceinline__ int warp_search(int incl, int idx) {
   return pos;
 }
 
-// Generic rasterizer: f(row_info, row_disp, k) for every owned sample of the
-// side.  Rows are enumerated per z-slice over the slice's y range, 32 rows per
-// step (lanes compute the exact x-intervals), then the flattened samples of
-// those rows are swept 32 at a time.  All lanes of the warp must call it.
+// Generic rasterizer: visits every owned sample of the side.  Rows are
+// enumerated per z-slice over the slice's y range, 32 rows per step (lanes
+// compute the exact x-intervals); non-empty rows are compacted into shared
+// memory and their flattened samples are swept 32 per step.  A lane finds its
+// row from the mask of row starts inside the 32-sample window (one redux.or and
+// a popc).  Lanes past the end evaluate sample 0 of the last row with
+// valid = false (no divergence).  All lanes of the warp must call it.
 template <class F>
 __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, WarpSmem& S, int lane,
                                        F& f) {
+  const unsigned lt_mask = (1u << lane) - 1u;
   for (int z0 = R.lo[2]; z0 <= R.hi[2]; z0 += 32) {
     const int zl = z0 + lane;
     int ylo = 0, yhi = -1;
@@ -429,31 +434,41 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, WarpSme
       int len = 0, xl = 0;
       const int z = z0 + zp;
       const int y = zylo + (r - (zinc - zcnt));
-      float4 drow = make_float4(0.f, 0.f, 0.f, 0.f);
       if (r < nrows) {
         int xh;
         row_interval(R, y, z, xl, xh);
         len = max(0, xh - xl + 1);
-        const float ox = (float)(xl - R.lo[0]), oy = (float)(y - R.lo[1]), oz = (float)(z - R.lo[2]);
-        drow.x = fmaf(R.A[0][2], oz, fmaf(R.A[0][1], oy, fmaf(R.A[0][0], ox, R.d0[0])));
-        drow.y = fmaf(R.A[1][2], oz, fmaf(R.A[1][1], oy, fmaf(R.A[1][0], ox, R.d0[1])));
-        drow.z = fmaf(R.A[2][2], oz, fmaf(R.A[2][1], oy, fmaf(R.A[2][0], ox, R.d0[2])));
       }
       const int incl = warp_incl_scan(len, lane);
       const int total = __shfl_sync(FULLMASK, incl, 31);
       if (total == 0) continue;
+      const unsigned ne = __ballot_sync(FULLMASK, len > 0);
+      const int start = incl - len;
       __syncwarp();
-      S.row_i[lane] = make_int4(incl - len, (z * ny + y) * nx + xl, xl, y | (z << 16));
-      S.row_d[lane] = drow;
+      if (len > 0) {
+        const int c = __popc(ne & lt_mask);
+        const float ox = (float)(xl - R.lo[0]), oy = (float)(y - R.lo[1]), oz = (float)(z - R.lo[2]);
+        float4 drow;
+        drow.x = fmaf(R.A[0][2], oz, fmaf(R.A[0][1], oy, fmaf(R.A[0][0], ox, R.d0[0])));
+        drow.y = fmaf(R.A[1][2], oz, fmaf(R.A[1][1], oy, fmaf(R.A[1][0], ox, R.d0[1])));
+        drow.z = fmaf(R.A[2][2], oz, fmaf(R.A[2][1], oy, fmaf(R.A[2][0], ox, R.d0[2])));
+        drow.w = 0.f;
+        S.row_i[c] = make_int4(start, (z * ny + y) * nx + xl, xl, y | (z << 16));
+        S.row_d[c] = drow;
+        S.row_p[c] = make_float4((float)xl, (float)y, (float)z, 0.f);
+      }
       __syncwarp();
+      const int last = __popc(ne) - 1;
+      int rprev = -1;
       for (int s0 = 0; s0 < total; s0 += 32) {
+        const unsigned bit = (len > 0 && start >= s0 && start < s0 + 32) ? (1u << (start - s0)) : 0u;
+        const unsigned M = __reduce_or_sync(FULLMASK, bit);
+        const int row = min(rprev + __popc(M & ((2u << lane) - 1u)), last);
+        rprev += __popc(M);
         const int idx = s0 + lane;
-        const int pos = warp_search(incl, idx);
-        if (idx < total) {
-          const int4 ri = S.row_i[pos];
-          const float4 rd = S.row_d[pos];
-          f(ri, rd, idx - ri.x);
-        }
+        const bool valid = idx < total;
+        const int4 ri = S.row_i[row];
+        f.sample(ri, S.row_d[row], S.row_p[row], valid ? idx - ri.x : 0, valid);
       }
       __syncwarp();
     }
@@ -504,10 +519,18 @@ __device__ __noinline__ bool exact_fg(const SideRec& R, int qx, int qy, int qz, 
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 
-// a5 + a6: one sample of one side.  NOEXACT: no axis of the item is an exact
-// translation axis, so a position farther than eps from every lattice plane has
-// all 8 corners of positive weight when it is inside [0, n-1] (checked per sample).
-template <bool NOEXACT, bool TEX>
+// Positivity-exact lerp: (1 - t) a + t b as fma(t, b, (1 - t) a).  For a, b >= 0
+// and t in [0, 1] it is > 0 iff a contributing value (a with t < 1, b with
+// t > 0) is > 0, barring underflow (excluded by the value precondition of
+// morea_load_images: non-zero intensities >= 2^-40).
+__device__ __forceinline__ float plerp(float a, float b, float t, float omt) {
+  return fmaf(t, b, omt * a);
+}
+
+// a5 + a6: one sample of one side.  The footprint weights are exact: 0 / 1 on
+// clamped axes and exact-integer axes, and in [eps, 1 - eps] otherwise unless the
+// position is ambiguous (then exact_fg decides), so fg = (b > 0) is exact.
+template <bool TEX>
 struct Sample {
   const SideRec& R;
   const float* __restrict__ Iown;
@@ -518,7 +541,7 @@ struct Sample {
   int V;
   int nx, ny, nz;
   float ax, ay, az;  // displacement gradient along x (fp32)
-  float ex, ey, ez;  // per-axis filter bounds
+  float ex, ey, ez;  // 0.5 - eps per axis (ambiguity threshold on |f - 0.5|)
   double r, inv_r;
   const double* w;   // pair weights of this side
   double h_sum, g_sum;
@@ -527,10 +550,9 @@ struct Sample {
   const unsigned long long* tex_moth;  // gather textures of the other side's maps
 
   // the 8 corners (i0 .. i0+1)^3: two 2x2 texture gathers (tld4) or 8 loads
-  __device__ __forceinline__ void corners(const float* __restrict__ vol, unsigned long long tex,
-                                          int base, int i0x, int i0y, int i0z, float c[8]) const {
+  __device__ __forceinline__ void gather(const float* __restrict__ vol, unsigned long long tex,
+                                         float u, float v, int base, float c[8]) const {
     if (TEX) {
-      const float u = (float)(i0x + 1), v = (float)(i0z * ny + i0y + 1);
       const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v, 0);
       const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v + (float)ny, 0);
       // gather order: (x0,y1) (x1,y1) (x1,y0) (x0,y0)
@@ -545,50 +567,46 @@ struct Sample {
     }
   }
 
-  __device__ __forceinline__ void operator()(const int4& ri, const float4& rd, int k) {
-    const int qx = ri.z + k, qy = ri.w & 0xffff, qz = ri.w >> 16;
+  __device__ __forceinline__ float tri(const float c[8], float fx, float fy, float fz, float gx,
+                                       float gy, float gz) const {
+    return plerp(plerp(plerp(c[0], c[1], fx, gx), plerp(c[2], c[3], fx, gx), fy, gy),
+                 plerp(plerp(c[4], c[5], fx, gx), plerp(c[6], c[7], fx, gx), fy, gy), fz, gz);
+  }
+
+  __device__ __forceinline__ void sample(const int4& ri, const float4& rd, const float4& rp, int k,
+                                         bool valid) {
     const int lin = ri.y + k;
     const float a = __ldg(&Iown[lin]);
-    const unsigned bm0 = band ? (unsigned)__ldg(&band[lin]) : 0u;
-    const float dx = fmaf(ax, (float)k, rd.x);
-    const float dy = fmaf(ay, (float)k, rd.y);
-    const float dz = fmaf(az, (float)k, rd.z);
+    const unsigned bm = (band && valid) ? (unsigned)__ldg(&band[lin]) : 0u;
+    const float kf = (float)k;
+    const float dx = fmaf(ax, kf, rd.x), dy = fmaf(ay, kf, rd.y), dz = fmaf(az, kf, rd.z);
     const float flx = floorf(dx), fly = floorf(dy), flz = floorf(dz);
     float fx = dx - flx, fy = dy - fly, fz = dz - flz;
-    int i0x = qx + (int)flx, i0y = qy + (int)fly, i0z = qz + (int)flz;
-    bool amb = (fx < ex) | (fx > 1.0f - ex) | (fy < ey) | (fy > 1.0f - ey) | (fz < ez) | (fz > 1.0f - ez);
-    amb = amb && NOEXACT;
-    const bool inside = ((unsigned)i0x < (unsigned)(nx - 1)) & ((unsigned)i0y < (unsigned)(ny - 1)) &
-                        ((unsigned)i0z < (unsigned)(nz - 1));
-    if (!inside) {
-      // O5 clamp: x <= 0 -> corner 0 (f = 0); x >= n-1 -> corner n-1 (i0 = n-2, f = 1)
-      if (i0x < 0 || (i0x == 0 && fx == 0.f)) { i0x = 0; fx = 0.f; } else if (i0x >= nx - 1) { i0x = nx - 2; fx = 1.f; }
-      if (i0y < 0 || (i0y == 0 && fy == 0.f)) { i0y = 0; fy = 0.f; } else if (i0y >= ny - 1) { i0y = ny - 2; fy = 1.f; }
-      if (i0z < 0 || (i0z == 0 && fz == 0.f)) { i0z = 0; fz = 0.f; } else if (i0z >= nz - 1) { i0z = nz - 2; fz = 1.f; }
-    }
-    const int base = (i0z * ny + i0y) * nx + i0x;
-    float cc[8];
-    corners(Ioth, tex_oth, base, i0x, i0y, i0z, cc);
-    const float c000 = cc[0], c100 = cc[1], c010 = cc[2], c110 = cc[3];
-    const float c001 = cc[4], c101 = cc[5], c011 = cc[6], c111 = cc[7];
-    const float b = lerpf(lerpf(lerpf(c000, c100, fx), lerpf(c010, c110, fx), fy),
-                          lerpf(lerpf(c001, c101, fx), lerpf(c011, c111, fx), fy), fz);
-    bool fg;
-    if (amb) {
-      fg = exact_fg(R, qx, qy, qz, dx, dy, dz, Ioth, nx, ny, nz);
-    } else if (NOEXACT && inside) {
-      // all 8 corners contribute; values are >= 0, so the sum is > 0 iff one is
-      fg = ((c000 + c100) + (c010 + c110)) + ((c001 + c101) + (c011 + c111)) > 0.f;
+    const bool amb = (fabsf(fx - 0.5f) > ex) | (fabsf(fy - 0.5f) > ey) | (fabsf(fz - 0.5f) > ez);
+    // lattice corner i0 as exact floats (< 2^24); O5 clamp: x <= 0 -> (0, f = 0),
+    // x >= n-1 -> (n-2, f = 1)
+    float ix = rp.x + kf + flx, iy = rp.y + fly, iz = rp.z + flz;
+    const float mx = (float)(nx - 2), my = (float)(ny - 2), mz = (float)(nz - 2);
+    fx = ix < 0.f ? 0.f : (ix > mx ? 1.f : fx);
+    fy = iy < 0.f ? 0.f : (iy > my ? 1.f : fy);
+    fz = iz < 0.f ? 0.f : (iz > mz ? 1.f : fz);
+    ix = fminf(fmaxf(ix, 0.f), mx);
+    iy = fminf(fmaxf(iy, 0.f), my);
+    iz = fminf(fmaxf(iz, 0.f), mz);
+    const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
+    float u = 0.f, v = 0.f;
+    int base = 0;
+    if (TEX) {
+      u = ix + 1.0f;
+      v = fmaf(iz, (float)ny, iy) + 1.0f;
     } else {
-      // contributing corners: lower corner iff f < 1, upper corner iff f > 0 (per axis)
-      const unsigned m = (c000 > 0.f) | ((c100 > 0.f) << 1) | ((c010 > 0.f) << 2) |
-                         ((c110 > 0.f) << 3) | ((c001 > 0.f) << 4) | ((c101 > 0.f) << 5) |
-                         ((c011 > 0.f) << 6) | ((c111 > 0.f) << 7);
-      const unsigned mx = (fx < 1.f ? 0x55u : 0u) | (fx > 0.f ? 0xAAu : 0u);
-      const unsigned my = (fy < 1.f ? 0x33u : 0u) | (fy > 0.f ? 0xCCu : 0u);
-      const unsigned mz = (fz < 1.f ? 0x0Fu : 0u) | (fz > 0.f ? 0xF0u : 0u);
-      fg = (m & mx & my & mz) != 0u;
+      base = ((int)iz * ny + (int)iy) * nx + (int)ix;
     }
+    float c[8];
+    gather(Ioth, tex_oth, u, v, base, c);
+    const float b = tri(c, fx, fy, fz, gx, gy, gz);
+    bool fg = b > 0.f;
+    if (amb) fg = exact_fg(R, ri.z + k, ri.w & 0xffff, ri.w >> 16, dx, dy, dz, Ioth, nx, ny, nz);
     // h of PAPER.md §4.1.2 (L318-322) with the exact case split (O6)
     float h;
     if (a > 0.f && fg) {
@@ -597,23 +615,22 @@ struct Sample {
     } else {
       h = (a == 0.f && !fg) ? 0.f : 1.f;
     }
-    h_sum += (double)h;
-    n += 1;
-    // pairs in a warp-uniform order: a texture instruction needs the same handle on
-    // every executing lane, so loop over the OR of the active lanes' band bits
-    unsigned wbm = __reduce_or_sync(__activemask(), bm0);
+    if (valid) {
+      h_sum += (double)h;
+      n += 1;
+    }
+    // a6: guidance over the band bits, pairs in a warp-uniform order (a texture
+    // instruction needs the same handle on every executing lane)
+    unsigned wbm = __reduce_or_sync(FULLMASK, bm);
     while (wbm) {
       const int i = __ffs(wbm) - 1;
       wbm &= wbm - 1;
-      if (!((bm0 >> i) & 1u)) continue;
+      if (!((bm >> i) & 1u)) continue;
       nb += 1;
       const float d = __ldg(&dmap_own[(long long)i * V + lin]);
-      float ee[8];
-      corners(dmap_oth + (long long)i * V, TEX ? __ldg(&tex_moth[i]) : 0ull, base, i0x, i0y, i0z, ee);
-      const float e000 = ee[0], e100 = ee[1], e010 = ee[2], e110 = ee[3];
-      const float e001 = ee[4], e101 = ee[5], e011 = ee[6], e111 = ee[7];
-      const float Dp = lerpf(lerpf(lerpf(e000, e100, fx), lerpf(e010, e110, fx), fy),
-                             lerpf(lerpf(e001, e101, fx), lerpf(e011, e111, fx), fy), fz);
+      float e[8];
+      gather(dmap_oth + (long long)i * V, TEX ? __ldg(&tex_moth[i]) : 0ull, u, v, base, e);
+      const float Dp = tri(e, fx, fy, fz, gx, gy, gz);
       const double dd = (double)d - (double)Dp;
       // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit)
       g_sum += __ldg(&w[i]) * ((r - (double)d) * inv_r) * dd * dd;
@@ -641,14 +658,14 @@ __device__ __forceinline__ void load_rec(WarpSmem& S, const SideRec* src, int la
   __syncwarp();
 }
 
-template <bool FAST, bool TEX>
+template <bool TEX>
 __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int lane, int s,
                                             double& h_sum, double& g_sum, int& n, int& nb) {
   const SideRec& R = S.R;
-  Sample<FAST, TEX> f{R, V.I[s], V.I[1 - s], V.band[s], V.dmap[s], V.dmap[1 - s], (int)V.V, V.nx,
-                      V.ny, V.nz, R.A[0][0], R.A[1][0], R.A[2][0], R.eps[0], R.eps[1],
-                      R.eps[2], V.r, 1.0 / V.r, V.w + s * kMaxPairs, 0.0, 0.0, 0, 0,
-                      TEX ? V.texI[1 - s] : 0ull, TEX ? V.texD + (1 - s) * kMaxPairs : nullptr};
+  Sample<TEX> f{R, V.I[s], V.I[1 - s], V.band[s], V.dmap[s], V.dmap[1 - s], (int)V.V, V.nx,
+                V.ny, V.nz, R.A[0][0], R.A[1][0], R.A[2][0], 0.5f - R.eps[0], 0.5f - R.eps[1],
+                0.5f - R.eps[2], V.r, 1.0 / V.r, V.w + s * kMaxPairs, 0.0, 0.0, 0, 0,
+                TEX ? V.texI[1 - s] : 0ull, TEX ? V.texD + (1 - s) * kMaxPairs : nullptr};
   raster(R, V.nx, V.ny, S, lane, f);
   h_sum += f.h_sum;
   g_sum += f.g_sum;
@@ -685,8 +702,7 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
       load_rec(S, &A.geom[2 * i + s], lane);
       const int fl = S.R.flags;
       if (!(fl & 1)) continue;
-      if (fl & 2) raster_side<true, TEX>(A.vol, S, lane, s, h_sum, g_sum, n, nb);
-      else raster_side<false, TEX>(A.vol, S, lane, s, h_sum, g_sum, n, nb);
+      raster_side<TEX>(A.vol, S, lane, s, h_sum, g_sum, n, nb);
     }
     HGN out;
     out.h = warp_sum_d(h_sum);
@@ -904,7 +920,9 @@ cudaError_t launch_check_folds(const MeshDev& m, const double sp[3], int P, cons
 struct OwnerSample {
   int* owner;
   int tet;
-  __device__ __forceinline__ void operator()(const int4& ri, const float4&, int k) {
+  __device__ __forceinline__ void sample(const int4& ri, const float4&, const float4&, int k,
+                                         bool valid) {
+    if (!valid) return;
     const int lin = ri.y + k;
     const int old = atomicCAS(&owner[lin], -1, tet);
     if (old != -1) atomicExch(&owner[lin], -2);
@@ -946,7 +964,8 @@ __global__ void k_validate_volume(const float* __restrict__ I, long long V, int*
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < V;
        i += (long long)gridDim.x * blockDim.x) {
     const float v = I[i];
-    if (!(v >= 0.0f) || isinf(v)) atomicOr(bad, 1);
+    // finite, >= 0, and either exactly 0 (background) or >= 2^-40
+    if (!(v >= 0.0f) || isinf(v) || (v > 0.0f && v < 9.094947017729282e-13f)) atomicOr(bad, 1);
   }
 }
 
