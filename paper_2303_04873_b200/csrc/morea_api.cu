@@ -225,11 +225,20 @@ Volumes volumes_of(const morea_ctx* c) {
   }
   v.K = c->K;
   v.r = c->r;
+  v.inv_r = c->r > 0 ? 1.0 / c->r : 0.0;
+  v.fnx2 = (float)(c->nx - 2);
+  v.fny2 = (float)(c->ny - 2);
+  v.fnz2 = (float)(c->nz - 2);
+  v.fny = (float)c->ny;
   v.w = c->wts.as<double>();
   v.use_tex = c->use_tex ? 1 : 0;
   v.texI[0] = c->texI[0];
   v.texI[1] = c->texI[1];
-  v.texD = c->use_tex ? c->tex_handles.as<unsigned long long>() : nullptr;
+  for (int s = 0; s < 2; s++)
+    for (int i = 0; i < kMaxPairs; i++) v.texD[s][i] = 0ull;
+  if (c->use_tex)
+    for (int s = 0; s < 2; s++)
+      for (int i = 0; i < c->K; i++) v.texD[s][i] = (unsigned long long)c->texD[s * c->K + i];
   return v;
 }
 

@@ -26,7 +26,8 @@ struct __align__(16) SideRec {
   float A[3][3];              // displacement gradient du_a / dq_b
   float d0[3];                // displacement at lo
   float eps[3];               // fp32 position filter bound per axis (0 = exact axis)
-  int flags;                  // bit 0: rasterize; bit 1: no exact axis
+  int flags;                  // bit 0: rasterize; bit 1: every position of the bbox is inside
+                              // [0, n-1) with margin (no clamp needed)
   float vy[4], vz[4];         // vertex y, z (voxel units, exact) for per-slice y ranges
   int lo[3], hi[3];           // lattice bbox clipped to the image
   int U[4][3];                // Q_other - Q_own per vertex
@@ -57,12 +58,13 @@ struct Volumes {
   const unsigned char* band[2];  // per voxel bit i = [D_i(q) < r]; nullptr when K == 0
   const float* dmap[2];          // K * V fp32 per side
   int K;
-  double r;
+  double r, inv_r;
+  float fnx2, fny2, fnz2, fny;  // (n - 2) per axis and ny as floats (constant-bank operands)
   const double* w;  // device: w[side * kMaxPairs + i] = |C_i| / |G_side|
   // texture-gather path: I_s / I_t and the maps as tall 2D textures (texel (x, y + ny z)),
   // gathered 2x2 per slice (tld4); 0 / nullptr when the volume exceeds the gather limits
   unsigned long long texI[2];
-  const unsigned long long* texD;  // [side * kMaxPairs + i]
+  unsigned long long texD[2][kMaxPairs];  // in the parameter space: uniform (constant-bank) loads
   int use_tex;
 };
 

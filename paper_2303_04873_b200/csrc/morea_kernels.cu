@@ -27,8 +27,12 @@
 #include "morea.h"
 #include "morea_internal.h"
 
+#ifndef MOREA_SPLIT_CLAMP
+#define MOREA_SPLIT_CLAMP 0  // separate no-clamp sample loop for items far from the border
+#endif
+
 #ifndef MOREA_RASTER_MINB
-#define MOREA_RASTER_MINB 4  // resident 256-thread blocks per SM the register budget targets
+#define MOREA_RASTER_MINB 3  // resident 256-thread blocks per SM the register budget targets
 #endif
 
 namespace morea {
@@ -146,7 +150,7 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
 #pragma unroll
   for (int k = 0; k < 4; k++)
     elo[k] = 1024 * (G.nrm[k][0] * G.lo[0] + G.nrm[k][1] * G.lo[1] + G.nrm[k][2] * G.lo[2]) - G.cst[k];
-  bool any_exact = false;
+  bool inside = true;
 #pragma unroll
   for (int a = 0; a < 3; a++) {
     bool exact = true;
@@ -164,27 +168,33 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
       // every vertex moves by the same U_a: x_a = q_a + U_a / 1024 exactly (fp32-exact)
       G.d0[a] = (float)G.U[0][a] * (1.0f / 1024.0f);
       G.eps[a] = 0.0f;
-      any_exact = true;
+      const double u = (double)G.U[0][a] / 1024.0;
+      if (!((double)G.lo[a] + u >= 1e-3 && (double)G.hi[a] + u <= (double)(dims[a] - 1) - 1e-3)) inside = false;
     } else {
       i128 N = 0;
 #pragma unroll
       for (int k = 0; k < 4; k++) N += (i128)elo[k] * (i128)G.U[k][a];
       const double d0 = (double)N / (1024.0 * (double)G.absdet);
       G.d0[a] = (float)d0;
-      double amax = fabs(d0);
+      double amax = 0.0, xmin = 1e300, xmax = -1e300;
 #pragma unroll
-      for (int c = 1; c < 8; c++) {
+      for (int c = 0; c < 8; c++) {
         const double v = d0 + Aab[0] * ((c & 1) ? L[0] : 0.0) + Aab[1] * ((c & 2) ? L[1] : 0.0) +
                          Aab[2] * ((c & 4) ? L[2] : 0.0);
         amax = fmax(amax, fabs(v));
+        const double xq = v + (double)(((c >> a) & 1) ? G.hi[a] : G.lo[a]);
+        xmin = fmin(xmin, xq);
+        xmax = fmax(xmax, xq);
       }
+      // positions are affine over the bbox: extremes at its corners
+      if (!(xmin >= 1e-3 && xmax <= (double)(dims[a] - 1) - 1e-3)) inside = false;
       // fp32 error of d = fma(A_x0, k, d_row(fp32 fma chain)) and of frac(d):
       // <= 2^-24 (5 (|u|max + sum_b |A_ab| L_b) + 1); eps = 3x that
       const double bound = amax + fabs(Aab[0]) * L[0] + fabs(Aab[1]) * L[1] + fabs(Aab[2]) * L[2] + 1.0;
       G.eps[a] = (float)ldexp(bound, -19);
     }
   }
-  G.flags = 1 | (any_exact ? 0 : 2);
+  G.flags = 1 | (inside ? 2 : 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -385,6 +395,7 @@ struct WarpSmem {
   int4 row_i[32];    // (exclusive prefix, linear index of row start, xl, y | z << 16)
   float4 row_d[32];  // fp32 displacement at the row start
   float4 row_p[32];  // row start as floats: (xl, y, z, z * ny + y)
+  float4 sc0, sc1;   // per-side sample constants (see Sample)
 };
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -527,39 +538,32 @@ __device__ __forceinline__ float plerp(float a, float b, float t, float omt) {
   return fmaf(t, b, omt * a);
 }
 
-// a5 + a6: one sample of one side.  The footprint weights are exact: 0 / 1 on
+// a5 + a6: one sample of side SIDE.  The footprint weights are exact: 0 / 1 on
 // clamped axes and exact-integer axes, and in [eps, 1 - eps] otherwise unless the
 // position is ambiguous (then exact_fg decides), so fg = (b > 0) is exact.
-template <bool TEX>
+// Volume pointers and texture handles are read from the kernel parameters with
+// compile-time offsets (constant bank): no registers, and texture handles are
+// provably warp-uniform (no waterfall loop around tld4).
+template <bool TEX, int SIDE, bool CLAMP>
 struct Sample {
+  const Volumes& V;
   const SideRec& R;
-  const float* __restrict__ Iown;
-  const float* __restrict__ Ioth;
-  const unsigned char* __restrict__ band;
-  const float* __restrict__ dmap_own;
-  const float* __restrict__ dmap_oth;
-  int V;
-  int nx, ny, nz;
-  float ax, ay, az;  // displacement gradient along x (fp32)
-  float ex, ey, ez;  // 0.5 - eps per axis (ambiguity threshold on |f - 0.5|)
-  double r, inv_r;
-  const double* w;   // pair weights of this side
+  const float4& sc0;  // shared: (A_x0, A_y0, A_z0, 0.5 - eps_x)  displacement gradient along x
+  const float4& sc1;  // shared: (0.5 - eps_y, 0.5 - eps_z, -, -)  ambiguity thresholds on |f - 0.5|
   double h_sum, g_sum;
   int n, nb;
-  unsigned long long tex_oth;          // gather texture of the other volume
-  const unsigned long long* tex_moth;  // gather textures of the other side's maps
 
   // the 8 corners (i0 .. i0+1)^3: two 2x2 texture gathers (tld4) or 8 loads
   __device__ __forceinline__ void gather(const float* __restrict__ vol, unsigned long long tex,
                                          float u, float v, int base, float c[8]) const {
     if (TEX) {
       const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v, 0);
-      const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v + (float)ny, 0);
+      const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v + V.fny, 0);
       // gather order: (x0,y1) (x1,y1) (x1,y0) (x0,y0)
       c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
       c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
     } else {
-      const int sy = nx, sz = nx * ny;
+      const int sy = V.nx, sz = V.nx * V.ny;
       c[0] = __ldg(&vol[base]); c[1] = __ldg(&vol[base + 1]);
       c[2] = __ldg(&vol[base + sy]); c[3] = __ldg(&vol[base + sy + 1]);
       c[4] = __ldg(&vol[base + sz]); c[5] = __ldg(&vol[base + sz + 1]);
@@ -567,46 +571,51 @@ struct Sample {
     }
   }
 
-  __device__ __forceinline__ float tri(const float c[8], float fx, float fy, float fz, float gx,
-                                       float gy, float gz) const {
+  __device__ __forceinline__ static float tri(const float c[8], float fx, float fy, float fz,
+                                              float gx, float gy, float gz) {
     return plerp(plerp(plerp(c[0], c[1], fx, gx), plerp(c[2], c[3], fx, gx), fy, gy),
                  plerp(plerp(c[4], c[5], fx, gx), plerp(c[6], c[7], fx, gx), fy, gy), fz, gz);
   }
 
   __device__ __forceinline__ void sample(const int4& ri, const float4& rd, const float4& rp, int k,
                                          bool valid) {
+    constexpr int OTH = 1 - SIDE;
+    const int nx = V.nx, ny = V.ny, nz = V.nz;
     const int lin = ri.y + k;
-    const float a = __ldg(&Iown[lin]);
-    const unsigned bm = (band && valid) ? (unsigned)__ldg(&band[lin]) : 0u;
+    const float a = __ldg(&V.I[SIDE][lin]);
+    const unsigned bm = (V.K > 0 && valid) ? (unsigned)__ldg(&V.band[SIDE][lin]) : 0u;
     const float kf = (float)k;
-    const float dx = fmaf(ax, kf, rd.x), dy = fmaf(ay, kf, rd.y), dz = fmaf(az, kf, rd.z);
+    const float4 s0 = sc0;
+    const float dx = fmaf(s0.x, kf, rd.x), dy = fmaf(s0.y, kf, rd.y), dz = fmaf(s0.z, kf, rd.z);
     const float flx = floorf(dx), fly = floorf(dy), flz = floorf(dz);
     float fx = dx - flx, fy = dy - fly, fz = dz - flz;
-    const bool amb = (fabsf(fx - 0.5f) > ex) | (fabsf(fy - 0.5f) > ey) | (fabsf(fz - 0.5f) > ez);
-    // lattice corner i0 as exact floats (< 2^24); O5 clamp: x <= 0 -> (0, f = 0),
-    // x >= n-1 -> (n-2, f = 1)
+    const float4 s1 = sc1;
+    const bool amb = (fabsf(fx - 0.5f) > s0.w) | (fabsf(fy - 0.5f) > s1.x) | (fabsf(fz - 0.5f) > s1.y);
+    // lattice corner i0 as exact floats (< 2^24)
     float ix = rp.x + kf + flx, iy = rp.y + fly, iz = rp.z + flz;
-    const float mx = (float)(nx - 2), my = (float)(ny - 2), mz = (float)(nz - 2);
-    fx = ix < 0.f ? 0.f : (ix > mx ? 1.f : fx);
-    fy = iy < 0.f ? 0.f : (iy > my ? 1.f : fy);
-    fz = iz < 0.f ? 0.f : (iz > mz ? 1.f : fz);
-    ix = fminf(fmaxf(ix, 0.f), mx);
-    iy = fminf(fmaxf(iy, 0.f), my);
-    iz = fminf(fmaxf(iz, 0.f), mz);
+    if (CLAMP) {
+      // O5 clamp: x <= 0 -> (0, f = 0), x >= n-1 -> (n-2, f = 1)
+      fx = ix < 0.f ? 0.f : (ix > V.fnx2 ? 1.f : fx);
+      fy = iy < 0.f ? 0.f : (iy > V.fny2 ? 1.f : fy);
+      fz = iz < 0.f ? 0.f : (iz > V.fnz2 ? 1.f : fz);
+      ix = fminf(fmaxf(ix, 0.f), V.fnx2);
+      iy = fminf(fmaxf(iy, 0.f), V.fny2);
+      iz = fminf(fmaxf(iz, 0.f), V.fnz2);
+    }
     const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
     float u = 0.f, v = 0.f;
     int base = 0;
     if (TEX) {
       u = ix + 1.0f;
-      v = fmaf(iz, (float)ny, iy) + 1.0f;
+      v = fmaf(iz, V.fny, iy) + 1.0f;
     } else {
       base = ((int)iz * ny + (int)iy) * nx + (int)ix;
     }
     float c[8];
-    gather(Ioth, tex_oth, u, v, base, c);
+    gather(V.I[OTH], TEX ? V.texI[OTH] : 0ull, u, v, base, c);
     const float b = tri(c, fx, fy, fz, gx, gy, gz);
     bool fg = b > 0.f;
-    if (amb) fg = exact_fg(R, ri.z + k, ri.w & 0xffff, ri.w >> 16, dx, dy, dz, Ioth, nx, ny, nz);
+    if (amb) fg = exact_fg(R, ri.z + k, ri.w & 0xffff, ri.w >> 16, dx, dy, dz, V.I[OTH], nx, ny, nz);
     // h of PAPER.md §4.1.2 (L318-322) with the exact case split (O6)
     float h;
     if (a > 0.f && fg) {
@@ -627,13 +636,13 @@ struct Sample {
       wbm &= wbm - 1;
       if (!((bm >> i) & 1u)) continue;
       nb += 1;
-      const float d = __ldg(&dmap_own[(long long)i * V + lin]);
+      const float d = __ldg(&V.dmap[SIDE][(long long)i * V.V + lin]);
       float e[8];
-      gather(dmap_oth + (long long)i * V, TEX ? __ldg(&tex_moth[i]) : 0ull, u, v, base, e);
+      gather(V.dmap[OTH] + (long long)i * V.V, TEX ? V.texD[OTH][i] : 0ull, u, v, base, e);
       const float Dp = tri(e, fx, fy, fz, gx, gy, gz);
       const double dd = (double)d - (double)Dp;
       // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit)
-      g_sum += __ldg(&w[i]) * ((r - (double)d) * inv_r) * dd * dd;
+      g_sum += __ldg(&V.w[SIDE * kMaxPairs + i]) * ((V.r - (double)d) * V.inv_r) * dd * dd;
     }
   }
 };
@@ -658,19 +667,31 @@ __device__ __forceinline__ void load_rec(WarpSmem& S, const SideRec* src, int la
   __syncwarp();
 }
 
-template <bool TEX>
-__device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int lane, int s,
-                                            double& h_sum, double& g_sum, int& n, int& nb) {
+template <bool TEX, int SIDE, bool CLAMP>
+__device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int lane, double& h_sum,
+                                            double& g_sum, int& n, int& nb) {
   const SideRec& R = S.R;
-  Sample<TEX> f{R, V.I[s], V.I[1 - s], V.band[s], V.dmap[s], V.dmap[1 - s], (int)V.V, V.nx,
-                V.ny, V.nz, R.A[0][0], R.A[1][0], R.A[2][0], 0.5f - R.eps[0], 0.5f - R.eps[1],
-                0.5f - R.eps[2], V.r, 1.0 / V.r, V.w + s * kMaxPairs, 0.0, 0.0, 0, 0,
-                TEX ? V.texI[1 - s] : 0ull, TEX ? V.texD + (1 - s) * kMaxPairs : nullptr};
+  if (lane == 0) {
+    S.sc0 = make_float4(R.A[0][0], R.A[1][0], R.A[2][0], 0.5f - R.eps[0]);
+    S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], 0.f, 0.f);
+  }
+  __syncwarp();
+  Sample<TEX, SIDE, CLAMP> f{V, R, S.sc0, S.sc1, 0.0, 0.0, 0, 0};
   raster(R, V.nx, V.ny, S, lane, f);
   h_sum += f.h_sum;
   g_sum += f.g_sum;
   n += f.n;
   nb += f.nb;
+}
+
+template <bool TEX, int SIDE>
+__device__ __forceinline__ void raster_side_any(const Volumes& V, WarpSmem& S, int lane,
+                                                double& h_sum, double& g_sum, int& n, int& nb) {
+#if MOREA_SPLIT_CLAMP
+  if (S.R.flags & 2) raster_side<TEX, SIDE, false>(V, S, lane, h_sum, g_sum, n, nb);
+  else
+#endif
+    raster_side<TEX, SIDE, true>(V, S, lane, h_sum, g_sum, n, nb);
 }
 
 // ---------------------------------------------------------------------------
@@ -697,13 +718,10 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
     const long long i = ((long long)v * A.n_entries + e) * A.P + sol;
     double h_sum = 0.0, g_sum = 0.0;
     int n = 0, nb = 0;
-#pragma unroll 1
-    for (int s = 0; s < 2; s++) {
-      load_rec(S, &A.geom[2 * i + s], lane);
-      const int fl = S.R.flags;
-      if (!(fl & 1)) continue;
-      raster_side<TEX>(A.vol, S, lane, s, h_sum, g_sum, n, nb);
-    }
+    load_rec(S, &A.geom[2 * i], lane);
+    if (S.R.flags & 1) raster_side_any<TEX, 0>(A.vol, S, lane, h_sum, g_sum, n, nb);
+    load_rec(S, &A.geom[2 * i + 1], lane);
+    if (S.R.flags & 1) raster_side_any<TEX, 1>(A.vol, S, lane, h_sum, g_sum, n, nb);
     HGN out;
     out.h = warp_sum_d(h_sum);
     out.g = warp_sum_d(g_sum);
