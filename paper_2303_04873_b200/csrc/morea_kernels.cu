@@ -27,10 +27,6 @@
 #include "morea.h"
 #include "morea_internal.h"
 
-#ifndef MOREA_SPLIT_CLAMP
-#define MOREA_SPLIT_CLAMP 0  // separate no-clamp sample loop for items far from the border
-#endif
-
 #ifndef MOREA_RASTER_MINB
 #define MOREA_RASTER_MINB 3  // resident 256-thread blocks per SM the register budget targets
 #endif
@@ -396,6 +392,7 @@ struct WarpSmem {
   float4 row_d[32];  // fp32 displacement at the row start
   float4 row_p[32];  // row start as floats: (xl, y, z, z * ny + y)
   float4 sc0, sc1;   // per-side sample constants (see Sample)
+  unsigned long long stat[3];  // samples, band entries, items of this warp (profiling)
 };
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -544,14 +541,19 @@ __device__ __forceinline__ float plerp(float a, float b, float t, float omt) {
 // Volume pointers and texture handles are read from the kernel parameters with
 // compile-time offsets (constant bank): no registers, and texture handles are
 // provably warp-uniform (no waterfall loop around tld4).
-template <bool TEX, int SIDE, bool CLAMP>
+struct Acc {
+  double h, g;  // per-lane sums of h and of the guidance term (fp64)
+  int n, nb;    // samples, band entries
+};
+
+template <bool TEX, int SIDE>
 struct Sample {
   const Volumes& V;
   const SideRec& R;
   const float4& sc0;  // shared: (A_x0, A_y0, A_z0, 0.5 - eps_x)  displacement gradient along x
   const float4& sc1;  // shared: (0.5 - eps_y, 0.5 - eps_z, -, -)  ambiguity thresholds on |f - 0.5|
-  double h_sum, g_sum;
-  int n, nb;
+  Acc& acc;
+  bool clamp;         // some position of the item may leave [0, n-1): apply the O5 clamp
 
   // the 8 corners (i0 .. i0+1)^3: two 2x2 texture gathers (tld4) or 8 loads
   __device__ __forceinline__ void gather(const float* __restrict__ vol, unsigned long long tex,
@@ -593,7 +595,7 @@ struct Sample {
     const bool amb = (fabsf(fx - 0.5f) > s0.w) | (fabsf(fy - 0.5f) > s1.x) | (fabsf(fz - 0.5f) > s1.y);
     // lattice corner i0 as exact floats (< 2^24)
     float ix = rp.x + kf + flx, iy = rp.y + fly, iz = rp.z + flz;
-    if (CLAMP) {
+    if (clamp) {  // warp-uniform
       // O5 clamp: x <= 0 -> (0, f = 0), x >= n-1 -> (n-2, f = 1)
       fx = ix < 0.f ? 0.f : (ix > V.fnx2 ? 1.f : fx);
       fy = iy < 0.f ? 0.f : (iy > V.fny2 ? 1.f : fy);
@@ -625,8 +627,8 @@ struct Sample {
       h = (a == 0.f && !fg) ? 0.f : 1.f;
     }
     if (valid) {
-      h_sum += (double)h;
-      n += 1;
+      acc.h += (double)h;
+      acc.n += 1;
     }
     // a6: guidance over the band bits, pairs in a warp-uniform order (a texture
     // instruction needs the same handle on every executing lane)
@@ -635,14 +637,14 @@ struct Sample {
       const int i = __ffs(wbm) - 1;
       wbm &= wbm - 1;
       if (!((bm >> i) & 1u)) continue;
-      nb += 1;
+      acc.nb += 1;
       const float d = __ldg(&V.dmap[SIDE][(long long)i * V.V + lin]);
       float e[8];
       gather(V.dmap[OTH] + (long long)i * V.V, TEX ? V.texD[OTH][i] : 0ull, u, v, base, e);
       const float Dp = tri(e, fx, fy, fz, gx, gy, gz);
       const double dd = (double)d - (double)Dp;
       // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit)
-      g_sum += __ldg(&V.w[SIDE * kMaxPairs + i]) * ((V.r - (double)d) * V.inv_r) * dd * dd;
+      acc.g += __ldg(&V.w[SIDE * kMaxPairs + i]) * ((V.r - (double)d) * V.inv_r) * dd * dd;
     }
   }
 };
@@ -667,31 +669,16 @@ __device__ __forceinline__ void load_rec(WarpSmem& S, const SideRec* src, int la
   __syncwarp();
 }
 
-template <bool TEX, int SIDE, bool CLAMP>
-__device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int lane, double& h_sum,
-                                            double& g_sum, int& n, int& nb) {
+template <bool TEX, int SIDE>
+__device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int lane, Acc& acc) {
   const SideRec& R = S.R;
   if (lane == 0) {
     S.sc0 = make_float4(R.A[0][0], R.A[1][0], R.A[2][0], 0.5f - R.eps[0]);
     S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], 0.f, 0.f);
   }
   __syncwarp();
-  Sample<TEX, SIDE, CLAMP> f{V, R, S.sc0, S.sc1, 0.0, 0.0, 0, 0};
+  Sample<TEX, SIDE> f{V, R, S.sc0, S.sc1, acc, (R.flags & 2) == 0};
   raster(R, V.nx, V.ny, S, lane, f);
-  h_sum += f.h_sum;
-  g_sum += f.g_sum;
-  n += f.n;
-  nb += f.nb;
-}
-
-template <bool TEX, int SIDE>
-__device__ __forceinline__ void raster_side_any(const Volumes& V, WarpSmem& S, int lane,
-                                                double& h_sum, double& g_sum, int& n, int& nb) {
-#if MOREA_SPLIT_CLAMP
-  if (S.R.flags & 2) raster_side<TEX, SIDE, false>(V, S, lane, h_sum, g_sum, n, nb);
-  else
-#endif
-    raster_side<TEX, SIDE, true>(V, S, lane, h_sum, g_sum, n, nb);
 }
 
 // ---------------------------------------------------------------------------
@@ -704,7 +691,7 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
   WarpSmem& S = smem[warp];
   const long long per_v = (long long)A.n_entries * A.P;
   const long long n_items = per_v * A.n_raster_versions;
-  unsigned long long my_samples = 0, my_band = 0, my_items = 0;
+  if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0ull;
   while (true) {
     unsigned long long item = 0;
     if (lane == 0) item = atomicAdd(A.counter, 1ULL);
@@ -716,28 +703,27 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
     const int sol = (int)(rem - (long long)es * A.P);
     const int e = A.sched[es];
     const long long i = ((long long)v * A.n_entries + e) * A.P + sol;
-    double h_sum = 0.0, g_sum = 0.0;
-    int n = 0, nb = 0;
+    Acc acc{0.0, 0.0, 0, 0};
     load_rec(S, &A.geom[2 * i], lane);
-    if (S.R.flags & 1) raster_side_any<TEX, 0>(A.vol, S, lane, h_sum, g_sum, n, nb);
+    if (S.R.flags & 1) raster_side<TEX, 0>(A.vol, S, lane, acc);
     load_rec(S, &A.geom[2 * i + 1], lane);
-    if (S.R.flags & 1) raster_side_any<TEX, 1>(A.vol, S, lane, h_sum, g_sum, n, nb);
+    if (S.R.flags & 1) raster_side<TEX, 1>(A.vol, S, lane, acc);
     HGN out;
-    out.h = warp_sum_d(h_sum);
-    out.g = warp_sum_d(g_sum);
-    out.n = warp_sum_i(n);
-    out.nb = warp_sum_i(nb);
+    out.h = warp_sum_d(acc.h);
+    out.g = warp_sum_d(acc.g);
+    out.n = warp_sum_i(acc.n);
+    out.nb = warp_sum_i(acc.nb);
     if (lane == 0) {
       A.hgn[i] = out;
-      my_samples += out.n;
-      my_band += out.nb;
-      my_items += 1;
+      S.stat[0] += out.n;
+      S.stat[1] += out.nb;
+      S.stat[2] += 1;
     }
   }
   if (lane == 0 && A.stats) {
-    atomicAdd(&A.stats[0], my_samples);
-    atomicAdd(&A.stats[1], my_band);
-    atomicAdd(&A.stats[2], my_items);
+    atomicAdd(&A.stats[0], S.stat[0]);
+    atomicAdd(&A.stats[1], S.stat[1]);
+    atomicAdd(&A.stats[2], S.stat[2]);
   }
 }
 
