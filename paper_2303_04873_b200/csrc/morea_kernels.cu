@@ -27,6 +27,10 @@
 #include "morea.h"
 #include "morea_internal.h"
 
+#ifndef MOREA_SIDE_TEMPLATE
+#define MOREA_SIDE_TEMPLATE 0  // 1: one sample-loop instantiation per side (twice the code)
+#endif
+
 #ifndef MOREA_RASTER_MINB
 #define MOREA_RASTER_MINB 3  // resident 256-thread blocks per SM the register budget targets
 #endif
@@ -313,7 +317,7 @@ __device__ __forceinline__ i64 face_e(const SideRec& R, int k, int x, int y, int
   return 1024 * (R.nrm[k][0] * x + R.nrm[k][1] * y + R.nrm[k][2] * z) - R.cst[k];
 }
 
-__device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, int& xl, int& xh) {
+__device__ __noinline__ void row_interval(const SideRec& R, int y, int z, int& xl, int& xh) {
   const int lo = R.lo[0], hi = R.hi[0];
   xl = lo;
   xh = hi;
@@ -360,7 +364,7 @@ __device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, int
 
 // Conservative y range of the tet's cross-section with the plane z (exact
 // vertex coordinates; edge intersections in fp32 with a 1e-3 voxel margin).
-__device__ __forceinline__ void slice_y_range(const SideRec& R, int z, int& ylo, int& yhi) {
+__device__ __noinline__ void slice_y_range(const SideRec& R, int z, int& ylo, int& yhi) {
   float ymin = 3.0e38f, ymax = -3.0e38f;
   const float zf = (float)z;
 #pragma unroll
@@ -388,9 +392,8 @@ __device__ __forceinline__ void slice_y_range(const SideRec& R, int z, int& ylo,
 
 struct WarpSmem {
   SideRec R;
-  int4 row_i[32];    // (exclusive prefix, linear index of row start, xl, y | z << 16)
-  float4 row_d[32];  // fp32 displacement at the row start
-  float4 row_p[32];  // row start as floats: (xl, y, z, z * ny + y)
+  int4 row_a[32];    // (exclusive prefix, linear index of row start, dx0, dy0 as float bits)
+  float4 row_b[32];  // (dz0, xl, y, z): fp32 displacement z at the row start, row start as floats
   float4 sc0, sc1;   // per-side sample constants (see Sample)
   unsigned long long stat[3];  // samples, band entries, items of this warp (profiling)
 };
@@ -461,9 +464,8 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, WarpSme
         drow.y = fmaf(R.A[1][2], oz, fmaf(R.A[1][1], oy, fmaf(R.A[1][0], ox, R.d0[1])));
         drow.z = fmaf(R.A[2][2], oz, fmaf(R.A[2][1], oy, fmaf(R.A[2][0], ox, R.d0[2])));
         drow.w = 0.f;
-        S.row_i[c] = make_int4(start, (z * ny + y) * nx + xl, xl, y | (z << 16));
-        S.row_d[c] = drow;
-        S.row_p[c] = make_float4((float)xl, (float)y, (float)z, 0.f);
+        S.row_a[c] = make_int4(start, (z * ny + y) * nx + xl, __float_as_int(drow.x), __float_as_int(drow.y));
+        S.row_b[c] = make_float4(drow.z, (float)xl, (float)y, (float)z);
       }
       __syncwarp();
       const int last = __popc(ne) - 1;
@@ -475,8 +477,8 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, WarpSme
         rprev += __popc(M);
         const int idx = s0 + lane;
         const bool valid = idx < total;
-        const int4 ri = S.row_i[row];
-        f.sample(ri, S.row_d[row], S.row_p[row], valid ? idx - ri.x : 0, valid);
+        const int4 ra = S.row_a[row];
+        f.sample(ra, S.row_b[row], valid ? idx - ra.x : 0, valid);
       }
       __syncwarp();
     }
@@ -543,10 +545,11 @@ __device__ __forceinline__ float plerp(float a, float b, float t, float omt) {
 // provably warp-uniform (no waterfall loop around tld4).
 struct Acc {
   double h, g;  // per-lane sums of h and of the guidance term (fp64)
+  float hf;     // fp32 partial sum of h over the last < 16 samples (flushed into h)
   int n, nb;    // samples, band entries
 };
 
-template <bool TEX, int SIDE>
+template <bool TEX, int SIDE_T>
 struct Sample {
   const Volumes& V;
   const SideRec& R;
@@ -554,6 +557,12 @@ struct Sample {
   const float4& sc1;  // shared: (0.5 - eps_y, 0.5 - eps_z, -, -)  ambiguity thresholds on |f - 0.5|
   Acc& acc;
   bool clamp;         // some position of the item may leave [0, n-1): apply the O5 clamp
+  int side;           // runtime side when SIDE_T < 0 (warp-uniform)
+
+  // per-side data selected by a warp-uniform branch on compile-time parameter
+  // offsets, so texture handles stay in uniform registers
+  __device__ __forceinline__ const float* vol(int s) const { return s == 0 ? V.I[0] : V.I[1]; }
+  __device__ __forceinline__ unsigned long long tex(int s) const { return s == 0 ? V.texI[0] : V.texI[1]; }
 
   // the 8 corners (i0 .. i0+1)^3: two 2x2 texture gathers (tld4) or 8 loads
   __device__ __forceinline__ void gather(const float* __restrict__ vol, unsigned long long tex,
@@ -573,28 +582,69 @@ struct Sample {
     }
   }
 
+  // tld4 pair with the handle taken straight from the parameter space inside a
+  // branch per value (each tld4 sees a compile-time handle: no waterfall loop)
+  __device__ __forceinline__ void gather_tex(int which, int pair, float u, float v, float c[8]) const {
+    float4 g0, g1;
+#define MOREA_G(H)                                                           \
+  {                                                                          \
+    g0 = tex2Dgather<float4>((cudaTextureObject_t)(H), u, v, 0);             \
+    g1 = tex2Dgather<float4>((cudaTextureObject_t)(H), u, v + V.fny, 0);     \
+  }
+    if (pair < 0) {
+      if (which == 0) MOREA_G(V.texI[0]) else MOREA_G(V.texI[1])
+    } else if (which == 0) {
+      switch (pair) {
+        case 0: MOREA_G(V.texD[0][0]) break;
+        case 1: MOREA_G(V.texD[0][1]) break;
+        case 2: MOREA_G(V.texD[0][2]) break;
+        case 3: MOREA_G(V.texD[0][3]) break;
+        case 4: MOREA_G(V.texD[0][4]) break;
+        case 5: MOREA_G(V.texD[0][5]) break;
+        case 6: MOREA_G(V.texD[0][6]) break;
+        default: MOREA_G(V.texD[0][7]) break;
+      }
+    } else {
+      switch (pair) {
+        case 0: MOREA_G(V.texD[1][0]) break;
+        case 1: MOREA_G(V.texD[1][1]) break;
+        case 2: MOREA_G(V.texD[1][2]) break;
+        case 3: MOREA_G(V.texD[1][3]) break;
+        case 4: MOREA_G(V.texD[1][4]) break;
+        case 5: MOREA_G(V.texD[1][5]) break;
+        case 6: MOREA_G(V.texD[1][6]) break;
+        default: MOREA_G(V.texD[1][7]) break;
+      }
+    }
+#undef MOREA_G
+    // gather order: (x0,y1) (x1,y1) (x1,y0) (x0,y0)
+    c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
+    c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
+  }
+
   __device__ __forceinline__ static float tri(const float c[8], float fx, float fy, float fz,
                                               float gx, float gy, float gz) {
     return plerp(plerp(plerp(c[0], c[1], fx, gx), plerp(c[2], c[3], fx, gx), fy, gy),
                  plerp(plerp(c[4], c[5], fx, gx), plerp(c[6], c[7], fx, gx), fy, gy), fz, gz);
   }
 
-  __device__ __forceinline__ void sample(const int4& ri, const float4& rd, const float4& rp, int k,
-                                         bool valid) {
-    constexpr int OTH = 1 - SIDE;
+  __device__ __forceinline__ void sample(const int4& ra, const float4& rb, int k, bool valid) {
+    const int SIDE = SIDE_T >= 0 ? SIDE_T : side;
+    const int OTH = 1 - SIDE;
     const int nx = V.nx, ny = V.ny, nz = V.nz;
-    const int lin = ri.y + k;
-    const float a = __ldg(&V.I[SIDE][lin]);
+    const int lin = ra.y + k;
+    const float a = __ldg(&vol(SIDE)[lin]);
     const unsigned bm = (V.K > 0 && valid) ? (unsigned)__ldg(&V.band[SIDE][lin]) : 0u;
     const float kf = (float)k;
     const float4 s0 = sc0;
-    const float dx = fmaf(s0.x, kf, rd.x), dy = fmaf(s0.y, kf, rd.y), dz = fmaf(s0.z, kf, rd.z);
+    const float dx = fmaf(s0.x, kf, __int_as_float(ra.z)), dy = fmaf(s0.y, kf, __int_as_float(ra.w)),
+                dz = fmaf(s0.z, kf, rb.x);
     const float flx = floorf(dx), fly = floorf(dy), flz = floorf(dz);
     float fx = dx - flx, fy = dy - fly, fz = dz - flz;
     const float4 s1 = sc1;
     const bool amb = (fabsf(fx - 0.5f) > s0.w) | (fabsf(fy - 0.5f) > s1.x) | (fabsf(fz - 0.5f) > s1.y);
     // lattice corner i0 as exact floats (< 2^24)
-    float ix = rp.x + kf + flx, iy = rp.y + fly, iz = rp.z + flz;
+    float ix = rb.y + kf + flx, iy = rb.z + fly, iz = rb.w + flz;
     if (clamp) {  // warp-uniform
       // O5 clamp: x <= 0 -> (0, f = 0), x >= n-1 -> (n-2, f = 1)
       fx = ix < 0.f ? 0.f : (ix > V.fnx2 ? 1.f : fx);
@@ -614,10 +664,11 @@ struct Sample {
       base = ((int)iz * ny + (int)iy) * nx + (int)ix;
     }
     float c[8];
-    gather(V.I[OTH], TEX ? V.texI[OTH] : 0ull, u, v, base, c);
+    if (TEX) gather_tex(OTH, -1, u, v, c);
+    else gather(vol(OTH), 0ull, u, v, base, c);
     const float b = tri(c, fx, fy, fz, gx, gy, gz);
     bool fg = b > 0.f;
-    if (amb) fg = exact_fg(R, ri.z + k, ri.w & 0xffff, ri.w >> 16, dx, dy, dz, V.I[OTH], nx, ny, nz);
+    if (amb) fg = exact_fg(R, (int)rb.y + k, (int)rb.z, (int)rb.w, dx, dy, dz, vol(OTH), nx, ny, nz);
     // h of PAPER.md §4.1.2 (L318-322) with the exact case split (O6)
     float h;
     if (a > 0.f && fg) {
@@ -626,9 +677,14 @@ struct Sample {
     } else {
       h = (a == 0.f && !fg) ? 0.f : 1.f;
     }
+    // fp32 partial sums of at most 16 samples, flushed into the fp64 lane sum
     if (valid) {
-      acc.h += (double)h;
+      acc.hf += h;
       acc.n += 1;
+      if ((acc.n & 15) == 0) {
+        acc.h += (double)acc.hf;
+        acc.hf = 0.f;
+      }
     }
     // a6: guidance over the band bits, pairs in a warp-uniform order (a texture
     // instruction needs the same handle on every executing lane)
@@ -640,7 +696,8 @@ struct Sample {
       acc.nb += 1;
       const float d = __ldg(&V.dmap[SIDE][(long long)i * V.V + lin]);
       float e[8];
-      gather(V.dmap[OTH] + (long long)i * V.V, TEX ? V.texD[OTH][i] : 0ull, u, v, base, e);
+      if (TEX) gather_tex(OTH, i, u, v, e);
+      else gather(V.dmap[OTH] + (long long)i * V.V, 0ull, u, v, base, e);
       const float Dp = tri(e, fx, fy, fz, gx, gy, gz);
       const double dd = (double)d - (double)Dp;
       // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit)
@@ -669,15 +726,16 @@ __device__ __forceinline__ void load_rec(WarpSmem& S, const SideRec* src, int la
   __syncwarp();
 }
 
-template <bool TEX, int SIDE>
-__device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int lane, Acc& acc) {
+template <bool TEX, int SIDE_T>
+__device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int lane, Acc& acc,
+                                            int side) {
   const SideRec& R = S.R;
   if (lane == 0) {
     S.sc0 = make_float4(R.A[0][0], R.A[1][0], R.A[2][0], 0.5f - R.eps[0]);
     S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], 0.f, 0.f);
   }
   __syncwarp();
-  Sample<TEX, SIDE> f{V, R, S.sc0, S.sc1, acc, (R.flags & 2) == 0};
+  Sample<TEX, SIDE_T> f{V, R, S.sc0, S.sc1, acc, (R.flags & 2) == 0, side};
   raster(R, V.nx, V.ny, S, lane, f);
 }
 
@@ -703,13 +761,21 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
     const int sol = (int)(rem - (long long)es * A.P);
     const int e = A.sched[es];
     const long long i = ((long long)v * A.n_entries + e) * A.P + sol;
-    Acc acc{0.0, 0.0, 0, 0};
+    Acc acc{0.0, 0.0, 0.f, 0, 0};
+#if MOREA_SIDE_TEMPLATE
     load_rec(S, &A.geom[2 * i], lane);
-    if (S.R.flags & 1) raster_side<TEX, 0>(A.vol, S, lane, acc);
+    if (S.R.flags & 1) raster_side<TEX, 0>(A.vol, S, lane, acc, 0);
     load_rec(S, &A.geom[2 * i + 1], lane);
-    if (S.R.flags & 1) raster_side<TEX, 1>(A.vol, S, lane, acc);
+    if (S.R.flags & 1) raster_side<TEX, 1>(A.vol, S, lane, acc, 1);
+#else
+#pragma unroll 1
+    for (int side = 0; side < 2; side++) {
+      load_rec(S, &A.geom[2 * i + side], lane);
+      if (S.R.flags & 1) raster_side<TEX, -1>(A.vol, S, lane, acc, side);
+    }
+#endif
     HGN out;
-    out.h = warp_sum_d(acc.h);
+    out.h = warp_sum_d(acc.h + (double)acc.hf);
     out.g = warp_sum_d(acc.g);
     out.n = warp_sum_i(acc.n);
     out.nb = warp_sum_i(acc.nb);
@@ -924,10 +990,9 @@ cudaError_t launch_check_folds(const MeshDev& m, const double sp[3], int P, cons
 struct OwnerSample {
   int* owner;
   int tet;
-  __device__ __forceinline__ void sample(const int4& ri, const float4&, const float4&, int k,
-                                         bool valid) {
+  __device__ __forceinline__ void sample(const int4& ra, const float4&, int k, bool valid) {
     if (!valid) return;
-    const int lin = ri.y + k;
+    const int lin = ra.y + k;
     const int old = atomicCAS(&owner[lin], -1, tet);
     if (old != -1) atomicExch(&owner[lin], -2);
   }
