@@ -70,13 +70,13 @@ struct morea_ctx {
   double sp[3] = {1, 1, 1};
   double r = 0;
   double w[2][kMaxPairs] = {};
-  DevBuf I[2], band[2], dmap[2], wts, tex_handles;
+  DevBuf I[2], band[2], dmap[2], wts;
   // texture-gather copies (tall 2D arrays) of I_s, I_t and the maps
   bool use_tex = false;
   cudaArray_t arrI[2] = {nullptr, nullptr};
   cudaTextureObject_t texI[2] = {0, 0};
-  std::vector<cudaArray_t> arrD;
-  std::vector<cudaTextureObject_t> texD;
+  cudaArray_t arrM[2] = {nullptr, nullptr};
+  cudaTextureObject_t texM[2] = {0, 0};
   // mesh
   bool have_mesh = false;
   int N = 0, T = 0, spoke_mode = 0;
@@ -234,11 +234,9 @@ Volumes volumes_of(const morea_ctx* c) {
   v.use_tex = c->use_tex ? 1 : 0;
   v.texI[0] = c->texI[0];
   v.texI[1] = c->texI[1];
-  for (int s = 0; s < 2; s++)
-    for (int i = 0; i < kMaxPairs; i++) v.texD[s][i] = 0ull;
-  if (c->use_tex)
-    for (int s = 0; s < 2; s++)
-      for (int i = 0; i < c->K; i++) v.texD[s][i] = (unsigned long long)c->texD[s * c->K + i];
+  v.texM[0] = c->texM[0];
+  v.texM[1] = c->texM[1];
+  v.fnx = (float)c->nx;
   return v;
 }
 
@@ -396,26 +394,30 @@ void release_textures(morea_ctx* ctx) {
     ctx->texI[s] = 0;
     ctx->arrI[s] = nullptr;
   }
-  for (auto t : ctx->texD)
-    if (t) cudaDestroyTextureObject(t);
-  for (auto a : ctx->arrD)
-    if (a) cudaFreeArray(a);
-  ctx->texD.clear();
-  ctx->arrD.clear();
+  for (int s = 0; s < 2; s++) {
+    if (ctx->texM[s]) cudaDestroyTextureObject(ctx->texM[s]);
+    if (ctx->arrM[s]) cudaFreeArray(ctx->arrM[s]);
+    ctx->texM[s] = 0;
+    ctx->arrM[s] = nullptr;
+  }
   ctx->use_tex = false;
 }
 
-// A float volume (nx x ny x nz, x-fastest, device) as a tall 2D gather texture:
-// texel (x, y + ny z).  Point sampling, clamp, unnormalised coordinates.
-cudaError_t make_gather_texture(morea_ctx* ctx, const float* dev, cudaArray_t* arr,
+// `count` float volumes (nx x ny x nz, x-fastest, device, consecutive) as one 2D
+// gather texture: volume i, voxel (x, y, z) -> texel (x + i nx, y + ny z).  Point
+// sampling, clamp, unnormalised coordinates.
+cudaError_t make_gather_texture(morea_ctx* ctx, const float* dev, int count, cudaArray_t* arr,
                                 cudaTextureObject_t* tex) {
   cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
-  const size_t W = ctx->nx, H = (size_t)ctx->ny * ctx->nz;
+  const size_t W = (size_t)ctx->nx * count, H = (size_t)ctx->ny * ctx->nz;
   cudaError_t e = cudaMallocArray(arr, &fd, W, H, cudaArrayTextureGather);
   if (e != cudaSuccess) return e;
-  e = cudaMemcpy2DToArrayAsync(*arr, 0, 0, dev, W * sizeof(float), W * sizeof(float), H,
-                               cudaMemcpyDeviceToDevice, ctx->stream);
-  if (e != cudaSuccess) return e;
+  for (int i = 0; i < count; i++) {
+    e = cudaMemcpy2DToArrayAsync(*arr, (size_t)i * ctx->nx * sizeof(float), 0, dev + (size_t)i * ctx->V,
+                                 ctx->nx * sizeof(float), ctx->nx * sizeof(float), H,
+                                 cudaMemcpyDeviceToDevice, ctx->stream);
+    if (e != cudaSuccess) return e;
+  }
   cudaResourceDesc rd;
   std::memset(&rd, 0, sizeof(rd));
   rd.resType = cudaResourceTypeArray;
@@ -437,28 +439,16 @@ cudaError_t build_textures(morea_ctx* ctx) {
   int gw = 0, gh = 0;
   cudaDeviceGetAttribute(&gw, cudaDevAttrMaxTexture2DGatherWidth, ctx->device);
   cudaDeviceGetAttribute(&gh, cudaDevAttrMaxTexture2DGatherHeight, ctx->device);
-  if ((long long)ctx->nx > gw || (long long)ctx->ny * ctx->nz > gh) return cudaSuccess;
+  if ((long long)ctx->nx * std::max(ctx->K, 1) > gw || (long long)ctx->ny * ctx->nz > gh) return cudaSuccess;
   for (int s = 0; s < 2; s++) {
-    cudaError_t e = make_gather_texture(ctx, ctx->I[s].as<float>(), &ctx->arrI[s], &ctx->texI[s]);
+    cudaError_t e = make_gather_texture(ctx, ctx->I[s].as<float>(), 1, &ctx->arrI[s], &ctx->texI[s]);
     if (e != cudaSuccess) return e;
-  }
-  std::vector<unsigned long long> h(2 * kMaxPairs, 0ull);
-  for (int s = 0; s < 2; s++)
-    for (int i = 0; i < ctx->K; i++) {
-      cudaArray_t a = nullptr;
-      cudaTextureObject_t t = 0;
-      cudaError_t e = make_gather_texture(ctx, ctx->dmap[s].as<float>() + (size_t)i * ctx->V, &a, &t);
+    if (ctx->K > 0) {
+      e = make_gather_texture(ctx, ctx->dmap[s].as<float>(), ctx->K, &ctx->arrM[s], &ctx->texM[s]);
       if (e != cudaSuccess) return e;
-      ctx->arrD.push_back(a);
-      ctx->texD.push_back(t);
-      h[s * kMaxPairs + i] = (unsigned long long)t;
     }
-  cudaError_t e = ctx->tex_handles.ensure(h.size() * sizeof(unsigned long long));
-  if (e != cudaSuccess) return e;
-  e = cudaMemcpyAsync(ctx->tex_handles.p, h.data(), h.size() * sizeof(unsigned long long),
-                      cudaMemcpyHostToDevice, ctx->stream);
-  if (e != cudaSuccess) return e;
-  e = cudaStreamSynchronize(ctx->stream);
+  }
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e == cudaSuccess) ctx->use_tex = true;
   return e;
 }
@@ -511,7 +501,7 @@ void morea_destroy(morea_ctx* ctx) {
     cudaEventDestroy(p.second);
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
-                    &ctx->dmap[1], &ctx->wts, &ctx->tex_handles, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
+                    &ctx->dmap[1], &ctx->wts, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
                     &ctx->full_sched, &ctx->full_group_off, &ctx->geom, &ctx->scal, &ctx->hgn,
                     &ctx->counter, &ctx->stats, &ctx->st_off, &ctx->st_nv, &ctx->st_cache_in,
                     &ctx->st_base_acc, &ctx->st_obj, &ctx->st_acc, &ctx->st_cache_out,

@@ -64,7 +64,9 @@ struct Volumes {
   // texture-gather path: I_s / I_t and the maps as tall 2D textures (texel (x, y + ny z)),
   // gathered 2x2 per slice (tld4); 0 / nullptr when the volume exceeds the gather limits
   unsigned long long texI[2];
-  unsigned long long texD[2][kMaxPairs];  // in the parameter space: uniform (constant-bank) loads
+  // the K maps of a side side by side in one gather texture: texel (x + i nx, y + ny z)
+  unsigned long long texM[2];
+  float fnx;  // nx as float (map offset in texM)
   int use_tex;
 };
 

@@ -31,6 +31,10 @@
 #define MOREA_SIDE_TEMPLATE 0  // 1: one sample-loop instantiation per side (twice the code)
 #endif
 
+#ifndef MOREA_ABLATE
+#define MOREA_ABLATE 0  // dev experiments only (4: no guidance evaluation, 5: no band loads)
+#endif
+
 #ifndef MOREA_RASTER_MINB
 #define MOREA_RASTER_MINB 3  // resident 256-thread blocks per SM the register budget targets
 #endif
@@ -376,7 +380,7 @@ __device__ __noinline__ void slice_y_range(const SideRec& R, int z, int& ylo, in
       if (zf < lo || zf > hi) continue;
       float y0, y1;
       if (hi > lo) {
-        const float t = (zf - zi) / (zj - zi);
+        const float t = __fdividef(zf - zi, zj - zi);  // ~2 ulp: covered by the 1e-3 margin
         y0 = y1 = fmaf(t, R.vy[j] - R.vy[i], R.vy[i]);
       } else {
         y0 = R.vy[i];
@@ -390,12 +394,18 @@ __device__ __noinline__ void slice_y_range(const SideRec& R, int z, int& ylo, in
   yhi = min(R.hi[1], (int)floorf(fminf(ymax + 1e-3f, 1.0e6f)));
 }
 
+constexpr int kQueueCap = 64;  // < 32 pending + one round of <= 32
+
 struct WarpSmem {
   SideRec R;
   int4 row_a[32];    // (exclusive prefix, linear index of row start, dx0, dy0 as float bits)
   float4 row_b[32];  // (dz0, xl, y, z): fp32 displacement z at the row start, row start as floats
   float4 sc0, sc1;   // per-side sample constants (see Sample)
   unsigned long long stat[3];  // samples, band entries, items of this warp (profiling)
+  // band-entry queue of the guidance term (a6): entries are evaluated 32 at a time
+  float4 qa[kQueueCap];  // (u, v, fx, fy): footprint texel coordinates and weights
+  int4 qb[kQueueCap];    // (fz bits, own linear index, pair i, -)
+  int qn;                // entries queued (warp-uniform)
 };
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -470,6 +480,10 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, WarpSme
       __syncwarp();
       const int last = __popc(ne) - 1;
       int rprev = -1;
+#if MOREA_ABLATE == 6
+      f.count_only(lane == 0 ? total : 0);
+      continue;
+#endif
       for (int s0 = 0; s0 < total; s0 += 32) {
         const unsigned bit = (len > 0 && start >= s0 && start < s0 + 32) ? (1u << (start - s0)) : 0u;
         const unsigned M = __reduce_or_sync(FULLMASK, bit);
@@ -545,14 +559,16 @@ __device__ __forceinline__ float plerp(float a, float b, float t, float omt) {
 // provably warp-uniform (no waterfall loop around tld4).
 struct Acc {
   double h, g;  // per-lane sums of h and of the guidance term (fp64)
-  float hf;     // fp32 partial sum of h over the last < 16 samples (flushed into h)
+  float hf;     // fp32 partial sum of h over the last < 16 steps (flushed into h)
   int n, nb;    // samples, band entries
+  int steps;    // sample steps (warp-uniform)
 };
 
 template <bool TEX, int SIDE_T>
 struct Sample {
   const Volumes& V;
   const SideRec& R;
+  WarpSmem& S;
   const float4& sc0;  // shared: (A_x0, A_y0, A_z0, 0.5 - eps_x)  displacement gradient along x
   const float4& sc1;  // shared: (0.5 - eps_y, 0.5 - eps_z, -, -)  ambiguity thresholds on |f - 0.5|
   Acc& acc;
@@ -583,40 +599,16 @@ struct Sample {
   }
 
   // tld4 pair with the handle taken straight from the parameter space inside a
-  // branch per value (each tld4 sees a compile-time handle: no waterfall loop)
-  __device__ __forceinline__ void gather_tex(int which, int pair, float u, float v, float c[8]) const {
+  // branch per side (each tld4 sees a compile-time handle: no waterfall loop)
+  __device__ __forceinline__ void gather_tex(int which, float u, float v, float c[8]) const {
     float4 g0, g1;
-#define MOREA_G(H)                                                           \
-  {                                                                          \
-    g0 = tex2Dgather<float4>((cudaTextureObject_t)(H), u, v, 0);             \
-    g1 = tex2Dgather<float4>((cudaTextureObject_t)(H), u, v + V.fny, 0);     \
-  }
-    if (pair < 0) {
-      if (which == 0) MOREA_G(V.texI[0]) else MOREA_G(V.texI[1])
-    } else if (which == 0) {
-      switch (pair) {
-        case 0: MOREA_G(V.texD[0][0]) break;
-        case 1: MOREA_G(V.texD[0][1]) break;
-        case 2: MOREA_G(V.texD[0][2]) break;
-        case 3: MOREA_G(V.texD[0][3]) break;
-        case 4: MOREA_G(V.texD[0][4]) break;
-        case 5: MOREA_G(V.texD[0][5]) break;
-        case 6: MOREA_G(V.texD[0][6]) break;
-        default: MOREA_G(V.texD[0][7]) break;
-      }
+    if (which == 0) {
+      g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texI[0], u, v, 0);
+      g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texI[0], u, v + V.fny, 0);
     } else {
-      switch (pair) {
-        case 0: MOREA_G(V.texD[1][0]) break;
-        case 1: MOREA_G(V.texD[1][1]) break;
-        case 2: MOREA_G(V.texD[1][2]) break;
-        case 3: MOREA_G(V.texD[1][3]) break;
-        case 4: MOREA_G(V.texD[1][4]) break;
-        case 5: MOREA_G(V.texD[1][5]) break;
-        case 6: MOREA_G(V.texD[1][6]) break;
-        default: MOREA_G(V.texD[1][7]) break;
-      }
+      g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texI[1], u, v, 0);
+      g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texI[1], u, v + V.fny, 0);
     }
-#undef MOREA_G
     // gather order: (x0,y1) (x1,y1) (x1,y0) (x0,y0)
     c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
     c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
@@ -628,13 +620,96 @@ struct Sample {
                  plerp(plerp(c[4], c[5], fx, gx), plerp(c[6], c[7], fx, gx), fy, gy), fz, gz);
   }
 
+  // guidance term of the queued entries [q0, q0 + cnt) (a6, O8), one per lane
+  __device__ __forceinline__ void flush(int q0, int cnt, int s) {
+    const int lane = threadIdx.x & 31;
+    if (lane < cnt) {
+      const int o = 1 - s;
+      const float4 ea = S.qa[q0 + lane];
+      const int4 eb = S.qb[q0 + lane];
+      const float fz = __int_as_float(eb.x);
+      const int i = eb.z;
+      const float d = __ldg(&(s == 0 ? V.dmap[0] : V.dmap[1])[(long long)i * V.V + eb.y]);
+      float e[8];
+      if (TEX) {
+        const float uu = fmaf((float)i, V.fnx, ea.x);
+        float4 g0, g1;
+        if (o == 0) {
+          g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texM[0], uu, ea.y, 0);
+          g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texM[0], uu, ea.y + V.fny, 0);
+        } else {
+          g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texM[1], uu, ea.y, 0);
+          g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texM[1], uu, ea.y + V.fny, 0);
+        }
+        e[0] = g0.w; e[1] = g0.z; e[2] = g0.x; e[3] = g0.y;
+        e[4] = g1.w; e[5] = g1.z; e[6] = g1.x; e[7] = g1.y;
+      } else {
+        const int base = (int)(ea.y - 1.0f) * V.nx + (int)(ea.x - 1.0f);
+        gather((o == 0 ? V.dmap[0] : V.dmap[1]) + (long long)i * V.V, 0ull, 0.f, 0.f, base, e);
+      }
+      const float Dp = tri(e, ea.z, ea.w, fz, 1.f - ea.z, 1.f - ea.w, 1.f - fz);
+      const double dd = (double)d - (double)Dp;
+      // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit)
+      acc.g += __ldg(&V.w[s * kMaxPairs + i]) * ((V.r - (double)d) * V.inv_r) * dd * dd;
+    }
+  }
+
+  // append the band entries of this step's samples (one round per set bit), flush
+  // full batches of 32
+  __device__ __forceinline__ void enqueue(unsigned bm, int lin, float u, float v, float fx, float fy,
+                                          float fz, int s) {
+    const int lane = threadIdx.x & 31;
+    acc.nb += __popc(bm);
+    while (true) {
+      const unsigned take = __ballot_sync(FULLMASK, bm != 0u);
+      if (!take) break;
+      const int qn = S.qn;
+      if (bm) {
+        const int i = __ffs(bm) - 1;
+        bm &= bm - 1;
+        const int pos = qn + __popc(take & ((1u << lane) - 1u));
+        S.qa[pos] = make_float4(u, v, fx, fy);
+        S.qb[pos] = make_int4(__float_as_int(fz), lin, i, 0);
+      }
+      __syncwarp();
+      int n = qn + __popc(take);
+      if (n >= 32) {
+        flush(n - 32, 32, s);
+        n -= 32;
+      }
+      __syncwarp();
+      if (lane == 0) S.qn = n;
+      __syncwarp();
+    }
+  }
+
+  __device__ __forceinline__ void count_only(int t) { acc.n += t; }
+
+  // evaluate what is left in the queue (end of a side)
+  __device__ __forceinline__ void drain(int s) {
+    __syncwarp();
+    const int n = S.qn;
+    if (n > 0) flush(0, n, s);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) S.qn = 0;
+    __syncwarp();
+  }
+
   __device__ __forceinline__ void sample(const int4& ra, const float4& rb, int k, bool valid) {
     const int SIDE = SIDE_T >= 0 ? SIDE_T : side;
     const int OTH = 1 - SIDE;
+#if MOREA_ABLATE == 3
+    if (valid) { acc.n += 1; acc.hf += __int_as_float(ra.z) + (float)k; }
+    return;
+#endif
     const int nx = V.nx, ny = V.ny, nz = V.nz;
     const int lin = ra.y + k;
     const float a = __ldg(&vol(SIDE)[lin]);
+#if MOREA_ABLATE == 5
+    const unsigned bm = (a > 2.0f) ? 1u : 0u;
+#else
     const unsigned bm = (V.K > 0 && valid) ? (unsigned)__ldg(&V.band[SIDE][lin]) : 0u;
+#endif
     const float kf = (float)k;
     const float4 s0 = sc0;
     const float dx = fmaf(s0.x, kf, __int_as_float(ra.z)), dy = fmaf(s0.y, kf, __int_as_float(ra.w)),
@@ -655,16 +730,11 @@ struct Sample {
       iz = fminf(fmaxf(iz, 0.f), V.fnz2);
     }
     const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
-    float u = 0.f, v = 0.f;
-    int base = 0;
-    if (TEX) {
-      u = ix + 1.0f;
-      v = fmaf(iz, V.fny, iy) + 1.0f;
-    } else {
-      base = ((int)iz * ny + (int)iy) * nx + (int)ix;
-    }
+    // texel coordinates of corner i0 + (1, 1) in the (x, y + ny z) layout (exact floats)
+    const float u = ix + 1.0f, v = fmaf(iz, V.fny, iy) + 1.0f;
+    const int base = TEX ? 0 : ((int)iz * ny + (int)iy) * nx + (int)ix;
     float c[8];
-    if (TEX) gather_tex(OTH, -1, u, v, c);
+    if (TEX) gather_tex(OTH, u, v, c);
     else gather(vol(OTH), 0ull, u, v, base, c);
     const float b = tri(c, fx, fy, fz, gx, gy, gz);
     bool fg = b > 0.f;
@@ -677,32 +747,20 @@ struct Sample {
     } else {
       h = (a == 0.f && !fg) ? 0.f : 1.f;
     }
-    // fp32 partial sums of at most 16 samples, flushed into the fp64 lane sum
-    if (valid) {
-      acc.hf += h;
-      acc.n += 1;
-      if ((acc.n & 15) == 0) {
-        acc.h += (double)acc.hf;
-        acc.hf = 0.f;
-      }
+    // fp32 partial sums over at most 16 steps, flushed into the fp64 lane sum by the
+    // (warp-uniform) step counter
+    acc.hf += valid ? h : 0.f;
+    acc.n += valid ? 1 : 0;
+    if ((++acc.steps & 15) == 0) {
+      acc.h += (double)acc.hf;
+      acc.hf = 0.f;
     }
-    // a6: guidance over the band bits, pairs in a warp-uniform order (a texture
-    // instruction needs the same handle on every executing lane)
-    unsigned wbm = __reduce_or_sync(FULLMASK, bm);
-    while (wbm) {
-      const int i = __ffs(wbm) - 1;
-      wbm &= wbm - 1;
-      if (!((bm >> i) & 1u)) continue;
-      acc.nb += 1;
-      const float d = __ldg(&V.dmap[SIDE][(long long)i * V.V + lin]);
-      float e[8];
-      if (TEX) gather_tex(OTH, i, u, v, e);
-      else gather(V.dmap[OTH] + (long long)i * V.V, 0ull, u, v, base, e);
-      const float Dp = tri(e, fx, fy, fz, gx, gy, gz);
-      const double dd = (double)d - (double)Dp;
-      // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit)
-      acc.g += __ldg(&V.w[SIDE * kMaxPairs + i]) * ((V.r - (double)d) * V.inv_r) * dd * dd;
-    }
+    // a6: band entries go to the per-warp queue, evaluated 32 at a time
+#if MOREA_ABLATE == 4
+    acc.nb += __popc(bm);
+#else
+    if (__reduce_or_sync(FULLMASK, bm)) enqueue(bm, lin, u, v, fx, fy, fz, SIDE);
+#endif
   }
 };
 
@@ -735,8 +793,11 @@ __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int l
     S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], 0.f, 0.f);
   }
   __syncwarp();
-  Sample<TEX, SIDE_T> f{V, R, S.sc0, S.sc1, acc, (R.flags & 2) == 0, side};
+  if (lane == 0) S.qn = 0;
+  __syncwarp();
+  Sample<TEX, SIDE_T> f{V, R, S, S.sc0, S.sc1, acc, (R.flags & 2) == 0, side};
   raster(R, V.nx, V.ny, S, lane, f);
+  f.drain(SIDE_T >= 0 ? SIDE_T : side);
 }
 
 // ---------------------------------------------------------------------------
@@ -761,7 +822,7 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
     const int sol = (int)(rem - (long long)es * A.P);
     const int e = A.sched[es];
     const long long i = ((long long)v * A.n_entries + e) * A.P + sol;
-    Acc acc{0.0, 0.0, 0.f, 0, 0};
+    Acc acc{0.0, 0.0, 0.f, 0, 0, 0};
 #if MOREA_SIDE_TEMPLATE
     load_rec(S, &A.geom[2 * i], lane);
     if (S.R.flags & 1) raster_side<TEX, 0>(A.vol, S, lane, acc, 0);
@@ -990,6 +1051,7 @@ cudaError_t launch_check_folds(const MeshDev& m, const double sp[3], int P, cons
 struct OwnerSample {
   int* owner;
   int tet;
+  __device__ __forceinline__ void count_only(int) {}
   __device__ __forceinline__ void sample(const int4& ra, const float4&, int k, bool valid) {
     if (!valid) return;
     const int lin = ra.y + k;
