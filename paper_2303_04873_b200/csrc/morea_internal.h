@@ -18,8 +18,8 @@ constexpr int kRasterThreads = 32 * kWarpsPerBlock;
 // are roundings of exact (or fp64) values; each comes with an error bound so the
 // rasterizer can detect when only the exact integer fields can decide.
 struct __align__(16) SideRec {
-  float fa[4], fb[4], fc[4];  // face crossing x*(y,z) = fa + fb (y - lo_y) + fc (z - lo_z)
-  float fthr[4];              // bound on the fp32 crossing error (voxels)
+  float4 face[4];             // (fa, fb, fc, thr): crossing x*(y,z) = fa + fb (y - lo_y) + fc (z - lo_z)
+                              // and the bound on its fp32 error (voxels)
   int ftype[4];               // +-1: lower/upper bound face (n_x >< 0), 0: flat, +-2: exact search
   long long nrm[4][3];        // exact inward normals (|n| < 2^41)
   long long cst[4];           // e_k(q) = 1024 n_k . q - cst_k  (exact)

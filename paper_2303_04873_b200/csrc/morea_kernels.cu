@@ -133,17 +133,16 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
       const i128 num = (i128)G.cst[k] - (i128)1024 * ((i128)n1 * G.lo[1] + (i128)n2 * G.lo[2]);
       const double fa = (double)num / (1024.0 * (double)n0);
       const double fb = -(double)n1 / (double)n0, fc = -(double)n2 / (double)n0;
-      G.fa[k] = (float)fa;
-      G.fb[k] = (float)fb;
-      G.fc[k] = (float)fc;
+      G.face[k].x = (float)fa;
+      G.face[k].y = (float)fb;
+      G.face[k].z = (float)fc;
       // fp32 rounding of 3 coefficients + 2 fma: < 2^-22 (|fa| + |fb| Ly + |fc| Lz); 4x margin
       const double thr = ldexp(fabs(fa) + fabs(fb) * Ly + fabs(fc) * Lz + 1.0, -20);
-      G.fthr[k] = (float)thr;
+      G.face[k].w = (float)thr;
       G.ftype[k] = (n0 > 0 ? 1 : -1) * (thr >= 0.25 ? 2 : 1);
     } else {
       G.ftype[k] = 0;
-      G.fa[k] = G.fb[k] = G.fc[k] = 0.0f;
-      G.fthr[k] = 0.0f;
+      G.face[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
   // O4: displacement u(p) = sum_k lambda_k(p) U_k / 1024, lambda_k = e_k / |Delta|.
@@ -326,16 +325,19 @@ __device__ __noinline__ void row_interval(const SideRec& R, int y, int z, int& x
   xl = lo;
   xh = hi;
   const float dy = (float)(y - R.lo[1]), dz = (float)(z - R.lo[2]);
+  const int4 types = *reinterpret_cast<const int4*>(R.ftype);
+  const int tk[4] = {types.x, types.y, types.z, types.w};
 #pragma unroll
   for (int k = 0; k < 4; k++) {
-    const int t = R.ftype[k];
+    const int t = tk[k];
     if (t == 0) {
       const i64 E = face_e(R, k, 0, y, z);
       const bool own = E > 0 || (E == 0 && (R.nrm[k][1] > 0 || (R.nrm[k][1] == 0 && R.nrm[k][2] > 0)));
       if (!own) xh = lo - 1;
       continue;
     }
-    float xs = fmaf(R.fc[k], dz, fmaf(R.fb[k], dy, R.fa[k]));
+    const float4 fc4 = R.face[k];
+    float xs = fmaf(fc4.z, dz, fmaf(fc4.y, dy, fc4.x));
     xs = fminf(fmaxf(xs, (float)lo - 4.5f), (float)hi + 4.5f);
     const float xr = rintf(xs);
     if (t == 2 || t == -2) {  // exact monotone search (rare: nearly x-parallel face)
@@ -354,7 +356,7 @@ __device__ __noinline__ void row_interval(const SideRec& R, int y, int z, int& x
       continue;
     }
     int xi;
-    if (fabsf(xs - xr) > R.fthr[k]) {
+    if (fabsf(xs - xr) > fc4.w) {
       xi = (int)ceilf(xs) - (t < 0 ? 1 : 0);  // lower: smallest x > x*; upper: largest x < x*
     } else {  // x* within the error bound of the integer c: decide exactly
       const int c = (int)xr;
