@@ -46,6 +46,9 @@ extern "C" {
 /* ---- per-solution flags (morea_acc.flags) ---- */
 #define MOREA_F_DOMAIN 1 /* some point outside the Q.10 window: objectives are NaN */
 #define MOREA_F_EMPTY 2  /* no samples (n_samples == 0): objectives are NaN */
+#define MOREA_F_COVERAGE 4 /* full evaluation only: on some side the number of owned voxel
+                              centres differs from the base mesh's (row a9 coverage check:
+                              a gap or an overlap, e.g. from moved hull points or a fold) */
 
 /* ---- morea_set_mesh options ---- */
 #define MOREA_SPOKE_FACE_CENTROID 0 /* spoke = vertex -> centroid of the opposite face (O9, default) */

@@ -43,6 +43,7 @@ typedef __int128 i128;
 
 #define ORC_F_DOMAIN 1
 #define ORC_F_EMPTY 2
+#define ORC_F_COVERAGE 4
 
 /* Q.10 window (O1): Q in [-256*1024, 768*1024) on every axis. */
 #define QLO (-256LL * 1024LL)
@@ -81,6 +82,8 @@ typedef struct {
     int bsz, bn[3];
     int32_t *boff[2][64];
     int32_t *bidx[2][64];
+    /* coverage reference (row a9): owned-sample count per side of the base mesh; -1 = unknown */
+    int64_t expect[2];
 } orc_problem;
 
 /* ------------------------------------------------------------------ */
@@ -451,6 +454,7 @@ static void tet_side_samples(orc_problem *P, int s, const int64_t Q[2][4][3], do
                     continue;
                 }
                 (*n_owned)++;
+                if (!h_sum) continue; /* count only */
                 /* O4: x = q + sum_k lambda_k U_k / 1024, lambda_k = e_k / |Delta| */
                 i128 Pnum[3];
                 double xp[3];
@@ -569,6 +573,7 @@ orc_problem *orc_create(int nx, int ny, int nz, const double *spacing, const flo
     /* compact (a tet listing a point twice is invalid anyway) */
     free(fill);
     /* bucket grid for the nearest-point search */
+    P->expect[0] = P->expect[1] = -1;
     P->bsz = 4;
     for (int a = 0; a < 3; a++) P->bn[a] = (P->n[a] + 2) / P->bsz + 1;
     int nb = P->bn[0] * P->bn[1] * P->bn[2];
@@ -634,12 +639,29 @@ static int any_out_of_window(const orc_problem *P, const float *off) {
     return 0;
 }
 
+/* coverage reference: owned voxel centres per side at the base mesh (zero offsets) */
+static void base_counts(orc_problem *P) {
+    if (P->expect[0] >= 0) return;
+    int64_t c[2] = {0, 0};
+    for (int t = 0; t < P->T; t++) {
+        int64_t Q[2][4][3];
+        if (!tet_coords(P, NULL, t, Q)) continue;
+        for (int s = 0; s < 2; s++) tet_side_samples(P, s, Q, NULL, NULL, &c[s], NULL, t);
+    }
+    P->expect[0] = c[0];
+    P->expect[1] = c[1];
+}
+
 /* full evaluation of one solution (sum over all tets in index order) */
 int orc_eval(orc_problem *P, const float *offsets_one, double obj[3], orc_acc *acc) {
     memset(acc, 0, sizeof(*acc));
     double rec[PT_N];
+    int64_t ns = 0, nt = 0;
+    base_counts(P);
     for (int t = 0; t < P->T; t++) {
         tet_contrib(P, offsets_one, t, rec);
+        ns += (int64_t)rec[PT_NS];
+        nt += (int64_t)rec[PT_NT];
         acc->h_sum += rec[PT_H];
         acc->g_sum += rec[PT_G];
         acc->m_sum += rec[PT_M];
@@ -648,6 +670,7 @@ int orc_eval(orc_problem *P, const float *offsets_one, double obj[3], orc_acc *a
         acc->folds += (int32_t)rec[PT_FOLD_S] + (int32_t)rec[PT_FOLD_T];
     }
     if (any_out_of_window(P, offsets_one)) acc->flags |= ORC_F_DOMAIN;
+    else if (ns != P->expect[0] || nt != P->expect[1]) acc->flags |= ORC_F_COVERAGE; /* a9 */
     if (acc->n_samples == 0) acc->flags |= ORC_F_EMPTY;
     acc_objectives(P, acc, obj);
     return 0;

@@ -18,6 +18,7 @@ LIB = os.path.join(HERE, "liboracle.so")
 
 F_DOMAIN = 1
 F_EMPTY = 2
+F_COVERAGE = 4
 PT = dict(h=0, g=1, ns=2, nt=3, m=4, fold_s=5, fold_t=6, sev=7, domain=8)
 PT_N = 10
 

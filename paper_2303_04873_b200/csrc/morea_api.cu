@@ -85,6 +85,7 @@ struct morea_ctx {
   std::vector<int32_t> h_tets, inc_off, inc;
   std::vector<double> tet_size;
   DevBuf full_sched, full_group_off;
+  long long expect[2] = {-1, -1};  // base-mesh sample counts per side (coverage check)
   // scratch
   DevBuf geom, scal, hgn, counter, stats;
   DevBuf st_off, st_nv, st_cache_in, st_base_acc, st_obj, st_acc, st_cache_out, st_i32, st_f64,
@@ -680,6 +681,41 @@ int morea_set_mesh(morea_ctx* ctx, int n_points, const float* base_xyz, int n_te
   CK(cudaMemcpyAsync(ctx->full_group_off.p, goff, 2 * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->have_mesh = true;
+  // coverage reference: per-side owned-sample counts of the base mesh (zero offsets)
+  {
+    ctx->expect[0] = ctx->expect[1] = -1;
+    DevBuf zoff;
+    CK(zoff.ensure((size_t)n_points * 6 * sizeof(float)));
+    CK(cudaMemsetAsync(zoff.p, 0, (size_t)n_points * 6 * sizeof(float), ctx->stream));
+    EvalArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.vol = volumes_of(ctx);
+    a.mesh = mesh_of(ctx);
+    a.P = 1;
+    a.offsets = zoff.as<float>();
+    a.n_entries = n_tets;
+    a.sched = ctx->full_sched.as<int>();
+    a.n_setup_versions = 1;
+    a.n_raster_versions = 1;
+    a.expect[0] = a.expect[1] = -1;
+    CK(run_eval(ctx, a));
+    std::vector<HGN> hg(n_tets);
+    CK(cudaMemcpyAsync(hg.data(), ctx->hgn.p, n_tets * sizeof(HGN), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    long long c0 = 0, c1 = 0;
+    for (int t = 0; t < n_tets; t++) {
+      c0 += hg[t].n0;
+      c1 += hg[t].n - hg[t].n0;
+    }
+    ctx->expect[0] = c0;
+    ctx->expect[1] = c1;
+    zoff.release();
+    if (ctx->prof) {  // not part of any measured evaluation
+      for (auto& p : ctx->evs) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+      ctx->evs.clear();
+      ctx->prof_launches = 0;
+    }
+  }
   return MOREA_OK;
 }
 
@@ -717,6 +753,8 @@ int morea_eval_full(morea_ctx* ctx, int pop, const float* offsets, double* obj, 
   a.partial = 0;
   a.n_setup_versions = 1;
   a.n_raster_versions = 1;
+  a.expect[0] = ctx->expect[0];
+  a.expect[1] = ctx->expect[1];
   CK(run_eval(ctx, a));
   CK(launch_reduce(a, 1, ctx->full_group_off.as<int>(), nullptr, nullptr, (double*)ov[2].dev,
                    nullptr, nullptr, (double*)ov[0].dev, ov[1].dev, ctx->stream));
@@ -766,6 +804,7 @@ int morea_eval_partial(morea_ctx* ctx, int pop, const float* base_offsets,
   a.partial = 1;
   a.n_setup_versions = 2;
   a.n_raster_versions = cin ? 1 : 2;
+  a.expect[0] = a.expect[1] = -1;
   CK(run_eval(ctx, a));
   CK(launch_reduce(a, G, P.group_off.as<int>(), bacc, cin, (double*)ov[2].dev, P.changed.as<int>(),
                    P.grp_off.as<int>(), (double*)ov[0].dev, ov[1].dev, ctx->stream));
@@ -824,6 +863,7 @@ int morea_owner_map(morea_ctx* ctx, const float* offsets_one, int side, int32_t*
   a.sched = ctx->full_sched.as<int>();
   a.n_setup_versions = 1;
   a.n_raster_versions = 1;
+  a.expect[0] = a.expect[1] = -1;
   CK(eval_scratch(ctx, a));
   CK(launch_owner_map(a, side, (int*)ov[0].dev, ctx->stream));
   ctx->kernels += 3;

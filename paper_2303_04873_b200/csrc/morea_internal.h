@@ -46,7 +46,9 @@ static_assert(sizeof(Scal) == 32, "Scal layout");
 // Sample sums of one (version, entry, solution), both sides.
 struct HGN {
   double h, g;
-  long long n, nb;
+  int n, nb;  // samples (both sides), band entries
+  int n0;     // samples of side 0 (coverage check)
+  int pad;
 };
 static_assert(sizeof(HGN) == 32, "HGN layout");
 
@@ -99,6 +101,7 @@ struct EvalArgs {
   SideRec* geom;             // [version][entry][sol][side]
   Scal* scal;                // [version][entry][sol]
   HGN* hgn;                  // [version][entry][sol]
+  long long expect[2];       // per-side sample count of the base mesh (coverage check), -1: off
   unsigned long long* counter;  // work queue head (zeroed before launch)
   unsigned long long* stats;    // [samples, band entries, items]
 };

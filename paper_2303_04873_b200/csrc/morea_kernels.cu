@@ -828,13 +828,16 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
 #if MOREA_SIDE_TEMPLATE
     load_rec(S, &A.geom[2 * i], lane);
     if (S.R.flags & 1) raster_side<TEX, 0>(A.vol, S, lane, acc, 0);
+    const int n_side0 = acc.n;
     load_rec(S, &A.geom[2 * i + 1], lane);
     if (S.R.flags & 1) raster_side<TEX, 1>(A.vol, S, lane, acc, 1);
 #else
+    int n_side0 = 0;
 #pragma unroll 1
     for (int side = 0; side < 2; side++) {
       load_rec(S, &A.geom[2 * i + side], lane);
       if (S.R.flags & 1) raster_side<TEX, -1>(A.vol, S, lane, acc, side);
+      if (side == 0) n_side0 = acc.n;
     }
 #endif
     HGN out;
@@ -842,6 +845,8 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
     out.g = warp_sum_d(acc.g);
     out.n = warp_sum_i(acc.n);
     out.nb = warp_sum_i(acc.nb);
+    out.n0 = warp_sum_i(n_side0);
+    out.pad = 0;
     if (lane == 0) {
       A.hgn[i] = out;
       S.stat[0] += out.n;
@@ -887,7 +892,7 @@ __global__ void k_reduce(const EvalArgs A, int G, const int* __restrict__ group_
   const int T = A.mesh.T, N = A.mesh.N;
   const long long per_v = (long long)A.n_entries * P;
   double h = 0.0, gs = 0.0, m = 0.0, sev = 0.0;
-  long long n = 0;
+  long long n = 0, n0 = 0;
   int folds = 0, dom = 0;
   for (int e = group_off[g] + lane; e < group_off[g + 1]; e += 32) {
     const long long i0 = (long long)e * P + sol;
@@ -896,7 +901,7 @@ __global__ void k_reduce(const EvalArgs A, int G, const int* __restrict__ group_
     const int tet = A.canon_tet ? A.canon_tet[e] : e;
     dom |= s0.flags & 1;
     if (!A.partial) {
-      h += r0.h; gs += r0.g; m += s0.m; sev += s0.sev; n += r0.n; folds += s0.folds;
+      h += r0.h; gs += r0.g; m += s0.m; sev += s0.sev; n += r0.n; n0 += r0.n0; folds += s0.folds;
       if (cache_out) {
         double* c = cache_out + ((long long)sol * T + tet) * 4;
         c[0] = r0.h; c[1] = r0.g; c[2] = (double)r0.n; c[3] = s0.m;
@@ -944,6 +949,7 @@ __global__ void k_reduce(const EvalArgs A, int G, const int* __restrict__ group_
     m += __shfl_xor_sync(FULLMASK, m, o);
     sev += __shfl_xor_sync(FULLMASK, sev, o);
     n += __shfl_xor_sync(FULLMASK, n, o);
+    n0 += __shfl_xor_sync(FULLMASK, n0, o);
     folds += __shfl_xor_sync(FULLMASK, folds, o);
     dom |= __shfl_xor_sync(FULLMASK, dom, o);
   }
@@ -962,6 +968,8 @@ __global__ void k_reduce(const EvalArgs A, int G, const int* __restrict__ group_
     out.h_sum = h; out.g_sum = gs; out.m_sum = m; out.severity = sev;
     out.n_samples = n; out.folds = folds;
     out.flags = dom ? MOREA_F_DOMAIN : 0;
+    if (A.expect[0] >= 0 && !dom && (n0 != A.expect[0] || n - n0 != A.expect[1]))
+      out.flags |= MOREA_F_COVERAGE;  // row a9 coverage check
   }
   if (out.n_samples == 0) out.flags |= MOREA_F_EMPTY;
   const long long o = (long long)sol * G + g;

@@ -20,6 +20,7 @@ MOREA_OK = 0
 ERRORS = {-1: "EINVAL", -2: "ESTATE", -3: "EDOMAIN", -4: "ECUDA", -5: "ENOMEM"}
 F_DOMAIN = 1
 F_EMPTY = 2
+F_COVERAGE = 4
 SPOKE_FACE_CENTROID = 0
 SPOKE_TET_CENTROID = 1
 

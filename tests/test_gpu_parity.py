@@ -397,3 +397,29 @@ def test_spoke_mode_and_cdelta(wl):
         g_obj, _, _, _, _ = _gpu_full(ctx, w.offsets)
         for k in range(w.P):
             assert g_obj[k][0] == pytest.approx(orc.eval(w.offsets[k])[0][0], rel=1e-10)
+
+
+def test_coverage_flag_matches_oracle():
+    """Row a9 coverage check on the GPU == oracle (gap from a moved hull vertex, overlap
+    from a fold, none for identity / interior moves)."""
+    dims = (12, 12, 12)
+    g = [-0.5, 3.5, 7.5, 11.5]
+    base, tets = kuhn_lattice_mesh(g, g, g)
+    base = base.astype(np.float32)
+    I = blob_volume(dims, 3)
+    ctx = _ctx_raw(dims, I, I, base, tets)
+    orc = make_oracle(dims, I, I, base, tets)
+    offs = np.zeros((4, len(base), 6), np.float32)
+    offs[1, 0, 3:] = [2.0, 2.0, 2.0]
+    j = 1 * 16 + 1 * 4 + 1
+    t = int(np.nonzero((tets == j).any(1))[0][0])
+    others = [v for v in tets[t] if v != j]
+    c = base[others].astype(np.float64).mean(0)
+    offs[2, j, :3] = (2 * c - base[j]) - base[j]
+    offs[3, j] = [0.3, -0.2, 0.1, -0.4, 0.2, 0.3]
+    g_obj, g_acc, _, _, _ = _gpu_full(ctx, offs)
+    for k in range(4):
+        o_obj, o_acc = orc.eval(offs[k])
+        _assert_acc(g_acc[k], o_acc, f"coverage case {k}")
+    assert g_acc["flags"][0] == 0 and g_acc["flags"][3] == 0
+    assert g_acc["flags"][1] & morea.F_COVERAGE and g_acc["flags"][2] & morea.F_COVERAGE

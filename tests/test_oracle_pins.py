@@ -591,7 +591,8 @@ def test_partial_equals_full_and_move_back(wl):
                 full_off[S] = nv
                 fobj, facc = orc.eval(full_off)
                 assert acc.n_samples == facc.n_samples and acc.folds == facc.folds
-                assert acc.flags == facc.flags
+                # the coverage check (a9) is defined for full evaluations only
+                assert acc.flags == facc.flags & ~O.F_COVERAGE
                 for a, b in ((acc.h_sum, facc.h_sum), (acc.g_sum, facc.g_sum),
                              (acc.m_sum, facc.m_sum), (acc.severity, facc.severity)):
                     assert a == pytest.approx(b, rel=1e-12, abs=1e-9)
@@ -600,3 +601,34 @@ def test_partial_equals_full_and_move_back(wl):
                 assert bacc.n_samples == base_acc.n_samples
                 assert bacc.h_sum == pytest.approx(base_acc.h_sum, rel=1e-12)
                 assert bacc.g_sum == pytest.approx(base_acc.g_sum, rel=1e-12)
+
+
+def test_coverage_flag_detects_gaps_and_overlaps():
+    """Row a9 coverage check: per-side owned-sample counts vs the base mesh's.
+
+    Moving a hull vertex inward leaves lattice points of the image uncovered
+    (gap); folding an interior vertex covers some points twice (overlap).
+    Identity and tangential hull motion keep the counts.
+    """
+    dims = (12, 12, 12)
+    g = [-0.5, 3.5, 7.5, 11.5]
+    base, tets = kuhn_lattice_mesh(g, g, g)
+    base = base.astype(np.float32)
+    I = blob_volume(dims, 3)
+    orc = make_oracle(dims, I, I, base, tets)
+    off = np.zeros((len(base), 6), np.float32)
+    assert orc.eval(off)[1].flags == 0
+    # corner (0,0,0) moved inward on the target side: the hull shrinks -> gap
+    gap = off.copy()
+    gap[0, 3:] = [2.0, 2.0, 2.0]
+    _, acc = orc.eval(gap)
+    assert acc.flags & O.F_COVERAGE and acc.n_samples < 2 * 12 ** 3
+    # fold of an interior vertex on the source side: overlap (and a fold)
+    j = 1 * 16 + 1 * 4 + 1
+    t = int(np.nonzero((tets == j).any(1))[0][0])
+    others = [v for v in tets[t] if v != j]
+    c = base[others].astype(np.float64).mean(0)
+    fold = off.copy()
+    fold[j, :3] = (2 * c - base[j]) - base[j]
+    _, acc = orc.eval(fold)
+    assert acc.folds > 0 and acc.flags & O.F_COVERAGE
