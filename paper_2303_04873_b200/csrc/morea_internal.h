@@ -27,7 +27,8 @@ struct __align__(16) SideRec {
   float d0[3];                // displacement at lo
   float eps[3];               // fp32 position filter bound per axis (0 = exact axis)
   int flags;                  // bit 0: rasterize; bit 1: every position of the bbox is inside
-                              // [0, n-1) with margin (no clamp needed)
+                              // [0, n-1) with margin (no clamp needed); bit 2: every face is a
+                              // regular lower/upper face (fast row intervals)
   float vy[4], vz[4];         // vertex y, z (voxel units, exact) for per-slice y ranges
   int lo[3], hi[3];           // lattice bbox clipped to the image
   int U[4][3];                // Q_other - Q_own per vertex
@@ -58,11 +59,14 @@ struct Volumes {
   double sp[3];
   const float* I[2];
   const unsigned char* band[2];  // per voxel bit i = [D_i(q) < r]; nullptr when K == 0
+  const uint2* own[2];           // per voxel (bits of I_side(q), band bits): one 8-byte load
   const float* dmap[2];          // K * V fp32 per side
   int K;
   double r, inv_r;
   float fnx2, fny2, fnz2, fny;  // (n - 2) per axis and ny as floats (constant-bank operands)
   const double* w;  // device: w[side * kMaxPairs + i] = |C_i| / |G_side|
+  const float* wf;  // device: wf[side * kMaxPairs + i] = w / r (fp32)
+  float rf;         // r (fp32)
   // texture-gather path: I_s / I_t and the maps as tall 2D textures (texel (x, y + ny z)),
   // gathered 2x2 per slice (tld4); 0 / nullptr when the volume exceeds the gather limits
   unsigned long long texI[2];
@@ -112,6 +116,8 @@ cudaError_t launch_distance_maps(const float* pts, const long long* off, int K, 
                                  int nz, const double sp[3], float* dmap, cudaStream_t s);
 cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, unsigned char* band,
                              cudaStream_t s);
+cudaError_t launch_own_records(const float* I, const unsigned char* band, long long V, uint2* out,
+                               cudaStream_t s);
 cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s);
 cudaError_t launch_raster(const EvalArgs& a, int grid, cudaStream_t s);
 int raster_blocks_per_sm(bool tex);

@@ -197,7 +197,10 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
       G.eps[a] = (float)ldexp(bound, -19);
     }
   }
-  G.flags = 1 | (inside ? 2 : 0);
+  bool regular = true;
+#pragma unroll
+  for (int k = 0; k < 4; k++) regular = regular && (G.ftype[k] == 1 || G.ftype[k] == -1);
+  G.flags = 1 | (inside ? 2 : 0) | (regular ? 4 : 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -320,7 +323,7 @@ __device__ __forceinline__ i64 face_e(const SideRec& R, int k, int x, int y, int
   return 1024 * (R.nrm[k][0] * x + R.nrm[k][1] * y + R.nrm[k][2] * z) - R.cst[k];
 }
 
-__device__ __noinline__ void row_interval(const SideRec& R, int y, int z, int& xl, int& xh) {
+__device__ __noinline__ void row_interval_exact(const SideRec& R, int y, int z, int& xl, int& xh) {
   const int lo = R.lo[0], hi = R.hi[0];
   xl = lo;
   xh = hi;
@@ -366,6 +369,38 @@ __device__ __noinline__ void row_interval(const SideRec& R, int y, int z, int& x
     if (t > 0) xl = max(xl, xi);
     else xh = min(xh, xi);
   }
+}
+
+// Fast path for items whose four faces are regular (n_x != 0, small crossing
+// error bound): four fp32 crossings; the exact routine only when a crossing is
+// within its bound of an integer.
+__device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, int& xl, int& xh) {
+  if (!(R.flags & 4)) {
+    row_interval_exact(R, y, z, xl, xh);
+    return;
+  }
+  const int lo = R.lo[0], hi = R.hi[0];
+  const float dy = (float)(y - R.lo[1]), dz = (float)(z - R.lo[2]);
+  const float flo = (float)lo - 4.5f, fhi = (float)hi + 4.5f;
+  const int4 types = *reinterpret_cast<const int4*>(R.ftype);
+  const int tk[4] = {types.x, types.y, types.z, types.w};
+  int l = lo, h = hi;
+  bool amb = false;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const float4 fc4 = R.face[k];
+    const float xs = fminf(fmaxf(fmaf(fc4.z, dz, fmaf(fc4.y, dy, fc4.x)), flo), fhi);
+    amb = amb || (fabsf(xs - rintf(xs)) <= fc4.w);
+    const int c = __float2int_ru(xs);  // lower face: smallest x > x*; upper: largest x < x* = c - 1
+    if (tk[k] > 0) l = max(l, c);
+    else h = min(h, c - 1);
+  }
+  if (amb) {
+    row_interval_exact(R, y, z, xl, xh);
+    return;
+  }
+  xl = l;
+  xh = h;
 }
 
 // Conservative y range of the tet's cross-section with the plane z (exact
@@ -650,9 +685,12 @@ struct Sample {
         gather((o == 0 ? V.dmap[0] : V.dmap[1]) + (long long)i * V.V, 0ull, 0.f, 0.f, base, e);
       }
       const float Dp = tri(e, ea.z, ea.w, fz, 1.f - ea.z, 1.f - ea.w, 1.f - fz);
-      const double dd = (double)d - (double)Dp;
-      // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit)
-      acc.g += __ldg(&V.w[s * kMaxPairs + i]) * ((V.r - (double)d) * V.inv_r) * dd * dd;
+      const float dd = d - Dp;
+      // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit); term in fp32,
+      // sum in fp64
+      const float wr = __ldg(&V.wf[s * kMaxPairs + i]);  // w_i / r
+      const float rd = (float)(V.r - (double)d);          // r - d exactly rounded (d may be ~r)
+      acc.g += (double)(wr * rd * (dd * dd));
     }
   }
 
@@ -706,12 +744,9 @@ struct Sample {
 #endif
     const int nx = V.nx, ny = V.ny, nz = V.nz;
     const int lin = ra.y + k;
-    const float a = __ldg(&vol(SIDE)[lin]);
-#if MOREA_ABLATE == 5
-    const unsigned bm = (a > 2.0f) ? 1u : 0u;
-#else
-    const unsigned bm = (V.K > 0 && valid) ? (unsigned)__ldg(&V.band[SIDE][lin]) : 0u;
-#endif
+    const uint2 own = __ldg(&(SIDE == 0 ? V.own[0] : V.own[1])[lin]);
+    const float a = __uint_as_float(own.x);
+    const unsigned bm = valid ? own.y : 0u;
     const float kf = (float)k;
     const float4 s0 = sc0;
     const float dx = fmaf(s0.x, kf, __int_as_float(ra.z)), dy = fmaf(s0.y, kf, __int_as_float(ra.w)),
@@ -1169,6 +1204,20 @@ __global__ void k_band_mask(const float* __restrict__ dmap, int K, long long V, 
       if ((double)dmap[(long long)i * V + v] < r) m |= 1u << i;
     band[v] = (unsigned char)m;
   }
+}
+
+// own-side record per voxel: (bits of I(q), band bits) -> one 8-byte load per sample
+__global__ void k_own_records(const float* __restrict__ I, const unsigned char* __restrict__ band,
+                              long long V, uint2* __restrict__ out) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
+       v += (long long)gridDim.x * blockDim.x)
+    out[v] = make_uint2(__float_as_uint(I[v]), band ? (unsigned)band[v] : 0u);
+}
+
+cudaError_t launch_own_records(const float* I, const unsigned char* band, long long V, uint2* out,
+                               cudaStream_t s) {
+  k_own_records<<<2048, 256, 0, s>>>(I, band, V, out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, unsigned char* band,
