@@ -431,10 +431,12 @@ __device__ __noinline__ void slice_y_range(const SideRec& R, int z, int& ylo, in
   yhi = min(R.hi[1], (int)floorf(fminf(ymax + 1e-3f, 1.0e6f)));
 }
 
-constexpr int kQueueCap = 64;  // < 32 pending + one round of <= 32
+constexpr int kQueueCap = 64;     // < 32 pending + one round of <= 32
+constexpr int kStartWords = 128;  // row-start bitmap window: 4096 samples
 
 struct WarpSmem {
   SideRec R;
+  unsigned starts[kStartWords];  // row-start bitmap of the current row chunk
   int4 row_a[32];    // (exclusive prefix, linear index of row start, dx0, dy0 as float bits)
   float4 row_b[32];  // (dz0, xl, y, z): fp32 displacement z at the row start, row start as floats
   float4 sc0, sc1;   // per-side sample constants (see Sample)
@@ -514,22 +516,38 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, WarpSme
         S.row_a[c] = make_int4(start, (z * ny + y) * nx + xl, __float_as_int(drow.x), __float_as_int(drow.y));
         S.row_b[c] = make_float4(drow.z, (float)xl, (float)y, (float)z);
       }
-      __syncwarp();
-      const int last = __popc(ne) - 1;
-      int rprev = -1;
-#if MOREA_ABLATE == 6
       f.count_only(lane == 0 ? total : 0);
+#if MOREA_ABLATE == 6
       continue;
 #endif
-      for (int s0 = 0; s0 < total; s0 += 32) {
-        const unsigned bit = (len > 0 && start >= s0 && start < s0 + 32) ? (1u << (start - s0)) : 0u;
-        const unsigned M = __reduce_or_sync(FULLMASK, bit);
-        const int row = min(rprev + __popc(M & ((2u << lane) - 1u)), last);
-        rprev += __popc(M);
-        const int idx = s0 + lane;
-        const bool valid = idx < total;
-        const int4 ra = S.row_a[row];
-        f.sample(ra, S.row_b[row], valid ? idx - ra.x : 0, valid);
+      // Sweep in windows of 32 kStartWords samples.  The bitmap holds the row
+      // starts of the window (bit s of word s/32); a lane's row is the number of
+      // starts <= its sample index, minus one.  Past the end that is the last row
+      // (no starts there), evaluated with valid = false.  Blocks of 16 steps; the
+      // fp32 partial sums are flushed between blocks.
+      const unsigned le_mask = (2u << lane) - 1u;
+      int rprev = -1;
+      for (int base = 0; base < total; base += 32 * kStartWords) {
+        const int nw = min(kStartWords, (total - base + 31) >> 5);
+        __syncwarp();
+        for (int w = lane; w < nw; w += 32) S.starts[w] = 0u;
+        __syncwarp();
+        if (len > 0 && start >= base && start < base + 32 * kStartWords)
+          atomicOr(&S.starts[(start - base) >> 5], 1u << (start & 31));
+        __syncwarp();
+        for (int w0 = 0; w0 < nw; w0 += 16) {
+          const int wend = min(nw, w0 + 16);
+          for (int w = w0; w < wend; w++) {
+            const unsigned M = S.starts[w];
+            const int row = rprev + __popc(M & le_mask);
+            rprev += __popc(M);
+            const int idx = base + (w << 5) + lane;
+            const bool valid = idx < total;
+            const int4 ra = S.row_a[row];
+            f.sample(ra, S.row_b[row], valid ? idx - ra.x : 0, valid);
+          }
+          f.flush_h();
+        }
       }
       __syncwarp();
     }
@@ -725,6 +743,11 @@ struct Sample {
 
   __device__ __forceinline__ void count_only(int t) { acc.n += t; }
 
+  __device__ __forceinline__ void flush_h() {
+    acc.h += (double)acc.hf;
+    acc.hf = 0.f;
+  }
+
   // evaluate what is left in the queue (end of a side)
   __device__ __forceinline__ void drain(int s) {
     __syncwarp();
@@ -784,14 +807,9 @@ struct Sample {
     } else {
       h = (a == 0.f && !fg) ? 0.f : 1.f;
     }
-    // fp32 partial sums over at most 16 steps, flushed into the fp64 lane sum by the
-    // (warp-uniform) step counter
+    // fp32 partial sum over at most 16 steps; raster() flushes it into the fp64
+    // lane sum (flush_h) every 16 steps
     acc.hf += valid ? h : 0.f;
-    acc.n += valid ? 1 : 0;
-    if ((++acc.steps & 15) == 0) {
-      acc.h += (double)acc.hf;
-      acc.hf = 0.f;
-    }
     // a6: band entries go to the per-warp queue, evaluated 32 at a time
 #if MOREA_ABLATE == 4
     acc.nb += __popc(bm);
@@ -843,7 +861,11 @@ __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int l
 template <bool TEX>
 __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(const EvalArgs A) {
   __shared__ WarpSmem smem[kWarpsPerBlock];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index and lane through volatile asm: kept in registers instead of being
+  // re-derived from special registers at every use
+  int warp, lane;
+  asm volatile("shr.u32 %0, %1, 5;" : "=r"(warp) : "r"(threadIdx.x));
+  asm volatile("and.b32 %0, %1, 31;" : "=r"(lane) : "r"(threadIdx.x));
   WarpSmem& S = smem[warp];
   const long long per_v = (long long)A.n_entries * A.P;
   const long long n_items = per_v * A.n_raster_versions;
@@ -1096,6 +1118,7 @@ cudaError_t launch_check_folds(const MeshDev& m, const double sp[3], int P, cons
 struct OwnerSample {
   int* owner;
   int tet;
+  __device__ __forceinline__ void flush_h() {}
   __device__ __forceinline__ void count_only(int) {}
   __device__ __forceinline__ void sample(const int4& ra, const float4&, int k, bool valid) {
     if (!valid) return;
