@@ -70,13 +70,11 @@ struct morea_ctx {
   double sp[3] = {1, 1, 1};
   double r = 0;
   double w[2][kMaxPairs] = {};
-  DevBuf I[2], band[2], dmap[2], wts, wtsf, own[2];
+  DevBuf I[2], band[2], dmap[2], wts, wtsf, own;
   // texture-gather copies (tall 2D arrays) of I_s, I_t and the maps
   bool use_tex = false;
-  cudaArray_t arrI[2] = {nullptr, nullptr};
-  cudaTextureObject_t texI[2] = {0, 0};
-  cudaArray_t arrM[2] = {nullptr, nullptr};
-  cudaTextureObject_t texM[2] = {0, 0};
+  cudaArray_t arrI = nullptr, arrM = nullptr;
+  cudaTextureObject_t texI = 0, texM = 0;
   // mesh
   bool have_mesh = false;
   int N = 0, T = 0, spoke_mode = 0;
@@ -234,13 +232,11 @@ Volumes volumes_of(const morea_ctx* c) {
   v.w = c->wts.as<double>();
   v.wf = c->wtsf.as<float>();
   v.rf = (float)c->r;
-  v.own[0] = c->own[0].as<uint2>();
-  v.own[1] = c->own[1].as<uint2>();
+  v.own[0] = c->own.as<uint2>();
+  v.own[1] = v.own[0] ? v.own[0] + c->V : nullptr;
   v.use_tex = c->use_tex ? 1 : 0;
-  v.texI[0] = c->texI[0];
-  v.texI[1] = c->texI[1];
-  v.texM[0] = c->texM[0];
-  v.texM[1] = c->texM[1];
+  v.texI = c->texI;
+  v.texM = c->texM;
   v.fnx = (float)c->nx;
   return v;
 }
@@ -393,32 +389,26 @@ int build_plan(morea_ctx* ctx, int G, const int32_t* grp_off_in, const int32_t* 
 }
 
 void release_textures(morea_ctx* ctx) {
-  for (int s = 0; s < 2; s++) {
-    if (ctx->texI[s]) cudaDestroyTextureObject(ctx->texI[s]);
-    if (ctx->arrI[s]) cudaFreeArray(ctx->arrI[s]);
-    ctx->texI[s] = 0;
-    ctx->arrI[s] = nullptr;
-  }
-  for (int s = 0; s < 2; s++) {
-    if (ctx->texM[s]) cudaDestroyTextureObject(ctx->texM[s]);
-    if (ctx->arrM[s]) cudaFreeArray(ctx->arrM[s]);
-    ctx->texM[s] = 0;
-    ctx->arrM[s] = nullptr;
-  }
+  if (ctx->texI) cudaDestroyTextureObject(ctx->texI);
+  if (ctx->arrI) cudaFreeArray(ctx->arrI);
+  if (ctx->texM) cudaDestroyTextureObject(ctx->texM);
+  if (ctx->arrM) cudaFreeArray(ctx->arrM);
+  ctx->texI = ctx->texM = 0;
+  ctx->arrI = ctx->arrM = nullptr;
   ctx->use_tex = false;
 }
 
-// `count` float volumes (nx x ny x nz, x-fastest, device, consecutive) as one 2D
-// gather texture: volume i, voxel (x, y, z) -> texel (x + i nx, y + ny z).  Point
+// `count` float volumes (nx x ny x nz, x-fastest, device) as one 2D gather
+// texture: volume j, voxel (x, y, z) -> texel (x + j nx, y + ny z).  Point
 // sampling, clamp, unnormalised coordinates.
-cudaError_t make_gather_texture(morea_ctx* ctx, const float* dev, int count, cudaArray_t* arr,
+cudaError_t make_gather_texture(morea_ctx* ctx, const float* const* src, int count, cudaArray_t* arr,
                                 cudaTextureObject_t* tex) {
   cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
   const size_t W = (size_t)ctx->nx * count, H = (size_t)ctx->ny * ctx->nz;
   cudaError_t e = cudaMallocArray(arr, &fd, W, H, cudaArrayTextureGather);
   if (e != cudaSuccess) return e;
-  for (int i = 0; i < count; i++) {
-    e = cudaMemcpy2DToArrayAsync(*arr, (size_t)i * ctx->nx * sizeof(float), 0, dev + (size_t)i * ctx->V,
+  for (int j = 0; j < count; j++) {
+    e = cudaMemcpy2DToArrayAsync(*arr, (size_t)j * ctx->nx * sizeof(float), 0, src[j],
                                  ctx->nx * sizeof(float), ctx->nx * sizeof(float), H,
                                  cudaMemcpyDeviceToDevice, ctx->stream);
     if (e != cudaSuccess) return e;
@@ -444,16 +434,19 @@ cudaError_t build_textures(morea_ctx* ctx) {
   int gw = 0, gh = 0;
   cudaDeviceGetAttribute(&gw, cudaDevAttrMaxTexture2DGatherWidth, ctx->device);
   cudaDeviceGetAttribute(&gh, cudaDevAttrMaxTexture2DGatherHeight, ctx->device);
-  if ((long long)ctx->nx * std::max(ctx->K, 1) > gw || (long long)ctx->ny * ctx->nz > gh) return cudaSuccess;
-  for (int s = 0; s < 2; s++) {
-    cudaError_t e = make_gather_texture(ctx, ctx->I[s].as<float>(), 1, &ctx->arrI[s], &ctx->texI[s]);
+  if ((long long)ctx->nx * 2 * std::max(ctx->K, 1) > gw || (long long)ctx->ny * ctx->nz > gh)
+    return cudaSuccess;
+  const float* vols[2] = {ctx->I[0].as<float>(), ctx->I[1].as<float>()};
+  cudaError_t e = make_gather_texture(ctx, vols, 2, &ctx->arrI, &ctx->texI);
+  if (e != cudaSuccess) return e;
+  if (ctx->K > 0) {
+    std::vector<const float*> maps;
+    for (int s = 0; s < 2; s++)
+      for (int i = 0; i < ctx->K; i++) maps.push_back(ctx->dmap[s].as<float>() + (size_t)i * ctx->V);
+    e = make_gather_texture(ctx, maps.data(), (int)maps.size(), &ctx->arrM, &ctx->texM);
     if (e != cudaSuccess) return e;
-    if (ctx->K > 0) {
-      e = make_gather_texture(ctx, ctx->dmap[s].as<float>(), ctx->K, &ctx->arrM[s], &ctx->texM[s]);
-      if (e != cudaSuccess) return e;
-    }
   }
-  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  e = cudaStreamSynchronize(ctx->stream);
   if (e == cudaSuccess) ctx->use_tex = true;
   return e;
 }
@@ -506,7 +499,7 @@ void morea_destroy(morea_ctx* ctx) {
     cudaEventDestroy(p.second);
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
-                    &ctx->dmap[1], &ctx->wts, &ctx->wtsf, &ctx->own[0], &ctx->own[1], &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
+                    &ctx->dmap[1], &ctx->wts, &ctx->wtsf, &ctx->own, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
                     &ctx->full_sched, &ctx->full_group_off, &ctx->geom, &ctx->scal, &ctx->hgn,
                     &ctx->counter, &ctx->stats, &ctx->st_off, &ctx->st_nv, &ctx->st_cache_in,
                     &ctx->st_base_acc, &ctx->st_obj, &ctx->st_acc, &ctx->st_cache_out,
@@ -594,11 +587,10 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
     for (int i = 0; i < kMaxPairs; i++) wf[s][i] = (float)(ctx->w[s][i] / ctx->r);
   CK(ctx->wtsf.ensure(sizeof(wf)));
   CK(cudaMemcpyAsync(ctx->wtsf.p, wf, sizeof(wf), cudaMemcpyHostToDevice, ctx->stream));
-  for (int s = 0; s < 2; s++) {
-    CK(ctx->own[s].ensure(V * sizeof(uint2)));
+  CK(ctx->own.ensure(2 * V * sizeof(uint2)));
+  for (int s = 0; s < 2; s++)
     CK(launch_own_records(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr, V,
-                          ctx->own[s].as<uint2>(), ctx->stream));
-  }
+                          ctx->own.as<uint2>() + (size_t)s * V, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(build_textures(ctx));
   ctx->have_images = true;

@@ -59,7 +59,9 @@ struct Volumes {
   double sp[3];
   const float* I[2];
   const unsigned char* band[2];  // per voxel bit i = [D_i(q) < r]; nullptr when K == 0
-  const uint2* own[2];           // per voxel (bits of I_side(q), band bits): one 8-byte load
+  // per voxel (bits of I_side(q), band bits): one 8-byte load; one allocation,
+  // own[1] = own[0] + V, so side s of voxel q is own[0][s V + q]
+  const uint2* own[2];
   const float* dmap[2];          // K * V fp32 per side
   int K;
   double r, inv_r;
@@ -67,12 +69,13 @@ struct Volumes {
   const double* w;  // device: w[side * kMaxPairs + i] = |C_i| / |G_side|
   const float* wf;  // device: wf[side * kMaxPairs + i] = w / r (fp32)
   float rf;         // r (fp32)
-  // texture-gather path: I_s / I_t and the maps as tall 2D textures (texel (x, y + ny z)),
-  // gathered 2x2 per slice (tld4); 0 / nullptr when the volume exceeds the gather limits
-  unsigned long long texI[2];
-  // the K maps of a side side by side in one gather texture: texel (x + i nx, y + ny z)
-  unsigned long long texM[2];
-  float fnx;  // nx as float (map offset in texM)
+  // texture-gather path (0 when the layout exceeds the gather limits): volumes as
+  // tall 2D textures, voxel (x, y, z) of volume j -> texel (x + j nx, y + ny z),
+  // gathered 2x2 per slice (tld4).  texI: volumes I_s, I_t; texM: the 2K maps,
+  // side s pair i at j = s K + i.
+  unsigned long long texI;
+  unsigned long long texM;
+  float fnx;  // nx as float (volume offset in the textures)
   int use_tex;
 };
 

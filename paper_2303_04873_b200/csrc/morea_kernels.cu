@@ -475,8 +475,8 @@ __device__ __forceinline__ int warp_search(int incl, int idx) {
 // a popc).  Lanes past the end evaluate sample 0 of the last row with
 // valid = false (no divergence).  All lanes of the warp must call it.
 template <class F>
-__device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, WarpSmem& S, int lane,
-                                       F& f) {
+__device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int loff, WarpSmem& S,
+                                       int lane, F& f) {
   const unsigned lt_mask = (1u << lane) - 1u;
   for (int z0 = R.lo[2]; z0 <= R.hi[2]; z0 += 32) {
     const int zl = z0 + lane;
@@ -513,7 +513,8 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, WarpSme
         drow.y = fmaf(R.A[1][2], oz, fmaf(R.A[1][1], oy, fmaf(R.A[1][0], ox, R.d0[1])));
         drow.z = fmaf(R.A[2][2], oz, fmaf(R.A[2][1], oy, fmaf(R.A[2][0], ox, R.d0[2])));
         drow.w = 0.f;
-        S.row_a[c] = make_int4(start, (z * ny + y) * nx + xl, __float_as_int(drow.x), __float_as_int(drow.y));
+        S.row_a[c] = make_int4(start, (z * ny + y) * nx + xl + loff, __float_as_int(drow.x),
+                               __float_as_int(drow.y));
         S.row_b[c] = make_float4(drow.z, (float)xl, (float)y, (float)z);
       }
       f.count_only(lane == 0 ? total : 0);
@@ -625,7 +626,8 @@ struct Sample {
   const SideRec& R;
   WarpSmem& S;
   const float4& sc0;  // shared: (A_x0, A_y0, A_z0, 0.5 - eps_x)  displacement gradient along x
-  const float4& sc1;  // shared: (0.5 - eps_y, 0.5 - eps_z, -, -)  ambiguity thresholds on |f - 0.5|
+  const float4& sc1;  // shared: (0.5 - eps_y, 0.5 - eps_z, uoff, -): ambiguity thresholds on
+                      // |f - 0.5|; uoff = texel x offset of corner i0 + 1 in the gather layout
   Acc& acc;
   bool clamp;         // some position of the item may leave [0, n-1): apply the O5 clamp
   int side;           // runtime side when SIDE_T < 0 (warp-uniform)
@@ -633,7 +635,6 @@ struct Sample {
   // per-side data selected by a warp-uniform branch on compile-time parameter
   // offsets, so texture handles stay in uniform registers
   __device__ __forceinline__ const float* vol(int s) const { return s == 0 ? V.I[0] : V.I[1]; }
-  __device__ __forceinline__ unsigned long long tex(int s) const { return s == 0 ? V.texI[0] : V.texI[1]; }
 
   // the 8 corners (i0 .. i0+1)^3: two 2x2 texture gathers (tld4) or 8 loads
   __device__ __forceinline__ void gather(const float* __restrict__ vol, unsigned long long tex,
@@ -653,17 +654,10 @@ struct Sample {
     }
   }
 
-  // tld4 pair with the handle taken straight from the parameter space inside a
-  // branch per side (each tld4 sees a compile-time handle: no waterfall loop)
-  __device__ __forceinline__ void gather_tex(int which, float u, float v, float c[8]) const {
-    float4 g0, g1;
-    if (which == 0) {
-      g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texI[0], u, v, 0);
-      g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texI[0], u, v + V.fny, 0);
-    } else {
-      g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texI[1], u, v, 0);
-      g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texI[1], u, v + V.fny, 0);
-    }
+  // tld4 pair (slices i0_z and i0_z + 1); u carries the volume's x offset
+  __device__ __forceinline__ void gather_tex(float u, float v, float c[8]) const {
+    const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texI, u, v, 0);
+    const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texI, u, v + V.fny, 0);
     // gather order: (x0,y1) (x1,y1) (x1,y0) (x0,y0)
     c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
     c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
@@ -684,18 +678,14 @@ struct Sample {
       const int4 eb = S.qb[q0 + lane];
       const float fz = __int_as_float(eb.x);
       const int i = eb.z;
-      const float d = __ldg(&(s == 0 ? V.dmap[0] : V.dmap[1])[(long long)i * V.V + eb.y]);
+      // eb.y = s V + q (the own-record index)
+      const float d = __ldg(&(s == 0 ? V.dmap[0] : V.dmap[1])[(long long)(i - s) * V.V + eb.y]);
       float e[8];
       if (TEX) {
-        const float uu = fmaf((float)i, V.fnx, ea.x);
-        float4 g0, g1;
-        if (o == 0) {
-          g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texM[0], uu, ea.y, 0);
-          g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texM[0], uu, ea.y + V.fny, 0);
-        } else {
-          g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texM[1], uu, ea.y, 0);
-          g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texM[1], uu, ea.y + V.fny, 0);
-        }
+        // ea.x = i0_x + 1 + o nx (texel of I_o); map (o, i) is volume o K + i of texM
+        const float uu = fmaf((float)(o * (V.K - 1) + i), V.fnx, ea.x);
+        const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texM, uu, ea.y, 0);
+        const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texM, uu, ea.y + V.fny, 0);
         e[0] = g0.w; e[1] = g0.z; e[2] = g0.x; e[3] = g0.y;
         e[4] = g1.w; e[5] = g1.z; e[6] = g1.x; e[7] = g1.y;
       } else {
@@ -767,7 +757,7 @@ struct Sample {
 #endif
     const int nx = V.nx, ny = V.ny, nz = V.nz;
     const int lin = ra.y + k;
-    const uint2 own = __ldg(&(SIDE == 0 ? V.own[0] : V.own[1])[lin]);
+    const uint2 own = __ldg(&V.own[0][lin]);  // lin = SIDE V + q
     const float a = __uint_as_float(own.x);
     const unsigned bm = valid ? own.y : 0u;
     const float kf = (float)k;
@@ -791,10 +781,10 @@ struct Sample {
     }
     const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
     // texel coordinates of corner i0 + (1, 1) in the (x, y + ny z) layout (exact floats)
-    const float u = ix + 1.0f, v = fmaf(iz, V.fny, iy) + 1.0f;
+    const float u = ix + s1.z, v = fmaf(iz, V.fny, iy) + 1.0f;
     const int base = TEX ? 0 : ((int)iz * ny + (int)iy) * nx + (int)ix;
     float c[8];
-    if (TEX) gather_tex(OTH, u, v, c);
+    if (TEX) gather_tex(u, v, c);
     else gather(vol(OTH), 0ull, u, v, base, c);
     const float b = tri(c, fx, fy, fz, gx, gy, gz);
     bool fg = b > 0.f;
@@ -845,13 +835,15 @@ __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int l
   const SideRec& R = S.R;
   if (lane == 0) {
     S.sc0 = make_float4(R.A[0][0], R.A[1][0], R.A[2][0], 0.5f - R.eps[0]);
-    S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], 0.f, 0.f);
+    // texel x of corner i0 + 1: I_o is volume o of texI (TEX), else a plain index
+    const float uoff = 1.0f + (TEX ? (float)((1 - (SIDE_T >= 0 ? SIDE_T : side)) * V.nx) : 0.0f);
+    S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], uoff, 0.f);
   }
   __syncwarp();
   if (lane == 0) S.qn = 0;
   __syncwarp();
   Sample<TEX, SIDE_T> f{V, R, S, S.sc0, S.sc1, acc, (R.flags & 2) == 0, side};
-  raster(R, V.nx, V.ny, S, lane, f);
+  raster(R, V.nx, V.ny, (SIDE_T >= 0 ? SIDE_T : side) * (int)V.V, S, lane, f);
   f.drain(SIDE_T >= 0 ? SIDE_T : side);
 }
 
@@ -1138,7 +1130,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_owner_map(const EvalArgs A, 
   load_rec(S, &A.geom[2 * (long long)tet + side], lane);
   if (!(S.R.flags & 1)) return;
   OwnerSample f{owner, tet};
-  raster(S.R, A.vol.nx, A.vol.ny, S, lane, f);
+  raster(S.R, A.vol.nx, A.vol.ny, 0, S, lane, f);
 }
 
 __global__ void k_fill_int(int* p, long long n, int v) {
