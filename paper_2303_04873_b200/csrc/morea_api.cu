@@ -70,7 +70,7 @@ struct morea_ctx {
   double sp[3] = {1, 1, 1};
   double r = 0;
   double w[2][kMaxPairs] = {};
-  DevBuf I[2], band[2], dmap[2], wts, wtsf, own;
+  DevBuf I[2], band[2], dmap[2], wts, own;
   // texture-gather copies (tall 2D arrays) of I_s, I_t and the maps
   bool use_tex = false;
   cudaArray_t arrI = nullptr, arrM = nullptr;
@@ -230,8 +230,10 @@ Volumes volumes_of(const morea_ctx* c) {
   v.fnz2 = (float)(c->nz - 2);
   v.fny = (float)c->ny;
   v.w = c->wts.as<double>();
-  v.wf = c->wtsf.as<float>();
+  for (int s = 0; s < 2; s++)
+    for (int i = 0; i < kMaxPairs; i++) v.wf[s][i] = c->r > 0 ? (float)(c->w[s][i] / c->r) : 0.f;
   v.rf = (float)c->r;
+  v.rlo = (float)(c->r - (double)v.rf);
   v.own[0] = c->own.as<uint2>();
   v.own[1] = v.own[0] ? v.own[0] + c->V : nullptr;
   v.use_tex = c->use_tex ? 1 : 0;
@@ -499,7 +501,7 @@ void morea_destroy(morea_ctx* ctx) {
     cudaEventDestroy(p.second);
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
-                    &ctx->dmap[1], &ctx->wts, &ctx->wtsf, &ctx->own, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
+                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
                     &ctx->full_sched, &ctx->full_group_off, &ctx->geom, &ctx->scal, &ctx->hgn,
                     &ctx->counter, &ctx->stats, &ctx->st_off, &ctx->st_nv, &ctx->st_cache_in,
                     &ctx->st_base_acc, &ctx->st_obj, &ctx->st_acc, &ctx->st_cache_out,
@@ -582,11 +584,6 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
   }
   CK(ctx->wts.ensure(sizeof(ctx->w)));
   CK(cudaMemcpyAsync(ctx->wts.p, ctx->w, sizeof(ctx->w), cudaMemcpyHostToDevice, ctx->stream));
-  float wf[2][kMaxPairs];
-  for (int s = 0; s < 2; s++)
-    for (int i = 0; i < kMaxPairs; i++) wf[s][i] = (float)(ctx->w[s][i] / ctx->r);
-  CK(ctx->wtsf.ensure(sizeof(wf)));
-  CK(cudaMemcpyAsync(ctx->wtsf.p, wf, sizeof(wf), cudaMemcpyHostToDevice, ctx->stream));
   CK(ctx->own.ensure(2 * V * sizeof(uint2)));
   for (int s = 0; s < 2; s++)
     CK(launch_own_records(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr, V,

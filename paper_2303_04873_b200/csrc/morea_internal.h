@@ -67,8 +67,8 @@ struct Volumes {
   double r, inv_r;
   float fnx2, fny2, fnz2, fny;  // (n - 2) per axis and ny as floats (constant-bank operands)
   const double* w;  // device: w[side * kMaxPairs + i] = |C_i| / |G_side|
-  const float* wf;  // device: wf[side * kMaxPairs + i] = w / r (fp32)
-  float rf;         // r (fp32)
+  float wf[2][kMaxPairs];  // w / r (fp32), in the parameter space
+  float rf, rlo;           // r = rf + rlo (fp32 head and tail)
   // texture-gather path (0 when the layout exceeds the gather limits): volumes as
   // tall 2D textures, voxel (x, y, z) of volume j -> texel (x + j nx, y + ny z),
   // gathered 2x2 per slice (tld4).  texI: volumes I_s, I_t; texM: the 2K maps,

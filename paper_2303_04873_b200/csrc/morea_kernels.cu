@@ -444,7 +444,6 @@ struct WarpSmem {
   // band-entry queue of the guidance term (a6): entries are evaluated 32 at a time
   float4 qa[kQueueCap];  // (u, v, fx, fy): footprint texel coordinates and weights
   int4 qb[kQueueCap];    // (fz bits, own linear index, pair i, -)
-  int qn;                // entries queued (warp-uniform)
 };
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -616,8 +615,9 @@ __device__ __forceinline__ float plerp(float a, float b, float t, float omt) {
 struct Acc {
   double h, g;  // per-lane sums of h and of the guidance term (fp64)
   float hf;     // fp32 partial sum of h over the last < 16 steps (flushed into h)
+  float gf;     // fp32 partial sum of guidance terms since the last flush (into g)
   int n, nb;    // samples, band entries
-  int steps;    // sample steps (warp-uniform)
+  int qn;       // band entries in the per-warp queue (warp-uniform)
 };
 
 template <bool TEX, int SIDE_T>
@@ -669,41 +669,45 @@ struct Sample {
                  plerp(plerp(c[4], c[5], fx, gx), plerp(c[6], c[7], fx, gx), fy, gy), fz, gz);
   }
 
-  // guidance term of the queued entries [q0, q0 + cnt) (a6, O8), one per lane
-  __device__ __forceinline__ void flush(int q0, int cnt, int s) {
-    const int lane = threadIdx.x & 31;
-    if (lane < cnt) {
-      const int o = 1 - s;
-      const float4 ea = S.qa[q0 + lane];
-      const int4 eb = S.qb[q0 + lane];
-      const float fz = __int_as_float(eb.x);
-      const int i = eb.z;
-      // eb.y = s V + q (the own-record index)
-      const float d = __ldg(&(s == 0 ? V.dmap[0] : V.dmap[1])[(long long)(i - s) * V.V + eb.y]);
-      float e[8];
-      if (TEX) {
-        // ea.x = i0_x + 1 + o nx (texel of I_o); map (o, i) is volume o K + i of texM
-        const float uu = fmaf((float)(o * (V.K - 1) + i), V.fnx, ea.x);
-        const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texM, uu, ea.y, 0);
-        const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texM, uu, ea.y + V.fny, 0);
-        e[0] = g0.w; e[1] = g0.z; e[2] = g0.x; e[3] = g0.y;
-        e[4] = g1.w; e[5] = g1.z; e[6] = g1.x; e[7] = g1.y;
-      } else {
-        const int base = (int)(ea.y - 1.0f) * V.nx + (int)(ea.x - 1.0f);
-        gather((o == 0 ? V.dmap[0] : V.dmap[1]) + (long long)i * V.V, 0ull, 0.f, 0.f, base, e);
-      }
-      const float Dp = tri(e, ea.z, ea.w, fz, 1.f - ea.z, 1.f - ea.w, 1.f - fz);
-      const float dd = d - Dp;
-      // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit); term in fp32,
-      // sum in fp64
-      const float wr = __ldg(&V.wf[s * kMaxPairs + i]);  // w_i / r
-      const float rd = (float)(V.r - (double)d);          // r - d exactly rounded (d may be ~r)
-      acc.g += (double)(wr * rd * (dd * dd));
+  // guidance term of one band entry (a6, O8): pair i of the side-s sample with
+  // own-record index lin = s V + q, mapped to texel u, v and weights fx, fy, fz
+  __device__ __forceinline__ void entry(float u, float v, float fx, float fy, float fz, int lin,
+                                        int i, int s) {
+    const int o = 1 - s;
+#if MOREA_ABLATE == 8
+    const float d = 0.5f * (float)i;
+#else
+    const float d = __ldg(&(s == 0 ? V.dmap[0] : V.dmap[1])[(long long)(i - s) * V.V + lin]);
+#endif
+    float e[8];
+#if MOREA_ABLATE == 7
+    if (true) {
+      for (int j = 0; j < 8; j++) e[j] = u + (float)j * v;
+    } else
+#endif
+    if (TEX) {
+      // u = i0_x + 1 + o nx (texel of I_o); map (o, i) is volume o K + i of texM
+      const float uu = fmaf((float)(o * (V.K - 1) + i), V.fnx, u);
+      const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texM, uu, v, 0);
+      const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texM, uu, v + V.fny, 0);
+      e[0] = g0.w; e[1] = g0.z; e[2] = g0.x; e[3] = g0.y;
+      e[4] = g1.w; e[5] = g1.z; e[6] = g1.x; e[7] = g1.y;
+    } else {
+      const int base = (int)(v - 1.0f) * V.nx + (int)(u - 1.0f);
+      gather((o == 0 ? V.dmap[0] : V.dmap[1]) + (long long)i * V.V, 0ull, 0.f, 0.f, base, e);
     }
+    const float Dp = tri(e, fx, fy, fz, 1.f - fx, 1.f - fy, 1.f - fz);
+    const float dd = d - Dp;
+    // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit).  r - d as
+    // (r_f - d) + (r - r_f): exact first difference for d >= r_f / 2, so the
+    // relative error of the small differences near the band edge stays at ulp
+    // level.  Term in fp32, partial sums in fp32 (flushed with h), sum in fp64.
+    const float rd = (V.rf - d) + V.rlo;
+    acc.gf += V.wf[s][i] * rd * (dd * dd);
   }
 
-  // append the band entries of this step's samples (one round per set bit), flush
-  // full batches of 32
+  // Band entries of this step's samples, one round per set bit, go to the
+  // per-warp queue, evaluated 32 at a time (acc.qn: queued count, warp-uniform).
   __device__ __forceinline__ void enqueue(unsigned bm, int lin, float u, float v, float fx, float fy,
                                           float fz, int s) {
     const int lane = threadIdx.x & 31;
@@ -711,23 +715,25 @@ struct Sample {
     while (true) {
       const unsigned take = __ballot_sync(FULLMASK, bm != 0u);
       if (!take) break;
-      const int qn = S.qn;
+#if MOREA_ABLATE == 9
+      if (lane == 0) S.stat[2] += 1;
+#endif
       if (bm) {
         const int i = __ffs(bm) - 1;
-        bm &= bm - 1;
-        const int pos = qn + __popc(take & ((1u << lane) - 1u));
+        const int pos = acc.qn + __popc(take & ((1u << lane) - 1u));
         S.qa[pos] = make_float4(u, v, fx, fy);
         S.qb[pos] = make_int4(__float_as_int(fz), lin, i, 0);
+        bm &= bm - 1;
       }
-      __syncwarp();
-      int n = qn + __popc(take);
-      if (n >= 32) {
-        flush(n - 32, 32, s);
-        n -= 32;
+      acc.qn += __popc(take);
+      if (acc.qn >= 32) {
+        acc.qn -= 32;
+        __syncwarp();
+        const float4 ea = S.qa[acc.qn + lane];
+        const int4 eb = S.qb[acc.qn + lane];
+        entry(ea.x, ea.y, ea.z, ea.w, __int_as_float(eb.x), eb.y, eb.z, s);
+        __syncwarp();
       }
-      __syncwarp();
-      if (lane == 0) S.qn = n;
-      __syncwarp();
     }
   }
 
@@ -736,16 +742,22 @@ struct Sample {
   __device__ __forceinline__ void flush_h() {
     acc.h += (double)acc.hf;
     acc.hf = 0.f;
+    acc.g += (double)acc.gf;
+    acc.gf = 0.f;
   }
 
   // evaluate what is left in the queue (end of a side)
   __device__ __forceinline__ void drain(int s) {
+    const int lane = threadIdx.x & 31;
     __syncwarp();
-    const int n = S.qn;
-    if (n > 0) flush(0, n, s);
+    if (lane < acc.qn) {
+      const float4 ea = S.qa[lane];
+      const int4 eb = S.qb[lane];
+      entry(ea.x, ea.y, ea.z, ea.w, __int_as_float(eb.x), eb.y, eb.z, s);
+    }
     __syncwarp();
-    if ((threadIdx.x & 31) == 0) S.qn = 0;
-    __syncwarp();
+    acc.qn = 0;
+    flush_h();
   }
 
   __device__ __forceinline__ void sample(const int4& ra, const float4& rb, int k, bool valid) {
@@ -840,8 +852,6 @@ __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int l
     S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], uoff, 0.f);
   }
   __syncwarp();
-  if (lane == 0) S.qn = 0;
-  __syncwarp();
   Sample<TEX, SIDE_T> f{V, R, S, S.sc0, S.sc1, acc, (R.flags & 2) == 0, side};
   raster(R, V.nx, V.ny, (SIDE_T >= 0 ? SIDE_T : side) * (int)V.V, S, lane, f);
   f.drain(SIDE_T >= 0 ? SIDE_T : side);
@@ -873,7 +883,7 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
     const int sol = (int)(rem - (long long)es * A.P);
     const int e = A.sched[es];
     const long long i = ((long long)v * A.n_entries + e) * A.P + sol;
-    Acc acc{0.0, 0.0, 0.f, 0, 0, 0};
+    Acc acc{0.0, 0.0, 0.f, 0.f, 0, 0, 0};
 #if MOREA_SIDE_TEMPLATE
     load_rec(S, &A.geom[2 * i], lane);
     if (S.R.flags & 1) raster_side<TEX, 0>(A.vol, S, lane, acc, 0);
