@@ -10,7 +10,10 @@ namespace morea {
 constexpr int kMaxPairs = 8;
 constexpr int kQLo = -256 * 1024;  // Q.10 window (O1)
 constexpr int kQHi = 768 * 1024;
-constexpr int kWarpsPerBlock = 8;
+#ifndef MOREA_WARPS_PER_BLOCK
+#define MOREA_WARPS_PER_BLOCK 2  // k_raster / k_owner_map blocks (one WarpSmem per warp)
+#endif
+constexpr int kWarpsPerBlock = MOREA_WARPS_PER_BLOCK;
 constexpr int kRasterThreads = 32 * kWarpsPerBlock;
 
 // Geometry of one (version, entry, solution, side) item, written by k_setup and

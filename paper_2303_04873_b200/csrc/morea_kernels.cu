@@ -36,7 +36,7 @@
 #endif
 
 #ifndef MOREA_RASTER_MINB
-#define MOREA_RASTER_MINB 4  // resident 256-thread blocks per SM the register budget targets
+#define MOREA_RASTER_MINB 14  // resident 64-thread blocks per SM: 28 warps at 72 registers
 #endif
 
 namespace morea {
