@@ -23,6 +23,7 @@
  *   f_guidance, truncated distance maps      §4.1.3 eq. L338-342, App. A.3 L793-796 (O8)
  *   f_magnitude, 10 edges incl. 4 spokes     §4.1.1 eq. L251-259              (O9)
  *   partial evaluation (delta on dependents) §1, §4.2.1 L400-410        (O10)
+ *   Sobol-in-tetrahedron sampler (NEXT-1)    App. A.2 L744-751                (S1..S9)
  *
  * Everything that decides an integer (ownership, fold, the h case split, band
  * membership) is decided exactly in integer arithmetic (int64 / __int128) or
@@ -84,6 +85,9 @@ typedef struct {
     int32_t *bidx[2][64];
     /* coverage reference (row a9): owned-sample count per side of the base mesh; -1 = unknown */
     int64_t expect[2];
+    /* sample set: 0 = exactly-once voxel centres (O3), 1 = Sobol points per tet (NEXT-1) */
+    int sampler;
+    double rate; /* Sobol samples per voxel of tet volume */
 } orc_problem;
 
 /* ------------------------------------------------------------------ */
@@ -479,6 +483,198 @@ static void tet_side_samples(orc_problem *P, int s, const int64_t Q[2][4][3], do
             }
 }
 
+/* ------------------------------------------------------------------ */
+/* NEXT-1: Sobol-in-tetrahedron sampler (App. A.2).            */
+/* "We uniformly sample N points in each tetrahedron using its          */
+/* barycentric coordinate system, with N being determined by the volume */
+/* of the tetrahedron.  For each point, we sample 4 random real numbers */
+/* r_i in [0;1] and take -log(r_i) ... normalize the coordinates by     */
+/* their sum ... the Sobol sequence ... seeding the Sobol sequence for  */
+/* each tetrahedron with a seed derived from its coordinates."          */
+/* Readings S1..S9: the point generator (S1-S5) is the   */
+/* counter-based generator both implementations write out identically; */
+/* everything after it is the method's arithmetic, in fp64 here.        */
+/* ------------------------------------------------------------------ */
+static uint32_t SOBOL_V[4][32];
+static int sobol_ready = 0;
+
+/* S1: direction numbers of the first 4 Sobol dimensions (Joe & Kuo primitive
+ * polynomials; dimension 0 is van der Corput).  (s, a, m_1..m_s) per dimension;
+ * m_i = 2^s m_{i-s} ^ m_{i-s} ^ XOR_{k=1}^{s-1} 2^k a_k m_{i-k}, v_i = m_i 2^(31-i). */
+static void sobol_init(void) {
+    static const int S[4] = {0, 1, 2, 3}, A[4] = {0, 0, 1, 1};
+    static const uint32_t M0[4][3] = {{0, 0, 0}, {1, 0, 0}, {1, 3, 0}, {1, 3, 1}};
+    if (sobol_ready) return;
+    for (int j = 0; j < 4; j++) {
+        uint64_t m[32];
+        int s = S[j];
+        for (int i = 0; i < 32; i++) {
+            if (s == 0) { m[i] = 1; continue; }
+            if (i < s) { m[i] = M0[j][i]; continue; }
+            uint64_t v = m[i - s] ^ (m[i - s] << s);
+            for (int k = 1; k < s; k++)
+                if ((A[j] >> (s - 1 - k)) & 1) v ^= m[i - k] << k;
+            m[i] = v;
+        }
+        for (int i = 0; i < 32; i++) SOBOL_V[j][i] = (uint32_t)(m[i] << (31 - i));
+    }
+    sobol_ready = 1;
+}
+
+/* S2: point k of the sequence in Gray-code order (the order of scipy.stats.qmc.Sobol) */
+static void sobol_point(uint64_t k, uint32_t x[4]) {
+    uint64_t g = k ^ (k >> 1);
+    for (int j = 0; j < 4; j++) {
+        uint32_t v = 0;
+        for (int b = 0; b < 32; b++)
+            if ((g >> b) & 1) v ^= SOBOL_V[j][b];
+        x[j] = v;
+    }
+}
+
+/* S3: seed = FNV-1a (64 bit) over the 12 little-endian int32 Q.10 coordinates of
+ * the tet's vertices on the sampled side, in vertex order x, y, z.  S4: the
+ * "seeding" is a digital shift: x_j ^ mask_j, mask_j = high 32 bits of
+ * splitmix64(seed + j). */
+static uint64_t splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+static uint64_t fnv1a64(const unsigned char *b, size_t n) {
+    uint64_t h = 14695981039346656037ULL;
+    for (size_t i = 0; i < n; i++) {
+        h ^= b[i];
+        h *= 1099511628211ULL;
+    }
+    return h;
+}
+static uint64_t tet_seed(const int64_t Q[4][3]) {
+    unsigned char bytes[48];
+    for (int k = 0; k < 4; k++)
+        for (int a = 0; a < 3; a++) {
+            uint32_t c = (uint32_t)(int32_t)Q[k][a];
+            for (int b = 0; b < 4; b++) bytes[4 * (3 * k + a) + b] = (unsigned char)((c >> (8 * b)) & 0xFFu);
+        }
+    return fnv1a64(bytes, 48);
+}
+static void tet_masks(const int64_t Q[4][3], uint32_t mask[4]) {
+    uint64_t seed = tet_seed(Q);
+    for (int j = 0; j < 4; j++) mask[j] = (uint32_t)(splitmix64(seed + (uint64_t)j) >> 32);
+}
+
+/* S5: r = (x + 1/2) 2^-32 in (0, 1) and -log r with a fixed sequence of IEEE
+ * double operations (frexp, one division, a degree-23 odd series), so that
+ * both implementations get the same bits:  r = m 2^e, m in [sqrt(1/2), sqrt(2)),
+ * log m = 2 atanh t, t = (m - 1)/(m + 1), |t| <= 0.1716.  */
+static double neg_log(uint32_t x) {
+    double r = ((double)x + 0.5) * 2.3283064365386963e-10; /* 2^-32, exact */
+    int e;
+    double m = frexp(r, &e); /* r = m 2^e, m in [1/2, 1) */
+    if (m < 0.70710678118654752440) { m = m * 2.0; e = e - 1; }
+    double t = (m - 1.0) / (m + 1.0);
+    double t2 = t * t;
+    double p = 1.0 / 23.0;
+    p = p * t2 + 1.0 / 21.0;
+    p = p * t2 + 1.0 / 19.0;
+    p = p * t2 + 1.0 / 17.0;
+    p = p * t2 + 1.0 / 15.0;
+    p = p * t2 + 1.0 / 13.0;
+    p = p * t2 + 1.0 / 11.0;
+    p = p * t2 + 1.0 / 9.0;
+    p = p * t2 + 1.0 / 7.0;
+    p = p * t2 + 1.0 / 5.0;
+    p = p * t2 + 1.0 / 3.0;
+    p = p * t2 + 1.0;
+    double lm = 2.0 * t * p;
+    /* log 2 = LN2_HI + LN2_LO, LN2_HI with 32 trailing zero bits (e LN2_HI exact) */
+    double lr = (double)e * 6.93147180369123816490e-01 + ((double)e * 1.90821492927058770002e-10 + lm);
+    return -lr;
+}
+
+/* S6: number of samples of a tet side: N = floor(rate |Delta| / (6 1024^3) + 1/2),
+ * |Delta| / (6 1024^3) being the volume in voxels (rate 1.0 ~ one sample per voxel) */
+static int64_t sobol_count(const orc_problem *P, const int64_t Q[4][3]) {
+    i128 d = det4(Q);
+    if (d < 0) d = -d;
+    double vol = (double)(int64_t)d;
+    return (int64_t)floor(vol * (P->rate / 6442450944.0) + 0.5);
+}
+
+/* S7: barycentrics lambda_j = e_j / (((e_0 + e_1) + e_2) + e_3), and the point on
+ * a side:  X_0 + ((lambda_1 (X_1 - X_0) + lambda_2 (X_2 - X_0)) + lambda_3 (X_3 - X_0)),
+ * X = Q / 1024 (exact); the same lambda on both sides (T maps barycentrics). */
+static void sobol_lambda(const uint32_t x[4], const uint32_t mask[4], double lam[4]) {
+    double e[4];
+    for (int j = 0; j < 4; j++) e[j] = neg_log(x[j] ^ mask[j]);
+    double s = ((e[0] + e[1]) + e[2]) + e[3];
+    for (int j = 0; j < 4; j++) lam[j] = e[j] / s;
+}
+static void bary_point(const int64_t Q[4][3], const double lam[4], double p[3]) {
+    for (int a = 0; a < 3; a++) {
+        double x0 = (double)Q[0][a] / 1024.0;
+        double d1 = (double)(Q[1][a] - Q[0][a]) / 1024.0;
+        double d2 = (double)(Q[2][a] - Q[0][a]) / 1024.0;
+        double d3 = (double)(Q[3][a] - Q[0][a]) / 1024.0;
+        p[a] = x0 + ((lam[1] * d1 + lam[2] * d2) + lam[3] * d3);
+    }
+}
+
+/* S8: "value > 0" of the clamped trilinear interpolant at x, decided exactly:
+ * some contributing corner (O5/O6 footprint rules on each axis) has I > 0 */
+static int positive_at(const orc_problem *P, const float *vol, const double x[3]) {
+    int64_t s[3][2];
+    int c[3];
+    for (int a = 0; a < 3; a++) {
+        int n = P->n[a];
+        if (x[a] <= 0.0) { s[a][0] = 0; c[a] = 1; continue; }
+        if (x[a] >= (double)(n - 1)) { s[a][0] = n - 1; c[a] = 1; continue; }
+        double fl = floor(x[a]);
+        s[a][0] = (int64_t)fl;
+        if (x[a] == fl) { c[a] = 1; continue; }
+        s[a][1] = (int64_t)fl + 1;
+        c[a] = 2;
+    }
+    for (int k = 0; k < c[2]; k++)
+        for (int j = 0; j < c[1]; j++)
+            for (int i = 0; i < c[0]; i++)
+                if (vol[vidx(P, s[0][i], s[1][j], s[2][k])] > 0.0f) return 1;
+    return 0;
+}
+
+/* S9: one tet side in Sobol mode.  a = I_s(p) and b = I_s'(T p) are both trilinear
+ * (the paper's "interpolating intensity values between voxel centers", L744);
+ * h takes its case from the exact positivity of both; the guidance term uses
+ * d = D_i^s(p) (interpolated) for every pair with d < r. */
+static void tet_side_sobol(orc_problem *P, int s, const int64_t Q[2][4][3], double *h_sum,
+                           double *g_sum, int64_t *n_samples) {
+    int so = 1 - s;
+    int64_t N = sobol_count(P, Q[s]);
+    *n_samples += N;
+    uint32_t mask[4];
+    tet_masks(Q[s], mask);
+    for (int64_t k = 0; k < N; k++) {
+        uint32_t x[4];
+        double lam[4], p[3], tp[3];
+        sobol_point((uint64_t)k, x);
+        sobol_lambda(x, mask, lam);
+        bary_point(Q[s], lam, p);
+        bary_point(Q[so], lam, tp);
+        double a = trilinear(P, P->I[s], p);
+        double b = trilinear(P, P->I[so], tp);
+        int fa = positive_at(P, P->I[s], p), fb = positive_at(P, P->I[so], tp);
+        double h = (fa && fb) ? (a - b) * (a - b) : ((!fa && !fb) ? 0.0 : 1.0);
+        *h_sum += h;
+        for (int i = 0; i < P->K; i++) {
+            double d = trilinear_map(P, s, i, p);
+            if (!(d < P->r)) continue;
+            double dd = d - trilinear_map(P, so, i, tp);
+            *g_sum += P->w[s][i] * ((P->r - d) / P->r) * dd * dd;
+        }
+    }
+}
+
 /* per-tet contributions (both sides) for one solution */
 static void tet_contrib(orc_problem *P, const float *off, int t, double rec[PT_N]) {
     memset(rec, 0, sizeof(double) * PT_N);
@@ -495,7 +691,8 @@ static void tet_contrib(orc_problem *P, const float *off, int t, double rec[PT_N
             rec[PT_SEV] += vol * P->sp[0] * P->sp[1] * P->sp[2];
         }
         int64_t n = 0;
-        tet_side_samples(P, s, Q, &rec[PT_H], &rec[PT_G], &n, NULL, t);
+        if (P->sampler == 1) tet_side_sobol(P, s, Q, &rec[PT_H], &rec[PT_G], &n);
+        else tet_side_samples(P, s, Q, &rec[PT_H], &rec[PT_G], &n, NULL, t);
         rec[s == 0 ? PT_NS : PT_NT] = (double)n;
     }
     rec[PT_M] = magnitude(P, t, Q);
@@ -574,6 +771,9 @@ orc_problem *orc_create(int nx, int ny, int nz, const double *spacing, const flo
     free(fill);
     /* bucket grid for the nearest-point search */
     P->expect[0] = P->expect[1] = -1;
+    P->sampler = 0;
+    P->rate = 1.0;
+    sobol_init();
     P->bsz = 4;
     for (int a = 0; a < 3; a++) P->bn[a] = (P->n[a] + 2) / P->bsz + 1;
     int nb = P->bn[0] * P->bn[1] * P->bn[2];
@@ -657,7 +857,7 @@ int orc_eval(orc_problem *P, const float *offsets_one, double obj[3], orc_acc *a
     memset(acc, 0, sizeof(*acc));
     double rec[PT_N];
     int64_t ns = 0, nt = 0;
-    base_counts(P);
+    if (P->sampler == 0) base_counts(P);
     for (int t = 0; t < P->T; t++) {
         tet_contrib(P, offsets_one, t, rec);
         ns += (int64_t)rec[PT_NS];
@@ -670,7 +870,8 @@ int orc_eval(orc_problem *P, const float *offsets_one, double obj[3], orc_acc *a
         acc->folds += (int32_t)rec[PT_FOLD_S] + (int32_t)rec[PT_FOLD_T];
     }
     if (any_out_of_window(P, offsets_one)) acc->flags |= ORC_F_DOMAIN;
-    else if (ns != P->expect[0] || nt != P->expect[1]) acc->flags |= ORC_F_COVERAGE; /* a9 */
+    else if (P->sampler == 0 && (ns != P->expect[0] || nt != P->expect[1]))
+        acc->flags |= ORC_F_COVERAGE; /* a9 */
     if (acc->n_samples == 0) acc->flags |= ORC_F_EMPTY;
     acc_objectives(P, acc, obj);
     return 0;
@@ -806,6 +1007,49 @@ int orc_sample_debug(orc_problem *P, const float *offsets_one, int t, int s, con
 
 /* exported helpers for the pin tests (pure functions of their arguments) */
 double orc_h(double a, double b, int fg) { return h_of(a, b, fg); }
+
+/* NEXT-1 switches and pin hooks */
+int orc_set_sampler(orc_problem *P, int mode, double rate) {
+    if ((mode != 0 && mode != 1) || !(rate > 0.0)) return -1;
+    P->sampler = mode;
+    P->rate = rate;
+    return 0;
+}
+void orc_sobol_point(uint64_t k, uint32_t *x4) {
+    sobol_init();
+    sobol_point(k, x4);
+}
+double orc_neg_log(uint32_t x) { return neg_log(x); }
+uint64_t orc_fnv1a64(const unsigned char *b, int64_t n) { return fnv1a64(b, (size_t)n); }
+uint64_t orc_splitmix64(uint64_t z) { return splitmix64(z); }
+uint64_t orc_tet_seed(const int64_t *Q12, uint32_t *mask4) {
+    int64_t Q[4][3];
+    for (int k = 0; k < 4; k++)
+        for (int a = 0; a < 3; a++) Q[k][a] = Q12[3 * k + a];
+    tet_masks(Q, mask4);
+    return tet_seed(Q);
+}
+/* sample k of tet t, side s: out = lambda[4], p[3], Tp[3], a, b, fa, fb, h, N */
+int orc_sobol_debug(orc_problem *P, const float *offsets_one, int t, int s, int64_t k, double *out) {
+    int64_t Q[2][4][3];
+    if (t < 0 || t >= P->T || s < 0 || s > 1) return -1;
+    if (!tet_coords(P, offsets_one, t, Q)) return -3;
+    uint32_t x[4], mask[4];
+    double lam[4], p[3], tp[3];
+    tet_masks(Q[s], mask);
+    sobol_point((uint64_t)k, x);
+    sobol_lambda(x, mask, lam);
+    bary_point(Q[s], lam, p);
+    bary_point(Q[1 - s], lam, tp);
+    double a = trilinear(P, P->I[s], p), b = trilinear(P, P->I[1 - s], tp);
+    int fa = positive_at(P, P->I[s], p), fb = positive_at(P, P->I[1 - s], tp);
+    for (int j = 0; j < 4; j++) out[j] = lam[j];
+    for (int a2 = 0; a2 < 3; a2++) { out[4 + a2] = p[a2]; out[7 + a2] = tp[a2]; }
+    out[10] = a; out[11] = b; out[12] = fa; out[13] = fb;
+    out[14] = (fa && fb) ? (a - b) * (a - b) : ((!fa && !fb) ? 0.0 : 1.0);
+    out[15] = (double)sobol_count(P, Q[s]);
+    return 0;
+}
 double orc_trilinear_raw(int nx, int ny, int nz, const float *vol, double x, double y, double z) {
     orc_problem tmp;
     memset(&tmp, 0, sizeof(tmp));

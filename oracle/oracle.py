@@ -75,6 +75,17 @@ def lib():
         L.orc_ref_sign.argtypes = [vp, ctypes.c_int]
         L.orc_r.restype = ctypes.c_double
         L.orc_r.argtypes = [vp]
+        L.orc_set_sampler.argtypes = [vp, ctypes.c_int, ctypes.c_double]
+        L.orc_sobol_point.argtypes = [ctypes.c_uint64, vp]
+        L.orc_neg_log.restype = ctypes.c_double
+        L.orc_neg_log.argtypes = [ctypes.c_uint32]
+        L.orc_fnv1a64.restype = ctypes.c_uint64
+        L.orc_fnv1a64.argtypes = [ctypes.c_char_p, ctypes.c_int64]
+        L.orc_splitmix64.restype = ctypes.c_uint64
+        L.orc_splitmix64.argtypes = [ctypes.c_uint64]
+        L.orc_tet_seed.restype = ctypes.c_uint64
+        L.orc_tet_seed.argtypes = [vp, vp]
+        L.orc_sobol_debug.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp]
         _lib = L
     return _lib
 
@@ -195,6 +206,20 @@ class Oracle:
     def ref_sign(self, t):
         return lib().orc_ref_sign(self.h, int(t))
 
+    def set_sampler(self, mode, rate=1.0):
+        """0: exactly-once voxel centres (O3); 1: Sobol points per tet (NEXT-1, S1-S9)."""
+        if lib().orc_set_sampler(self.h, int(mode), float(rate)) != 0:
+            raise ValueError("bad sampler")
+
+    def sobol_debug(self, offsets_one, tet, side, k):
+        o = self._off(offsets_one)
+        out = np.zeros(16)
+        rc = lib().orc_sobol_debug(self.h, _p(o), int(tet), int(side), int(k), _p(out))
+        if rc != 0:
+            raise ValueError(rc)
+        return dict(lam=out[0:4].copy(), p=out[4:7].copy(), tp=out[7:10].copy(), a=out[10],
+                    b=out[11], fa=bool(out[12]), fb=bool(out[13]), h=out[14], N=int(out[15]))
+
 
 def h(a, b, fg):
     return lib().orc_h(float(a), float(b), int(fg))
@@ -216,3 +241,30 @@ def signed_det(Q):
 
 def canon(b, o):
     return lib().orc_canon(float(b), float(o))
+
+
+def sobol_points(n):
+    """The first n points (uint32 x 4) of the unscrambled sequence, Gray-code order."""
+    out = np.zeros((n, 4), dtype=np.uint32)
+    for k in range(n):
+        lib().orc_sobol_point(k, _p(out[k]))
+    return out
+
+
+def neg_log(x):
+    return lib().orc_neg_log(int(x))
+
+
+def fnv1a64(b: bytes):
+    return lib().orc_fnv1a64(b, len(b))
+
+
+def splitmix64(z):
+    return lib().orc_splitmix64(int(z))
+
+
+def tet_seed(Q12):
+    Q = np.ascontiguousarray(np.asarray(Q12, dtype=np.int64).reshape(12))
+    m = np.zeros(4, dtype=np.uint32)
+    seed = lib().orc_tet_seed(_p(Q), _p(m))
+    return seed, m
