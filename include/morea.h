@@ -54,6 +54,10 @@ extern "C" {
 #define MOREA_SPOKE_FACE_CENTROID 0 /* spoke = vertex -> centroid of the opposite face (O9, default) */
 #define MOREA_SPOKE_TET_CENTROID 1  /* spoke = tet centroid -> vertex (3/4 of the above) */
 
+/* ---- morea_set_sampler modes ---- */
+#define MOREA_SAMPLER_VOXEL 0 /* exactly-once voxel centres (north_star, O3; default) */
+#define MOREA_SAMPLER_SOBOL 1 /* Sobol points per tet (App. A.2; NEXT-1) */
+
 /* Q.10 window (reading O1): canonical coordinates Q = round-half-even(1024*B +
  * 1024*O) must satisfy -256*1024 <= Q < 768*1024 on every axis. */
 #define MOREA_WINDOW_LO_VOX (-256)
@@ -163,6 +167,26 @@ int morea_eval_partial(morea_ctx *ctx, int pop, const float *base_offsets,
                        const morea_acc *base_acc, int n_groups, const int32_t *grp_off,
                        const int32_t *changed_pts, const float *new_vals, const double *tet_cache,
                        double *obj, morea_acc *acc, double *dep_cache_out);
+
+/* Select the sample set of subsequent evaluations.
+ *  MOREA_SAMPLER_VOXEL: the voxel centres each tet owns, exactly once (O3).
+ *  MOREA_SAMPLER_SOBOL: PAPER.md App. A.2 "We uniformly sample N points
+ *    in each tetrahedron using its barycentric coordinate system, with N being
+ *    determined by the volume of the tetrahedron ... 4 random real numbers r_i
+ *    ... -log(r_i) ... normalize the coordinates by their sum ... the Sobol
+ *    sequence ... seeding the Sobol sequence for each tetrahedron with a seed
+ *    derived from its coordinates."  Per (solution, tet, side):
+ *    N = floor(rate |Delta| / (6 1024^3) + 1/2) (rate = samples per voxel of tet
+ *    volume); point k = Gray-code Sobol point k (4 dims, Joe-Kuo directions)
+ *    XOR-shifted by masks from FNV-1a of the side's Q.10 vertex coordinates;
+ *    a = trilinear I_side(p) and b = trilinear I_other(T p), both interpolated;
+ *    the guidance term uses d = trilinear D_i^side(p).  Readings S1..S9 in
+ *    DESIGN.md §3.  f_int / f_guid normalise by the total sample count.  The
+ *    coverage flag is not computed in this mode.
+ * rate must be > 0 and finite.  Takes effect for the following morea_eval_*
+ * calls (morea_owner_map always uses the voxel-centre rasterizer).
+ * Errors: EINVAL (bad mode / rate), ESTATE (before morea_create finished). */
+int morea_set_sampler(morea_ctx *ctx, int mode, double rate);
 
 /* The dependent tets of the plan of the last morea_eval_partial call: writes
  * up to `cap` tet ids (group order, ascending within a group) into `tets` (host)

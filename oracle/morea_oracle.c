@@ -643,6 +643,27 @@ static int positive_at(const orc_problem *P, const float *vol, const double x[3]
     return 0;
 }
 
+/* some corner of the clamped trilinear footprint of x (O5) has D_i^s < r */
+static int footprint_touches_band(orc_problem *P, int s, int i, const double x[3]) {
+    int64_t i0[3];
+    for (int a = 0; a < 3; a++) {
+        double xc = x[a];
+        if (xc < 0.0) xc = 0.0;
+        if (xc > (double)(P->n[a] - 1)) xc = (double)(P->n[a] - 1);
+        int64_t fl = (int64_t)floor(xc);
+        if (fl > P->n[a] - 2) fl = P->n[a] - 2;
+        i0[a] = fl;
+    }
+    for (int dz = 0; dz < 2; dz++)
+        for (int dy = 0; dy < 2; dy++)
+            for (int dx = 0; dx < 2; dx++) {
+                int64_t q[3] = {i0[0] + dx, i0[1] + dy, i0[2] + dz};
+                float d;
+                if (band(P, s, i, q, &d)) return 1;
+            }
+    return 0;
+}
+
 /* S9: one tet side in Sobol mode.  a = I_s(p) and b = I_s'(T p) are both trilinear
  * (the paper's "interpolating intensity values between voxel centers", L744);
  * h takes its case from the exact positivity of both; the guidance term uses
@@ -667,6 +688,10 @@ static void tet_side_sobol(orc_problem *P, int s, const int64_t Q[2][4][3], doub
         double h = (fa && fb) ? (a - b) * (a - b) : ((!fa && !fb) ? 0.0 : 1.0);
         *h_sum += h;
         for (int i = 0; i < P->K; i++) {
+            /* d is a convex combination of the footprint's corner distances: when
+             * none of them is < r, d >= r (up to one rounding) and the term is 0,
+             * so the exact map values are only needed near the band */
+            if (!footprint_touches_band(P, s, i, p)) continue;
             double d = trilinear_map(P, s, i, p);
             if (!(d < P->r)) continue;
             double dd = d - trilinear_map(P, so, i, tp);

@@ -71,6 +71,11 @@ struct morea_ctx {
   double r = 0;
   double w[2][kMaxPairs] = {};
   DevBuf I[2], band[2], dmap[2], wts, own;
+  // Sobol sampler (NEXT-1): mode, rate, dilated band masks (2 V bytes), direction numbers
+  int sampler = MOREA_SAMPLER_VOXEL;
+  double rate = 1.0;
+  DevBuf dil, sobolv;
+  int blocks_per_sm_sobol = 1, blocks_per_sm_sobol_tex = 1;
   // texture-gather copies (tall 2D arrays) of I_s, I_t and the maps
   bool use_tex = false;
   cudaArray_t arrI = nullptr, arrM = nullptr;
@@ -221,6 +226,7 @@ Volumes volumes_of(const morea_ctx* c) {
     v.I[s] = c->I[s].as<float>();
     v.band[s] = c->K > 0 ? c->band[s].as<unsigned char>() : nullptr;
     v.dmap[s] = c->K > 0 ? c->dmap[s].as<float>() : nullptr;
+    v.dil[s] = (c->K > 0 && c->dil.p) ? c->dil.as<unsigned char>() + (size_t)s * c->V : nullptr;
   }
   v.K = c->K;
   v.r = c->r;
@@ -280,7 +286,15 @@ cudaError_t eval_scratch(morea_ctx* ctx, EvalArgs& a) {
   return cudaSuccess;
 }
 
-// k_setup -> k_raster (the dominant kernel; bracketed by events when profiling).
+void set_sampler_args(const morea_ctx* ctx, EvalArgs& a) {
+  a.sampler = ctx->sampler;
+  a.rate = ctx->rate;
+  a.sobol_v = ctx->sobolv.as<unsigned>();
+  const char* fe = std::getenv("MOREA_SOBOL_FORCE_EXACT");
+  a.sobol_force_exact = (fe && fe[0] && fe[0] != '0') ? 1 : 0;
+}
+
+// k_setup -> k_raster / k_sobol (the dominant kernel; bracketed by events when profiling).
 cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
   cudaError_t e = eval_scratch(ctx, a);
   if (e != cudaSuccess) return e;
@@ -297,7 +311,14 @@ cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
     cudaEventCreate(&e1);
     cudaEventRecord(e0, ctx->stream);
   }
-  e = launch_raster(a, raster_grid(ctx, n_items), ctx->stream);
+  if (a.sampler == MOREA_SAMPLER_SOBOL) {
+    const long long g = (long long)ctx->n_sm *
+                        (ctx->use_tex ? ctx->blocks_per_sm_sobol_tex : ctx->blocks_per_sm_sobol);
+    const long long need = (n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    e = launch_sobol(a, (int)std::max<long long>(1, std::min(g, need)), ctx->stream);
+  } else {
+    e = launch_raster(a, raster_grid(ctx, n_items), ctx->stream);
+  }
   ctx->kernels++;
   if (ctx->prof) {
     cudaEventRecord(e1, ctx->stream);
@@ -388,6 +409,45 @@ int build_plan(morea_ctx* ctx, int G, const int32_t* grp_off_in, const int32_t* 
   P.dep_off = dep_off;
   P.valid = true;
   return MOREA_OK;
+}
+
+// S1: direction numbers v_j[b] of the first four Sobol dimensions,
+// row-major [4][32].  Dimension 0 is van der Corput (v = 2^(31-b)); dimensions
+// 1..3 come from the primitive polynomials x + 1, x^2 + x + 1, x^3 + x + 1
+// (degree s, inner coefficient bits a) with initial m = (1), (1, 3), (1, 3, 1)
+// (Joe & Kuo), extended by the Bratley-Fox recurrence on the v's directly:
+// v_b = v_{b-s} ^ (v_{b-s} >> s) ^ XOR_{k=1}^{s-1} a_k v_{b-k}.
+std::vector<unsigned> sobol_directions() {
+  struct Dim { int s; unsigned a; unsigned m[3]; };
+  const Dim dims[3] = {{1, 0u, {1, 0, 0}}, {2, 1u, {1, 3, 0}}, {3, 1u, {1, 3, 1}}};
+  std::vector<unsigned> v(4 * 32);
+  for (int b = 0; b < 32; b++) v[b] = 1u << (31 - b);
+  for (int d = 0; d < 3; d++) {
+    unsigned* w = &v[32 * (d + 1)];
+    const int s = dims[d].s;
+    for (int b = 0; b < s; b++) w[b] = dims[d].m[b] << (31 - b);
+    for (int b = s; b < 32; b++) {
+      unsigned x = w[b - s] ^ (w[b - s] >> s);
+      for (int k = 1; k < s; k++)
+        if ((dims[d].a >> (s - 1 - k)) & 1u) x ^= w[b - k];
+      w[b] = x;
+    }
+  }
+  return v;
+}
+
+// dilated band masks for the Sobol sampler (built on demand)
+cudaError_t ensure_dil(morea_ctx* ctx) {
+  if (ctx->sampler != MOREA_SAMPLER_SOBOL || !ctx->have_images || ctx->K == 0 || ctx->dil.p)
+    return cudaSuccess;
+  cudaError_t e = ctx->dil.ensure(2 * (size_t)ctx->V);
+  if (e != cudaSuccess) return e;
+  for (int s = 0; s < 2; s++) {
+    e = launch_dilate_band(ctx->band[s].as<unsigned char>(), ctx->nx, ctx->ny, ctx->nz,
+                           ctx->dil.as<unsigned char>() + (size_t)s * ctx->V, ctx->stream);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaStreamSynchronize(ctx->stream);
 }
 
 void release_textures(morea_ctx* ctx) {
@@ -482,6 +542,17 @@ int morea_create(int cuda_device, void* cuda_stream, morea_ctx** out) {
   cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, cuda_device);
   ctx->blocks_per_sm = raster_blocks_per_sm(false);
   ctx->blocks_per_sm_tex = raster_blocks_per_sm(true);
+  ctx->blocks_per_sm_sobol = sobol_blocks_per_sm(false);
+  ctx->blocks_per_sm_sobol_tex = sobol_blocks_per_sm(true);
+  {
+    const std::vector<unsigned> v = sobol_directions();
+    if (ctx->sobolv.ensure(v.size() * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemcpy(ctx->sobolv.p, v.data(), v.size() * sizeof(unsigned), cudaMemcpyHostToDevice) !=
+            cudaSuccess) {
+      delete ctx;
+      return MOREA_ECUDA;
+    }
+  }
   if (ctx->stats.ensure(4 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemset(ctx->stats.p, 0, 4 * sizeof(unsigned long long)) != cudaSuccess) {
     delete ctx;
@@ -501,7 +572,7 @@ void morea_destroy(morea_ctx* ctx) {
     cudaEventDestroy(p.second);
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
-                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
+                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->dil, &ctx->sobolv, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
                     &ctx->full_sched, &ctx->full_group_off, &ctx->geom, &ctx->scal, &ctx->hgn,
                     &ctx->counter, &ctx->stats, &ctx->st_off, &ctx->st_nv, &ctx->st_cache_in,
                     &ctx->st_base_acc, &ctx->st_obj, &ctx->st_acc, &ctx->st_cache_out,
@@ -590,7 +661,9 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
                           ctx->own.as<uint2>() + (size_t)s * V, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(build_textures(ctx));
+  ctx->dil.release();
   ctx->have_images = true;
+  CK(ensure_dil(ctx));
   return MOREA_OK;
 }
 
@@ -756,8 +829,9 @@ int morea_eval_full(morea_ctx* ctx, int pop, const float* offsets, double* obj, 
   a.partial = 0;
   a.n_setup_versions = 1;
   a.n_raster_versions = 1;
-  a.expect[0] = ctx->expect[0];
-  a.expect[1] = ctx->expect[1];
+  a.expect[0] = ctx->sampler == MOREA_SAMPLER_VOXEL ? ctx->expect[0] : -1;
+  a.expect[1] = ctx->sampler == MOREA_SAMPLER_VOXEL ? ctx->expect[1] : -1;
+  set_sampler_args(ctx, a);
   CK(run_eval(ctx, a));
   CK(launch_reduce(a, 1, ctx->full_group_off.as<int>(), nullptr, nullptr, (double*)ov[2].dev,
                    nullptr, nullptr, (double*)ov[0].dev, ov[1].dev, ctx->stream));
@@ -808,11 +882,24 @@ int morea_eval_partial(morea_ctx* ctx, int pop, const float* base_offsets,
   a.n_setup_versions = 2;
   a.n_raster_versions = cin ? 1 : 2;
   a.expect[0] = a.expect[1] = -1;
+  set_sampler_args(ctx, a);
   CK(run_eval(ctx, a));
   CK(launch_reduce(a, G, P.group_off.as<int>(), bacc, cin, (double*)ov[2].dev, P.changed.as<int>(),
                    P.grp_off.as<int>(), (double*)ov[0].dev, ov[1].dev, ctx->stream));
   ctx->kernels++;
   CK(finish_outputs(ctx, ov, 3));
+  return MOREA_OK;
+}
+
+int morea_set_sampler(morea_ctx* ctx, int mode, double rate) {
+  if (!ctx) return MOREA_EINVAL;
+  if (mode != MOREA_SAMPLER_VOXEL && mode != MOREA_SAMPLER_SOBOL)
+    return fail(ctx, MOREA_EINVAL, "unknown sampler mode %d", mode);
+  if (!(rate > 0.0) || !std::isfinite(rate)) return fail(ctx, MOREA_EINVAL, "rate must be > 0 and finite");
+  CK(cudaSetDevice(ctx->device));
+  ctx->sampler = mode;
+  ctx->rate = rate;
+  CK(ensure_dil(ctx));
   return MOREA_OK;
 }
 

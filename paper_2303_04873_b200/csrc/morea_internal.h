@@ -39,6 +39,21 @@ struct __align__(16) SideRec {
 };
 static_assert(sizeof(SideRec) == 384, "SideRec layout");
 
+// NEXT-1 (Sobol sampler, DESIGN.md §3 S1-S9): what k_sobol needs of one (version,
+// entry, solution, side) item.  Written by k_setup into the item's SideRec slot.
+struct __align__(16) SobolRec {
+  int Q[4][3];              // sampled side, Q.10 (exact; the fp64 fallback recomputes from these)
+  int Qo[4][3];             // other side
+  float x0[3], D[3][3];     // sampled side: X_0 and X_k - X_0 (k = 1..3), voxel units, fp32-exact
+  float x0o[3], Do[3][3];   // other side
+  unsigned mask[4];         // digital-shift masks (S3/S4)
+  long long N;              // samples of this side (S6)
+  float epsA, epsB;         // fast-path position error bound eps = epsA / s + epsB, s = sum -lg2 u
+  int flags;                // bit 0: N > 0; bit 1: every vertex of both sides inside [0, n-1]
+  int pad;
+};
+static_assert(sizeof(SobolRec) <= sizeof(SideRec), "SobolRec must fit a SideRec slot");
+
 // Per-tet scalar terms of one (version, entry, solution).
 struct Scal {
   double m, sev;
@@ -80,6 +95,9 @@ struct Volumes {
   unsigned long long texM;
   float fnx;  // nx as float (volume offset in the textures)
   int use_tex;
+  // Sobol sampler (NEXT-1): per side and voxel v, OR of the band bits of v + {0,1}^3
+  // (clamped): the pairs whose interpolated distance can be < r in v's cell
+  const unsigned char* dil[2];
 };
 
 struct MeshDev {
@@ -112,6 +130,10 @@ struct EvalArgs {
   Scal* scal;                // [version][entry][sol]
   HGN* hgn;                  // [version][entry][sol]
   long long expect[2];       // per-side sample count of the base mesh (coverage check), -1: off
+  int sampler;               // 0: exactly-once voxel centres (k_raster), 1: Sobol points (k_sobol)
+  double rate;               // Sobol samples per voxel of tet volume
+  const unsigned* sobol_v;   // [4][32] Sobol direction numbers (device)
+  int sobol_force_exact;     // test hook (env MOREA_SOBOL_FORCE_EXACT): every sample takes the fp64 path
   unsigned long long* counter;  // work queue head (zeroed before launch)
   unsigned long long* stats;    // [samples, band entries, items]
 };
@@ -127,6 +149,10 @@ cudaError_t launch_own_records(const float* I, const unsigned char* band, long l
 cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s);
 cudaError_t launch_raster(const EvalArgs& a, int grid, cudaStream_t s);
 int raster_blocks_per_sm(bool tex);
+cudaError_t launch_sobol(const EvalArgs& a, int grid, cudaStream_t s);
+int sobol_blocks_per_sm(bool tex);
+cudaError_t launch_dilate_band(const unsigned char* band, int nx, int ny, int nz, unsigned char* dil,
+                               cudaStream_t s);
 cudaError_t launch_reduce(const EvalArgs& a, int G, const int* group_off, const void* base_acc,
                           const double* cache_in, double* cache_out, const int* changed,
                           const int* grp_off, double* obj, void* acc, cudaStream_t s);

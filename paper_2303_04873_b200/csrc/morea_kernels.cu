@@ -35,6 +35,10 @@
 #define MOREA_ABLATE 0  // dev experiments only (4: no guidance evaluation, 5: no band loads)
 #endif
 
+#ifndef MOREA_SOBOL_MINB
+#define MOREA_SOBOL_MINB 14  // k_sobol: resident 64-thread blocks per SM
+#endif
+
 #ifndef MOREA_RASTER_MINB
 #define MOREA_RASTER_MINB 14  // resident 64-thread blocks per SM: 28 warps at 72 registers
 #endif
@@ -249,6 +253,8 @@ __device__ double magnitude(const int Q[2][4][3], double c, const double sp2[3],
   return c * m;
 }
 
+#include "morea_sobol_setup.cuh"
+
 // ---------------------------------------------------------------------------
 // k_setup: one thread per (version, canonical entry, solution).
 // ---------------------------------------------------------------------------
@@ -273,8 +279,13 @@ __global__ void __launch_bounds__(128) k_setup(const EvalArgs A) {
     sc.flags = 1;  // domain: the tet contributes nothing
     A.scal[i] = sc;
     if (raster) {
-      A.geom[2 * i].flags = 0;
-      A.geom[2 * i + 1].flags = 0;
+      if (A.sampler == 1) {
+        reinterpret_cast<SobolRec*>(&A.geom[2 * i])->flags = 0;
+        reinterpret_cast<SobolRec*>(&A.geom[2 * i + 1])->flags = 0;
+      } else {
+        A.geom[2 * i].flags = 0;
+        A.geom[2 * i + 1].flags = 0;
+      }
     }
     return;
   }
@@ -297,7 +308,8 @@ __global__ void __launch_bounds__(128) k_setup(const EvalArgs A) {
 #pragma unroll 1
   for (int s = 0; s < 2; s++) {
     SideRec G;
-    build_side(Q[s], Q[1 - s], V.nx, V.ny, V.nz, G);
+    if (A.sampler == 1) build_sobol(Q[s], Q[1 - s], V, A.rate, *reinterpret_cast<SobolRec*>(&G));
+    else build_side(Q[s], Q[1 - s], V.nx, V.ny, V.nz, G);
     const int4* src = reinterpret_cast<const int4*>(&G);
     int4* dst = reinterpret_cast<int4*>(&A.geom[2 * i + s]);
 #pragma unroll
@@ -1252,3 +1264,5 @@ cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, un
 }
 
 }  // namespace morea
+
+#include "morea_sobol.cuh"

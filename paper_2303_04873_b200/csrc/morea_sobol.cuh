@@ -1,0 +1,355 @@
+// morea_sobol.cuh -- NEXT-1: the Sobol-in-tetrahedron sampler of PAPER.md
+// App. A.2 (L744-751) on sm_100a, included by morea_kernels.cu (one TU).
+//
+// "We uniformly sample N points in each tetrahedron using its barycentric
+// coordinate system, with N being determined by the volume of the tetrahedron.
+// For each point, we sample 4 random real numbers r_i in [0;1] and take
+// -log(r_i) ... normalize the coordinates by their sum ... the Sobol sequence
+// ... seeding the Sobol sequence for each tetrahedron with a seed derived from
+// its coordinates."  Readings S1..S9: DESIGN.md §3.
+//
+// k_setup writes a SobolRec per (item, side) (build_sobol).  k_sobol: persistent
+// warps over the same item queue as k_raster; lane l of a 32-sample step takes
+// point k = s0 + l.  In Gray-code order point k is x(g(k)) with g(k) = k ^ k>>1
+// and x linear over GF(2) in g, so x(g(s0 + l)) = x(g(s0)) ^ x(g(l)) for s0 a
+// multiple of 32: one warp XOR-reduction per step (x(g(s0))) and a per-lane
+// constant (x(g(l))).
+//
+// Fast path in fp32: u = (x + 1/2) 2^-32, e = -lg2 u (MUFU), lambda = e / sum e
+// (the ln 2 factor cancels), positions by fma chains.  Every decision the
+// oracle takes on a position (clamp, floor, "is an integer") is taken from the
+// fp32 position only when it is farther than a derived bound eps from every
+// lattice plane; otherwise exact_sobol recomputes the position with the
+// oracle's exact sequence of IEEE fp64 operations (the same -log routine, S5)
+// and decides there.  Values (a, b, the guidance terms) stay fp32.
+#pragma once
+
+namespace morea {
+
+// ---------------------------------------------------------------------------
+// S8 exact fallback: lambda and both positions with the oracle's fp64 operation
+// sequence; fa / fb = "some contributing corner (O5 clamp rules) is > 0".
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool sb_positive_at(const float* __restrict__ vol, const double x[3],
+                                               int nx, int ny, int nz) {
+  const int dims[3] = {nx, ny, nz};
+  int s[3][2], c[3];
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    const int n = dims[a];
+    if (x[a] <= 0.0) {
+      s[a][0] = 0; c[a] = 1;
+    } else if (x[a] >= (double)(n - 1)) {
+      s[a][0] = n - 1; c[a] = 1;
+    } else {
+      const double fl = floor(x[a]);
+      s[a][0] = (int)fl;
+      s[a][1] = (int)fl + 1;
+      c[a] = (x[a] == fl) ? 1 : 2;
+    }
+  }
+  for (int k = 0; k < c[2]; k++)
+    for (int j = 0; j < c[1]; j++)
+      for (int i = 0; i < c[0]; i++)
+        if (__ldg(&vol[((long long)s[2][k] * ny + s[1][j]) * nx + s[0][i]]) > 0.0f) return true;
+  return false;
+}
+
+__device__ __noinline__ void exact_sobol(const SobolRec& R, const unsigned xm[4], const float* volS,
+                                         const float* volO, int nx, int ny, int nz, bool& fa,
+                                         bool& fb) {
+  double e[4];
+  for (int j = 0; j < 4; j++) e[j] = sb_neg_log(xm[j]);
+  const double s = __dadd_rn(__dadd_rn(__dadd_rn(e[0], e[1]), e[2]), e[3]);
+  double lam[4];
+  for (int j = 0; j < 4; j++) lam[j] = __ddiv_rn(e[j], s);
+  double p[3], tp[3];
+  for (int a = 0; a < 3; a++) {
+    const double x0 = (double)R.Q[0][a] / 1024.0, y0 = (double)R.Qo[0][a] / 1024.0;
+    const double d1 = (double)(R.Q[1][a] - R.Q[0][a]) / 1024.0;
+    const double d2 = (double)(R.Q[2][a] - R.Q[0][a]) / 1024.0;
+    const double d3 = (double)(R.Q[3][a] - R.Q[0][a]) / 1024.0;
+    const double o1 = (double)(R.Qo[1][a] - R.Qo[0][a]) / 1024.0;
+    const double o2 = (double)(R.Qo[2][a] - R.Qo[0][a]) / 1024.0;
+    const double o3 = (double)(R.Qo[3][a] - R.Qo[0][a]) / 1024.0;
+    p[a] = __dadd_rn(x0, __dadd_rn(__dadd_rn(__dmul_rn(lam[1], d1), __dmul_rn(lam[2], d2)),
+                                   __dmul_rn(lam[3], d3)));
+    tp[a] = __dadd_rn(y0, __dadd_rn(__dadd_rn(__dmul_rn(lam[1], o1), __dmul_rn(lam[2], o2)),
+                                    __dmul_rn(lam[3], o3)));
+  }
+  fa = sb_positive_at(volS, p, nx, ny, nz);
+  fb = sb_positive_at(volO, tp, nx, ny, nz);
+}
+
+// ---------------------------------------------------------------------------
+// k_sobol
+// ---------------------------------------------------------------------------
+struct SobolWarp {
+  SobolRec R;
+  unsigned long long stat[3];
+};
+
+__device__ __forceinline__ float sb_plerp(float a, float b, float t, float omt) {
+  return fmaf(t, b, omt * a);  // positivity-exact lerp (see plerp)
+}
+
+// corner, weights and texel coordinates of one position (O5 clamp), and the
+// ambiguity test |f - 1/2| >= 1/2 - eps on every axis
+struct SbPos {
+  float fx, fy, fz;  // weights of the upper corners
+  float ix, iy, iz;  // lower corner (clamped, exact floats)
+};
+
+__device__ __forceinline__ bool sb_locate(float x, float y, float z, float eps, bool clamp,
+                                          const Volumes& V, SbPos& P) {
+  const float flx = floorf(x), fly = floorf(y), flz = floorf(z);
+  P.fx = x - flx;
+  P.fy = y - fly;
+  P.fz = z - flz;
+  const float lim = 0.5f - eps;
+  const bool amb = (fabsf(P.fx - 0.5f) >= lim) | (fabsf(P.fy - 0.5f) >= lim) | (fabsf(P.fz - 0.5f) >= lim);
+  P.ix = flx;
+  P.iy = fly;
+  P.iz = flz;
+  if (clamp) {
+    P.fx = P.ix < 0.f ? 0.f : (P.ix > V.fnx2 ? 1.f : P.fx);
+    P.fy = P.iy < 0.f ? 0.f : (P.iy > V.fny2 ? 1.f : P.fy);
+    P.fz = P.iz < 0.f ? 0.f : (P.iz > V.fnz2 ? 1.f : P.fz);
+    P.ix = fminf(fmaxf(P.ix, 0.f), V.fnx2);
+    P.iy = fminf(fmaxf(P.iy, 0.f), V.fny2);
+    P.iz = fminf(fmaxf(P.iz, 0.f), V.fnz2);
+  }
+  return amb;
+}
+
+template <bool TEX>
+__device__ __forceinline__ float sb_trilinear(const Volumes& V, unsigned long long tex,
+                                              const float* __restrict__ vol, float uoff,
+                                              const SbPos& P) {
+  float c[8];
+  if (TEX) {
+    const float u = P.ix + uoff, v = fmaf(P.iz, V.fny, P.iy) + 1.0f;
+    const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v, 0);
+    const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v + V.fny, 0);
+    c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
+    c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
+  } else {
+    // plain loads; the corner indices are clamped into the volume (only ambiguous
+    // samples at the border can ask for index -1 or n, with weight ~0)
+    const int x0 = min(max((int)P.ix, 0), V.nx - 2), y0 = min(max((int)P.iy, 0), V.ny - 2),
+              z0 = min(max((int)P.iz, 0), V.nz - 2);
+    const long long sy = V.nx, sz = (long long)V.nx * V.ny;
+    const float* b = vol + z0 * sz + y0 * sy + x0;
+    c[0] = __ldg(b); c[1] = __ldg(b + 1); c[2] = __ldg(b + sy); c[3] = __ldg(b + sy + 1);
+    c[4] = __ldg(b + sz); c[5] = __ldg(b + sz + 1); c[6] = __ldg(b + sz + sy); c[7] = __ldg(b + sz + sy + 1);
+  }
+  const float gx = 1.f - P.fx, gy = 1.f - P.fy, gz = 1.f - P.fz;
+  return sb_plerp(sb_plerp(sb_plerp(c[0], c[1], P.fx, gx), sb_plerp(c[2], c[3], P.fx, gx), P.fy, gy),
+                  sb_plerp(sb_plerp(c[4], c[5], P.fx, gx), sb_plerp(c[6], c[7], P.fx, gx), P.fy, gy),
+                  P.fz, gz);
+}
+
+template <bool TEX>
+__global__ void __launch_bounds__(kRasterThreads, MOREA_SOBOL_MINB) k_sobol(const EvalArgs A) {
+  __shared__ SobolWarp smem[kWarpsPerBlock];
+  __shared__ unsigned sV[4][32];
+  int warp, lane;
+  asm volatile("shr.u32 %0, %1, 5;" : "=r"(warp) : "r"(threadIdx.x));
+  asm volatile("and.b32 %0, %1, 31;" : "=r"(lane) : "r"(threadIdx.x));
+  for (int t = threadIdx.x; t < 128; t += blockDim.x) sV[t >> 5][t & 31] = A.sobol_v[t];
+  __syncthreads();
+  SobolWarp& S = smem[warp];
+  const Volumes& V = A.vol;
+  // x(g(lane)): the per-lane constant part of the point index (S2)
+  unsigned xlo[4];
+  {
+    const unsigned gl = (unsigned)lane ^ ((unsigned)lane >> 1);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      unsigned v = 0;
+#pragma unroll
+      for (int b = 0; b < 5; b++)
+        if ((gl >> b) & 1u) v ^= sV[j][b];
+      xlo[j] = v;
+    }
+  }
+  const unsigned vlane[4] = {sV[0][lane], sV[1][lane], sV[2][lane], sV[3][lane]};
+  const long long per_v = (long long)A.n_entries * A.P;
+  const long long n_items = per_v * A.n_raster_versions;
+  if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0ull;
+  while (true) {
+    unsigned long long item = 0;
+    if (lane == 0) item = atomicAdd(A.counter, 1ULL);
+    item = __shfl_sync(FULLMASK, item, 0);
+    if ((long long)item >= n_items) break;
+    const int ver = (int)(item / (unsigned long long)per_v);
+    const long long rem = (long long)item - (long long)ver * per_v;
+    const int es = (int)(rem / A.P);
+    const int sol = (int)(rem - (long long)es * A.P);
+    const int e = A.sched[es];
+    const long long i = ((long long)ver * A.n_entries + e) * A.P + sol;
+    double hsum = 0.0, gsum = 0.0;
+    long long n_tot = 0, n_side0 = 0;
+    int nb = 0;
+#pragma unroll 1
+    for (int side = 0; side < 2; side++) {
+      const int oth = 1 - side;
+      constexpr int kVec = (int)(sizeof(SobolRec) / 16);
+      __syncwarp();
+      if (lane < kVec)
+        reinterpret_cast<int4*>(&S.R)[lane] =
+            __ldg(reinterpret_cast<const int4*>(&A.geom[2 * i + side]) + lane);
+      __syncwarp();
+      const SobolRec& R = S.R;
+      if (!(R.flags & 1)) continue;
+      const long long N = R.N;
+      n_tot += N;
+      if (side == 0) n_side0 = N;
+      const bool clamp = !(R.flags & 2);
+      const unsigned m0 = R.mask[0] ^ xlo[0], m1 = R.mask[1] ^ xlo[1], m2 = R.mask[2] ^ xlo[2],
+                     m3 = R.mask[3] ^ xlo[3];
+      const float uoffS = 1.0f + (TEX ? (float)side * V.fnx : 0.f);
+      const float uoffO = 1.0f + (TEX ? (float)oth * V.fnx : 0.f);
+      const float* volS = side == 0 ? V.I[0] : V.I[1];
+      const float* volO = side == 0 ? V.I[1] : V.I[0];
+      const unsigned char* dil = side == 0 ? V.dil[0] : V.dil[1];
+      float hf = 0.f, gf = 0.f;
+      int step = 0;
+#pragma unroll 1
+      for (long long s0 = 0; s0 < N; s0 += 32) {
+        // S2: x(g(s0)) by one XOR reduction per dimension (bit b of g(s0) <-> lane b)
+        const unsigned long long gs = (unsigned long long)s0 ^ ((unsigned long long)s0 >> 1);
+        const bool bit = (gs >> lane) & 1ull;
+        const unsigned x0 = __reduce_xor_sync(FULLMASK, bit ? vlane[0] : 0u) ^ m0;
+        const unsigned x1 = __reduce_xor_sync(FULLMASK, bit ? vlane[1] : 0u) ^ m1;
+        const unsigned x2 = __reduce_xor_sync(FULLMASK, bit ? vlane[2] : 0u) ^ m2;
+        const unsigned x3 = __reduce_xor_sync(FULLMASK, bit ? vlane[3] : 0u) ^ m3;
+        const bool valid = s0 + lane < N;
+        // S5/S7 fast path: e = -lg2 u (the ln 2 factor cancels in the normalisation)
+        const float e0 = -__log2f(fmaf((float)x0, 0x1.0p-32f, 0x1.0p-33f));
+        const float e1 = -__log2f(fmaf((float)x1, 0x1.0p-32f, 0x1.0p-33f));
+        const float e2 = -__log2f(fmaf((float)x2, 0x1.0p-32f, 0x1.0p-33f));
+        const float e3 = -__log2f(fmaf((float)x3, 0x1.0p-32f, 0x1.0p-33f));
+        const float sum = ((e0 + e1) + e2) + e3;
+        const float rs = __fdividef(1.0f, sum);
+        const float l1 = e1 * rs, l2 = e2 * rs, l3 = e3 * rs;
+        const float eps = fmaf(R.epsA, rs, R.epsB);
+        const float px = fmaf(l3, R.D[2][0], fmaf(l2, R.D[1][0], fmaf(l1, R.D[0][0], R.x0[0])));
+        const float py = fmaf(l3, R.D[2][1], fmaf(l2, R.D[1][1], fmaf(l1, R.D[0][1], R.x0[1])));
+        const float pz = fmaf(l3, R.D[2][2], fmaf(l2, R.D[1][2], fmaf(l1, R.D[0][2], R.x0[2])));
+        const float tx = fmaf(l3, R.Do[2][0], fmaf(l2, R.Do[1][0], fmaf(l1, R.Do[0][0], R.x0o[0])));
+        const float ty = fmaf(l3, R.Do[2][1], fmaf(l2, R.Do[1][1], fmaf(l1, R.Do[0][1], R.x0o[1])));
+        const float tz = fmaf(l3, R.Do[2][2], fmaf(l2, R.Do[1][2], fmaf(l1, R.Do[0][2], R.x0o[2])));
+        SbPos Pp, Pt;
+        bool amb = sb_locate(px, py, pz, eps, clamp, V, Pp);
+        amb = sb_locate(tx, ty, tz, eps, clamp, V, Pt) || amb;
+        const float a = sb_trilinear<TEX>(V, V.texI, volS, uoffS, Pp);
+        const float b = sb_trilinear<TEX>(V, V.texI, volO, uoffO, Pt);
+        bool fa = a > 0.f, fb = b > 0.f;
+        if ((amb || A.sobol_force_exact) && valid) {
+          const unsigned xm[4] = {x0, x1, x2, x3};
+          exact_sobol(R, xm, volS, volO, V.nx, V.ny, V.nz, fa, fb);
+        }
+        // h with both cases decided exactly (S8)
+        const float h = (fa && fb) ? (a - b) * (a - b) : ((!fa && !fb) ? 0.f : 1.f);
+        hf += valid ? h : 0.f;
+        // a6 (S9): pairs whose distance can be < r in p's cell
+        unsigned bm = 0u;
+        if (V.K > 0 && valid) {
+          const int cx = min(max((int)Pp.ix, 0), V.nx - 1), cy = min(max((int)Pp.iy, 0), V.ny - 1),
+                    cz = min(max((int)Pp.iz, 0), V.nz - 1);
+          bm = __ldg(&dil[((long long)cz * V.ny + cy) * V.nx + cx]);
+        }
+        nb += __popc(bm);
+        while (__any_sync(FULLMASK, bm != 0u)) {
+          if (bm) {
+            const int pi = __ffs(bm) - 1;
+            bm &= bm - 1;
+            float d, Dp;
+            if (TEX) {
+              d = sb_trilinear<true>(V, V.texM, nullptr, 1.0f + (float)(side * V.K + pi) * V.fnx, Pp);
+              Dp = sb_trilinear<true>(V, V.texM, nullptr, 1.0f + (float)(oth * V.K + pi) * V.fnx, Pt);
+            } else {
+              d = sb_trilinear<false>(V, 0ull, (side == 0 ? V.dmap[0] : V.dmap[1]) + (long long)pi * V.V,
+                                      1.0f, Pp);
+              Dp = sb_trilinear<false>(V, 0ull, (side == 0 ? V.dmap[1] : V.dmap[0]) + (long long)pi * V.V,
+                                       1.0f, Pt);
+            }
+            if (d < V.rf) {
+              const float dd = d - Dp;
+              gf += V.wf[side][pi] * ((V.rf - d) + V.rlo) * (dd * dd);
+            }
+          }
+        }
+        if ((++step & 15) == 0) {
+          hsum += (double)hf;
+          gsum += (double)gf;
+          hf = gf = 0.f;
+        }
+      }
+      hsum += (double)hf;
+      gsum += (double)gf;
+    }
+    HGN out;
+    out.h = warp_sum_d(hsum);
+    out.g = warp_sum_d(gsum);
+    out.n = (int)n_tot;
+    out.nb = warp_sum_i(nb);
+    out.n0 = (int)n_side0;
+    out.pad = 0;
+    if (lane == 0) {
+      A.hgn[i] = out;
+      S.stat[0] += n_tot;
+      S.stat[1] += out.nb;
+      S.stat[2] += 1;
+    }
+  }
+  if (lane == 0 && A.stats) {
+    atomicAdd(&A.stats[0], S.stat[0]);
+    atomicAdd(&A.stats[1], S.stat[1]);
+    atomicAdd(&A.stats[2], S.stat[2]);
+  }
+}
+
+int sobol_blocks_per_sm(bool tex) {
+  int nb = 0;
+  cudaError_t e = tex ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sobol<true>, kRasterThreads, 0)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sobol<false>, kRasterThreads, 0);
+  if (e != cudaSuccess) return 1;
+  return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_sobol(const EvalArgs& a, int grid, cudaStream_t s) {
+  if (a.vol.use_tex) k_sobol<true><<<grid, kRasterThreads, 0, s>>>(a);
+  else k_sobol<false><<<grid, kRasterThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// dil[v] = OR of band[c] over the cell corners c in v + {0,1}^3 (clamped)
+__global__ void k_dilate_band(const unsigned char* __restrict__ band, int nx, int ny, int nz,
+                              unsigned char* __restrict__ dil) {
+  const long long V = (long long)nx * ny * nz;
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
+       v += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((long long)nx * ny));
+    unsigned m = 0;
+    for (int dz = 0; dz < 2; dz++)
+      for (int dy = 0; dy < 2; dy++)
+        for (int dx = 0; dx < 2; dx++) {
+          const int cx = min(x + dx, nx - 1), cy = min(y + dy, ny - 1), cz = min(z + dz, nz - 1);
+          m |= band[((long long)cz * ny + cy) * nx + cx];
+        }
+    dil[v] = (unsigned char)m;
+  }
+}
+
+cudaError_t launch_dilate_band(const unsigned char* band, int nx, int ny, int nz, unsigned char* dil,
+                               cudaStream_t s) {
+  const long long V = (long long)nx * ny * nz;
+  const long long nblk = (V + 255) / 256;
+  const int grid = (int)(nblk < 148 * 16 ? nblk : 148 * 16);
+  k_dilate_band<<<grid, 256, 0, s>>>(band, nx, ny, nz, dil);
+  return cudaGetLastError();
+}
+
+}  // namespace morea

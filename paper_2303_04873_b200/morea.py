@@ -31,7 +31,9 @@ assert ACC_DTYPE.itemsize == 48
 EXPORTS = ["morea_create", "morea_destroy", "morea_last_error", "morea_stream", "morea_load_images",
            "morea_set_mesh", "morea_eval_full", "morea_eval_partial", "morea_partial_deps",
            "morea_check_folds", "morea_owner_map", "morea_distance_map", "morea_prof_enable",
-           "morea_prof_read", "morea_kernel_launches"]
+           "morea_prof_read", "morea_kernel_launches", "morea_set_sampler"]
+SAMPLER_VOXEL = 0
+SAMPLER_SOBOL = 1
 
 
 class MoreaError(RuntimeError):
@@ -62,6 +64,7 @@ def _load():
     L.morea_owner_map.argtypes = [vp, vp, i32, vp]
     L.morea_distance_map.argtypes = [vp, i32, i32, vp]
     L.morea_prof_enable.argtypes = [vp, i32]
+    L.morea_set_sampler.argtypes = [vp, i32, f64]
     L.morea_kernel_launches.argtypes = [vp]
     L.morea_kernel_launches.restype = i64
     L.morea_prof_read.argtypes = [vp] + [ctypes.POINTER(i64), ctypes.POINTER(f64)] + \
@@ -212,6 +215,11 @@ class Context:
             out = np.empty(self.V, np.float32)
         self._check(_lib.morea_distance_map(self.h, int(side), int(pair), _ptr(out)))
         return out
+
+    def set_sampler(self, mode, rate=1.0):
+        """SAMPLER_VOXEL (exactly-once voxel centres) or SAMPLER_SOBOL (App. A.2
+        Sobol points per tet, `rate` samples per voxel of tet volume)."""
+        self._check(_lib.morea_set_sampler(self.h, int(mode), float(rate)))
 
     # ------------------------------------------------------------------ profiling
     def kernel_launches(self):
