@@ -57,8 +57,11 @@ def test_sobol_per_tet_parity(wl):
     rec = orc.eval_tets(w.offsets[k])
     n_o = rec[:, 2] + rec[:, 3]
     assert np.array_equal(tc[0, :, 2].astype(np.int64), n_o.astype(np.int64))
-    np.testing.assert_allclose(tc[0, :, 0], rec[:, 0], rtol=RTOL, atol=1e-9 * np.maximum(n_o, 1))
-    np.testing.assert_allclose(tc[0, :, 1], rec[:, 1], rtol=RTOL, atol=1e-7 * np.maximum(n_o, 1))
+    # per-tet sums: 1e-5 relative, or an absolute slack of 1e-9 (h) / 1e-7 (g, mm^2) per sample
+    for col, ocol, per in ((0, 0, 1e-9), (1, 1, 1e-7)):
+        err = np.abs(tc[0, :, col] - rec[:, ocol])
+        bound = RTOL * np.abs(rec[:, ocol]) + per * np.maximum(n_o, 1)
+        assert (err <= bound).all(), (col, np.max(err / bound), np.argmax(err / bound))
     np.testing.assert_allclose(tc[0, :, 3], rec[:, 4], rtol=1e-12, atol=1e-12)
 
 
