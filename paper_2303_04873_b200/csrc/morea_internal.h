@@ -44,8 +44,10 @@ static_assert(sizeof(SideRec) == 384, "SideRec layout");
 struct __align__(16) SobolRec {
   int Q[4][3];              // sampled side, Q.10 (exact; the fp64 fallback recomputes from these)
   int Qo[4][3];             // other side
-  float x0[3], D[3][3];     // sampled side: X_0 and X_k - X_0 (k = 1..3), voxel units, fp32-exact
+  float x0[3], D[3][3];     // sampled side: frac(X_0) and X_k - X_0 (k = 1..3), voxel units,
+                            // fp32-exact; floor(X_0) in i0 (positions = i0 + x0 + sum l_k D_k)
   float x0o[3], Do[3][3];   // other side
+  float i0[3], i0o[3];      // floor(X_0) per side (exact small integers as floats)
   unsigned mask[4];         // digital-shift masks (S3/S4)
   long long N;              // samples of this side (S6)
   float epsA, epsB;         // fast-path position error bound eps = epsA / s + epsB, s = sum -lg2 u

@@ -15,7 +15,7 @@
 // multiple of 32: one warp XOR-reduction per step (x(g(s0))) and a per-lane
 // constant (x(g(l))).
 //
-// Fast path in fp32: u = (x + 1/2) 2^-32, e = -lg2 u (MUFU), lambda = e / sum e
+// Fast path in fp32: u = (x + 1/2) 2^-32, e = -lg2 u (MUFU.LG2), lambda = e / sum e
 // (the ln 2 factor cancels), positions by fma chains.  Every decision the
 // oracle takes on a position (clamp, floor, "is an integer") is taken from the
 // fp32 position only when it is farther than a derived bound eps from every
@@ -33,26 +33,28 @@ namespace morea {
 __device__ __forceinline__ bool sb_positive_at(const float* __restrict__ vol, const double x[3],
                                                int nx, int ny, int nz) {
   const int dims[3] = {nx, ny, nz};
-  int s[3][2], c[3];
+  int lo[3], hi[3];  // contributing corner indices per axis (lo == hi: one corner)
 #pragma unroll
   for (int a = 0; a < 3; a++) {
     const int n = dims[a];
     if (x[a] <= 0.0) {
-      s[a][0] = 0; c[a] = 1;
+      lo[a] = hi[a] = 0;
     } else if (x[a] >= (double)(n - 1)) {
-      s[a][0] = n - 1; c[a] = 1;
+      lo[a] = hi[a] = n - 1;
     } else {
       const double fl = floor(x[a]);
-      s[a][0] = (int)fl;
-      s[a][1] = (int)fl + 1;
-      c[a] = (x[a] == fl) ? 1 : 2;
+      lo[a] = (int)fl;
+      hi[a] = (x[a] == fl) ? lo[a] : lo[a] + 1;
     }
   }
-  for (int k = 0; k < c[2]; k++)
-    for (int j = 0; j < c[1]; j++)
-      for (int i = 0; i < c[0]; i++)
-        if (__ldg(&vol[((long long)s[2][k] * ny + s[1][j]) * nx + s[0][i]]) > 0.0f) return true;
-  return false;
+  // the (up to) 8 contributing corners, loaded together (one latency), then OR-ed
+  bool any = false;
+#pragma unroll
+  for (int c = 0; c < 8; c++) {
+    const int i = (c & 1) ? hi[0] : lo[0], j = (c & 2) ? hi[1] : lo[1], k = (c & 4) ? hi[2] : lo[2];
+    any = any | (__ldg(&vol[((long long)k * ny + j) * nx + i]) > 0.0f);
+  }
+  return any;
 }
 
 __device__ __noinline__ void exact_sobol(const SobolRec& R, const unsigned xm[4], const float* volS,
@@ -100,17 +102,18 @@ struct SbPos {
   float ix, iy, iz;  // lower corner (clamped, exact floats)
 };
 
-__device__ __forceinline__ bool sb_locate(float x, float y, float z, float eps, bool clamp,
-                                          const Volumes& V, SbPos& P) {
+// (x, y, z): position minus the integer offset i0 (floor of the tet's first vertex)
+__device__ __forceinline__ bool sb_locate(float x, float y, float z, const float* i0, float eps,
+                                          bool clamp, const Volumes& V, SbPos& P) {
   const float flx = floorf(x), fly = floorf(y), flz = floorf(z);
   P.fx = x - flx;
   P.fy = y - fly;
   P.fz = z - flz;
   const float lim = 0.5f - eps;
   const bool amb = (fabsf(P.fx - 0.5f) >= lim) | (fabsf(P.fy - 0.5f) >= lim) | (fabsf(P.fz - 0.5f) >= lim);
-  P.ix = flx;
-  P.iy = fly;
-  P.iz = flz;
+  P.ix = flx + i0[0];
+  P.iy = fly + i0[1];
+  P.iz = flz + i0[2];
   if (clamp) {
     P.fx = P.ix < 0.f ? 0.f : (P.ix > V.fnx2 ? 1.f : P.fx);
     P.fy = P.iy < 0.f ? 0.f : (P.iy > V.fny2 ? 1.f : P.fy);
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_SOBOL_MINB) k_sobol(cons
         const float e2 = -__log2f(fmaf((float)x2, 0x1.0p-32f, 0x1.0p-33f));
         const float e3 = -__log2f(fmaf((float)x3, 0x1.0p-32f, 0x1.0p-33f));
         const float sum = ((e0 + e1) + e2) + e3;
-        const float rs = __fdividef(1.0f, sum);
+        const float rs = __frcp_rn(sum);
         const float l1 = e1 * rs, l2 = e2 * rs, l3 = e3 * rs;
         const float eps = fmaf(R.epsA, rs, R.epsB);
         const float px = fmaf(l3, R.D[2][0], fmaf(l2, R.D[1][0], fmaf(l1, R.D[0][0], R.x0[0])));
@@ -241,8 +244,8 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_SOBOL_MINB) k_sobol(cons
         const float ty = fmaf(l3, R.Do[2][1], fmaf(l2, R.Do[1][1], fmaf(l1, R.Do[0][1], R.x0o[1])));
         const float tz = fmaf(l3, R.Do[2][2], fmaf(l2, R.Do[1][2], fmaf(l1, R.Do[0][2], R.x0o[2])));
         SbPos Pp, Pt;
-        bool amb = sb_locate(px, py, pz, eps, clamp, V, Pp);
-        amb = sb_locate(tx, ty, tz, eps, clamp, V, Pt) || amb;
+        bool amb = sb_locate(px, py, pz, R.i0, eps, clamp, V, Pp);
+        amb = sb_locate(tx, ty, tz, R.i0o, eps, clamp, V, Pt) || amb;
         const float a = sb_trilinear<TEX>(V, V.texI, volS, uoffS, Pp);
         const float b = sb_trilinear<TEX>(V, V.texI, volO, uoffO, Pt);
         bool fa = a > 0.f, fb = b > 0.f;

@@ -72,7 +72,7 @@ __device__ void build_sobol(const int Q[4][3], const int Qo[4][3], const Volumes
   for (int j = 0; j < 4; j++) R.mask[j] = (unsigned)(sb_splitmix64(seed + (unsigned long long)j) >> 32);
   const int dims[3] = {V.nx, V.ny, V.nz};
   bool inside = true;
-  float dmax = 0.f, rmax = 0.f;
+  float dmax = 0.f;
 #pragma unroll
   for (int k = 0; k < 4; k++)
 #pragma unroll
@@ -81,12 +81,15 @@ __device__ void build_sobol(const int Q[4][3], const int Qo[4][3], const Volumes
       R.Qo[k][a] = Qo[k][a];
       inside = inside && Q[k][a] >= 0 && Q[k][a] <= 1024 * (dims[a] - 1) && Qo[k][a] >= 0 &&
                Qo[k][a] <= 1024 * (dims[a] - 1);
-      rmax = fmaxf(rmax, fmaxf(fabsf((float)Q[k][a]), fabsf((float)Qo[k][a])) * (1.0f / 1024.0f));
     }
 #pragma unroll
   for (int a = 0; a < 3; a++) {
-    R.x0[a] = (float)Q[0][a] * (1.0f / 1024.0f);
-    R.x0o[a] = (float)Qo[0][a] * (1.0f / 1024.0f);
+    // X_0 = i0 + x0 with i0 = floor(X_0): the fp32 position is accumulated around
+    // x0 in [0, 1), so its rounding is relative to the tet size, not to |X|
+    R.i0[a] = (float)(Q[0][a] >> 10);
+    R.i0o[a] = (float)(Qo[0][a] >> 10);
+    R.x0[a] = (float)(Q[0][a] & 1023) * (1.0f / 1024.0f);
+    R.x0o[a] = (float)(Qo[0][a] & 1023) * (1.0f / 1024.0f);
 #pragma unroll
     for (int k = 1; k < 4; k++) {
       R.D[k - 1][a] = (float)(Q[k][a] - Q[0][a]) * (1.0f / 1024.0f);
@@ -94,11 +97,14 @@ __device__ void build_sobol(const int Q[4][3], const int Qo[4][3], const Volumes
       dmax = fmaxf(dmax, fmaxf(fabsf(R.D[k - 1][a]), fabsf(R.Do[k - 1][a])));
     }
   }
-  // |p_fast - p_exact| <= D (2 Delta / s + 2^-21) + 1.5 ulp(R), Delta = sum of the
-  // -lg2 errors <= 2^-21 (4 + s) + 2^-20.5 (u rounding, MUFU.LG2, fp32 sums),
-  // D = max |X_k - X_0|, R = max |X|; twice that.
-  R.epsA = 2.0f * dmax * (0x1.0p-18f + 0x1.6a09e6p-20f);
-  R.epsB = 2.0f * (dmax * (0x1.0p-20f + 0x1.0p-21f) + 1.5f * 0x1.0p-23f * (fmaxf(rmax, 1.0f) + 3.0f * dmax));
+  // Error of the fp32 offset y = x0 + sum_k l_k D_k against the oracle's position
+  // (DESIGN.md §4.5): e_j = -lg2.approx(u_j) (absolute error <= 2^-22.6, the
+  // exponent part is exact) on u_j rounded to fp32 (2^-24 relative, 2^-23.47 in
+  // e_j): Delta = sum_j |de_j| <= 2^-20; lambda_j = e_j rcp_rn(s) with s summed in
+  // fp32: sum_k |dl_k| <= 2 Delta / s + 2^-21; three fma roundings
+  // <= 1.5 2^-23 (1 + 3 D).  eps = 2x the bound, as epsA / s + epsB.
+  R.epsA = 2.0f * dmax * 0x1.0p-19f;
+  R.epsB = 2.0f * (dmax * 0x1.0p-21f + 1.5f * 0x1.0p-23f * (1.0f + 3.0f * dmax));
   R.flags = (R.N > 0 ? 1 : 0) | (inside ? 2 : 0);
   R.pad = 0;
 }

@@ -1,4 +1,5 @@
-"""Dev tool: per-source-line instruction and stall shares of one kernel in an ncu report."""
+"""Dev tool: per-source-line instruction and stall shares of one kernel in an ncu report
+(all source files of the kernel)."""
 import csv, subprocess, sys
 
 rep = sys.argv[1]
@@ -6,15 +7,21 @@ top = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-hdr = [i for i, r in enumerate(rows) if r and r[0] == "Line No"]
-h = rows[hdr[0]]
-ie = h.index("Instructions Executed")
-ws = h.index("Warp Stall Sampling (All Samples)")
-end = hdr[1] if len(hdr) > 1 else len(rows)
-data = [(int(r[0]), r[1], int(r[ws] or 0), int(r[ie] or 0))
-        for r in rows[hdr[0] + 1:end] if r and r[0].isdigit()]
-ts = sum(d[2] for d in data) or 1
-ti = sum(d[3] for d in data) or 1
+data, fname, cols = [], "?", None
+for r in rows:
+    if not r:
+        continue
+    if r[0] in ("File Path", "File Name"):
+        fname = r[1].split("/")[-1]
+        continue
+    if r[0] == "Line No":
+        cols = (r.index("Warp Stall Sampling (All Samples)"), r.index("Instructions Executed"))
+        continue
+    if cols and r[0].isdigit():
+        num = lambda x: int(x) if x.strip().lstrip("-").isdigit() else 0
+        data.append((fname, int(r[0]), r[1], num(r[cols[0]]), num(r[cols[1]])))
+ts = sum(d[3] for d in data) or 1
+ti = sum(d[4] for d in data) or 1
 print("stall samples", ts, "instructions", ti)
-for d in sorted(data, key=lambda d: -d[3])[:top]:
-    print("%5d %5.1f%% %5.1f%%  %s" % (d[0], 100 * d[2] / ts, 100 * d[3] / ti, d[1].strip()[:100]))
+for d in sorted(data, key=lambda d: -d[4])[:top]:
+    print("%-14s %5d %5.1f%% %5.1f%%  %s" % (d[0][:14], d[1], 100 * d[3] / ts, 100 * d[4] / ti, d[2].strip()[:90]))

@@ -7,7 +7,9 @@ from synth import make_workload, fos_plan, partial_request
 
 idx = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 t0 = time.time(); w = make_workload(idx); print("gen", time.time() - t0, flush=True)
-t0 = time.time(); ctx = morea.Context.from_workload(w); torch.cuda.synchronize(); print("load", time.time() - t0, flush=True)
+t0 = time.time(); ctx = morea.Context.from_workload(w)
+if "sobol" in sys.argv: ctx.set_sampler(morea.SAMPLER_SOBOL, 1.0)
+torch.cuda.synchronize(); print("load", time.time() - t0, flush=True)
 dev = torch.device("cuda:0")
 off = torch.from_numpy(w.offsets).to(dev)
 P = w.P
