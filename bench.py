@@ -294,6 +294,10 @@ def main():
     t_full = timed(lambda: ctx.eval_full(off_d, obj_d, acc_d, cache_d))
     t_part = timed(lambda: ctx.eval_partial(off_d, acc_d, go, ch, nv_d, cache_d, pobj_d, pacc_d))
     t_part_nc = timed(lambda: ctx.eval_partial(off_d, acc_d, go, ch, nv_d, None, pobj_d, pacc_d))
+    # NEXT-1: the paper's Sobol-in-tetrahedron sample set (App. A.2), rate 1 sample / voxel
+    ctx.set_sampler(morea.SAMPLER_SOBOL, 1.0)
+    t_sobol = timed(lambda: ctx.eval_full(off_d, obj_d, acc_d, None))
+    ctx.set_sampler(morea.SAMPLER_VOXEL)
 
     # ---- roofline of the dominant kernel (k_raster), SURVEY.md §8(d) algorithmic bytes
     peak, peak_src = measured_hbm_peak()
@@ -369,6 +373,8 @@ def main():
                 "full_evals_per_s": P * 1e3 / t_full, "full_ms": t_full,
                 "partial_evals_per_s": P * G * 1e3 / t_part, "partial_ms": t_part,
                 "partial_nocache_evals_per_s": P * G * 1e3 / t_part_nc,
+                "sobol_full_evals_per_s": P * 1e3 / t_sobol,
+                "sobol_full_ms": t_sobol,
                 "samples_per_launch": prof["samples"] / max(prof["launches"], 1),
                 "band_entries_per_launch": prof["band_entries"] / max(prof["launches"], 1),
                 "per_gpu_note": "breakdown figures are this rank's (per GPU)",

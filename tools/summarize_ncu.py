@@ -1,6 +1,6 @@
 """Summarise ncu outputs into profiles/ (dev tool, runs here without a GPU).
 
-usage: python tools/summarize_ncu.py <round tag> <launches.csv> <prof.ncu-rep>
+usage: python tools/summarize_ncu.py <round tag> <launches.csv> <prof.ncu-rep> [<prof2.ncu-rep> ...]
 Writes profiles/<tag>_launches.txt (per-kernel share of the launch list),
 profiles/<tag>_ncu_raster.txt (key metrics of the captured k_raster launches)
 and profiles/ncu_summary.json (DRAM bytes per k_raster launch, read by bench.py).
@@ -12,7 +12,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-tag, launches, rep = sys.argv[1], sys.argv[2], sys.argv[3]
+tag, launches, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
+rep = reps[0]
 prof = os.path.join(ROOT, "profiles")
 os.makedirs(prof, exist_ok=True)
 
@@ -39,9 +40,13 @@ for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
 out += ["", "# launch sequence (id, kernel, ms)"] + [f"{i:5d} {n:28s} {t/1e6:10.4f}" for i, n, t in seq]
 open(os.path.join(prof, f"{tag}_launches.txt"), "w").write("\n".join(out) + "\n")
 
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rr = list(csv.reader(raw.splitlines()))
-hdr, units, data = rr[0], rr[1], rr[2:]
+hdr, units, data = None, None, []
+for rp in reps:
+    raw = subprocess.run(["ncu", "-i", rp, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(raw.splitlines()))
+    if hdr is None:
+        hdr, units = rr[0], rr[1]
+    data += [dict(zip(rr[0], d)) for d in rr[2:]]
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct", "sm__inst_executed.sum",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
@@ -58,10 +63,9 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__warps_issue_stalled_mio_throttle_per_warp_active.pct",
         "smsp__warps_issue_stalled_tex_throttle_per_warp_active.pct",
         "smsp__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]
-lines = [f"# ncu --set full of k_raster ({os.path.basename(rep)}), one row per captured launch", ""]
+lines = [f"# ncu --set full of k_raster ({', '.join(os.path.basename(r) for r in reps)}), one row per captured launch", ""]
 dram = []
-for d in data:
-    m = dict(zip(hdr, d))
+for m in data:
     lines.append(f"launch {m.get('ID')} {m.get('Kernel Name','')[:40]}")
     for k in want:
         if k in m:
@@ -78,7 +82,7 @@ for d in data:
         pass
     lines.append("")
 open(os.path.join(prof, f"{tag}_ncu_raster.txt"), "w").write("\n".join(lines) + "\n")
-summ = {"round": tag, "source": os.path.basename(rep),
+summ = {"round": tag, "source": [os.path.basename(r) for r in reps],
         "k_raster_dram_bytes_per_launch": (sum(dram) / len(dram)) if dram else None,
         "k_raster_dram_bytes_each": dram}
 json.dump(summ, open(os.path.join(prof, "ncu_summary.json"), "w"), indent=1)
