@@ -24,6 +24,7 @@
  *   f_magnitude, 10 edges incl. 4 spokes     §4.1.1 eq. L251-259              (O9)
  *   partial evaluation (delta on dependents) §1, §4.2.1 L400-410        (O10)
  *   Sobol-in-tetrahedron sampler (NEXT-1)    App. A.2 L744-751                (S1..S9)
+ *   batched fold repair (NEXT-2)             §4.3.1 L429-437                  (P1..P7)
  *
  * Everything that decides an integer (ownership, fold, the h case split, band
  * membership) is decided exactly in integer arithmetic (int64 / __int128) or
@@ -564,12 +565,11 @@ static void tet_masks(const int64_t Q[4][3], uint32_t mask[4]) {
     for (int j = 0; j < 4; j++) mask[j] = (uint32_t)(splitmix64(seed + (uint64_t)j) >> 32);
 }
 
-/* S5: r = (x + 1/2) 2^-32 in (0, 1) and -log r with a fixed sequence of IEEE
+/* S5: r = (x + 1/2) 2^-32 in (0, 1) and -log r (det_ln: log r for r > 0) with a fixed sequence of IEEE
  * double operations (frexp, one division, a degree-23 odd series), so that
  * both implementations get the same bits:  r = m 2^e, m in [sqrt(1/2), sqrt(2)),
  * log m = 2 atanh t, t = (m - 1)/(m + 1), |t| <= 0.1716.  */
-static double neg_log(uint32_t x) {
-    double r = ((double)x + 0.5) * 2.3283064365386963e-10; /* 2^-32, exact */
+static double det_ln(double r) {
     int e;
     double m = frexp(r, &e); /* r = m 2^e, m in [1/2, 1) */
     if (m < 0.70710678118654752440) { m = m * 2.0; e = e - 1; }
@@ -590,7 +590,11 @@ static double neg_log(uint32_t x) {
     double lm = 2.0 * t * p;
     /* log 2 = LN2_HI + LN2_LO, LN2_HI with 32 trailing zero bits (e LN2_HI exact) */
     double lr = (double)e * 6.93147180369123816490e-01 + ((double)e * 1.90821492927058770002e-10 + lm);
-    return -lr;
+    return lr;
+}
+static double neg_log(uint32_t x) {
+    double r = ((double)x + 0.5) * 2.3283064365386963e-10; /* 2^-32, exact */
+    return -det_ln(r);
 }
 
 /* S6: number of samples of a tet side: N = floor(rate |Delta| / (6 1024^3) + 1/2),
@@ -698,6 +702,181 @@ static void tet_side_sobol(orc_problem *P, int s, const int64_t Q[2][4][3], doub
             *g_sum += P->w[s][i] * ((P->r - d) / P->r) * dd * dd;
         }
     }
+}
+
+/* ------------------------------------------------------------------ */
+/* NEXT-2: fold repair (§4.3.1).                      */
+/* "For each point in a folded tetrahedron, the method mutates the point */
+/* using a Gaussian distribution scaled by its estimated distance to the */
+/* surrounding 3D polygon.  After 64 samples, the change with the best   */
+/* constraint improvement is selected, if present.  If all samples result */
+/* in a deterioration, repair is aborted."  Readings P1..P7. */
+/* The Gaussian draws come from a counter-based generator (SplitMix64    */
+/* keys, Marsaglia's polar method, det_ln) that both implementations     */
+/* write out identically.                                                */
+/* ------------------------------------------------------------------ */
+#define REPAIR_CANDIDATES 64
+
+/* P5: standard normal pairs for one key: uniforms u, v = (32-bit half + 1/2) 2^-31 - 1
+ * (exact), s = u^2 + v^2, rejected unless 0 < s < 1, f = sqrt(-2 ln s / s) */
+static void gauss_pair(uint64_t key, uint64_t *ctr, double *z0, double *z1) {
+    for (;;) {
+        uint64_t w = splitmix64(key + (*ctr)++);
+        double u = ((double)(uint32_t)(w >> 32) + 0.5) * 4.656612873077392578125e-10 - 1.0;
+        double v = ((double)(uint32_t)w + 0.5) * 4.656612873077392578125e-10 - 1.0;
+        double sq = u * u + v * v;
+        if (!(sq < 1.0) || sq == 0.0) continue;
+        double f = sqrt(-2.0 * det_ln(sq) / sq);
+        *z0 = u * f;
+        *z1 = v * f;
+        return;
+    }
+}
+/* P5: key of candidate c of point j, side s, solution k */
+static uint64_t repair_key(uint64_t seed, int64_t k, int s, int j, int c) {
+    uint64_t h = splitmix64(seed + (uint64_t)k);
+    h = splitmix64(h + (uint64_t)s);
+    h = splitmix64(h + (uint64_t)j);
+    return splitmix64(h + (uint64_t)c);
+}
+static void repair_normal3(uint64_t key, double z[3]) {
+    uint64_t ctr = 0;
+    double d;
+    gauss_pair(key, &ctr, &z[0], &z[1]);
+    gauss_pair(key, &ctr, &z[2], &d);
+}
+
+/* Q of vertex k of tet t on side s, with point j's side-s offset replaced by o3 (if j >= 0) */
+static int tet_side_coords(const orc_problem *P, const float *off, int t, int s, int j,
+                           const float o3[3], int64_t Q[4][3]) {
+    int ok = 1;
+    for (int k = 0; k < 4; k++) {
+        int v = P->tets[4 * t + k];
+        for (int a = 0; a < 3; a++) {
+            float o = (v == j) ? o3[a] : off[6 * v + 3 * s + a];
+            Q[k][a] = canon(P->base[3 * v + a], o);
+        }
+        if (!in_window(Q[k])) ok = 0;
+    }
+    return ok;
+}
+
+/* O2 severity of tet t on side s (0 when its sign matches the reference) */
+static double side_severity(const orc_problem *P, const int64_t Q[4][3], int t) {
+    i128 d = det4(Q);
+    if (sgn128(d) == P->ref[t]) return 0.0;
+    return (double)(d < 0 ? -d : d) / (6.0 * 1073741824.0) * P->sp[0] * P->sp[1] * P->sp[2];
+}
+
+/* P6: constraint score of point j on side s with j's offset o3: (number of folded
+ * incident tets, their summed severity), compared lexicographically; a vertex
+ * leaving the Q.10 window scores (INT_MAX, +inf) */
+typedef struct { int32_t folds; double sev; } repair_score;
+static repair_score incident_score(const orc_problem *P, const float *off, int s, int j, const float o3[3]) {
+    repair_score r = {0, 0.0};
+    for (int32_t u = P->inc_off[j]; u < P->inc_off[j + 1]; u++) {
+        int t = P->inc[u];
+        int64_t Q[4][3];
+        if (!tet_side_coords(P, off, t, s, j, o3, Q)) {
+            r.folds = 0x7fffffff;
+            r.sev = INFINITY;
+            return r;
+        }
+        if (sgn128(det4(Q)) != P->ref[t]) {
+            r.folds++;
+            r.sev += side_severity(P, Q, t);
+        }
+    }
+    return r;
+}
+static int score_less(repair_score a, repair_score b) {
+    return a.folds < b.folds || (a.folds == b.folds && a.sev < b.sev);
+}
+
+/* P4: sigma = 1/2 min over the incident tets (unfolded ones, else all) of the distance
+ * from j to the plane of its opposite face, |Delta| / (1024 |n|), voxel units; 1/2 if none */
+static double repair_sigma(const orc_problem *P, const float *off, int s, int j) {
+    double best[2] = {INFINITY, INFINITY}; /* [unfolded only, all] */
+    for (int32_t u = P->inc_off[j]; u < P->inc_off[j + 1]; u++) {
+        int t = P->inc[u];
+        int64_t Q[4][3];
+        if (!tet_side_coords(P, off, t, s, -1, NULL, Q)) continue;
+        int kj = 0;
+        for (int k = 0; k < 4; k++)
+            if (P->tets[4 * t + k] == j) kj = k;
+        int f[3], m = 0;
+        for (int k = 0; k < 4; k++)
+            if (k != kj) f[m++] = k;
+        double e1[3], e2[3];
+        for (int a = 0; a < 3; a++) {
+            e1[a] = (double)(Q[f[1]][a] - Q[f[0]][a]);
+            e2[a] = (double)(Q[f[2]][a] - Q[f[0]][a]);
+        }
+        double n0 = e1[1] * e2[2] - e1[2] * e2[1];
+        double n1 = e1[2] * e2[0] - e1[0] * e2[2];
+        double n2 = e1[0] * e2[1] - e1[1] * e2[0];
+        double nn = sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+        if (!(nn > 0.0)) continue;
+        i128 d = det4(Q);
+        double dist = (double)(int64_t)(d < 0 ? -d : d) / (nn * 1024.0);
+        if (dist < best[1]) best[1] = dist;
+        if (sgn128(d) == P->ref[t] && dist < best[0]) best[0] = dist;
+    }
+    double b = best[0] < INFINITY ? best[0] : best[1];
+    return b < INFINITY ? 0.5 * b : 0.5;
+}
+
+/* P1-P8 for one solution (index k for the generator); offsets updated in place.
+ * fixed: NULL or N*3 flags of axes the repair must not move (P8, e.g. hull points
+ * constrained to their boundary planes, fixed corners); they apply to both sides. */
+int orc_repair(orc_problem *P, float *off, const uint8_t *fixed, uint64_t seed, int64_t k,
+               int32_t *moved, int32_t *aborted) {
+    *moved = *aborted = 0;
+    char *pts = (char *)malloc(P->N);
+    for (int s = 0; s < 2; s++) {
+        /* P1/P2: vertices of the tets folded on side s at the start of the pass */
+        memset(pts, 0, P->N);
+        for (int t = 0; t < P->T; t++) {
+            int64_t Q[4][3];
+            if (!tet_side_coords(P, off, t, s, -1, NULL, Q)) continue;
+            if (sgn128(det4(Q)) != P->ref[t])
+                for (int v = 0; v < 4; v++) pts[P->tets[4 * t + v]] = 1;
+        }
+        for (int j = 0; j < P->N; j++) {
+            if (!pts[j]) continue;
+            float cur[3];
+            for (int a = 0; a < 3; a++) cur[a] = off[6 * j + 3 * s + a];
+            repair_score s0 = incident_score(P, off, s, j, cur);
+            /* P3: no folded incident tet left (earlier moves fixed them): nothing to do */
+            if (s0.folds == 0) continue;
+            double sigma = repair_sigma(P, off, s, j);
+            repair_score best = {0x7fffffff, INFINITY};
+            int best_c = -1;
+            float best_o[3] = {0, 0, 0};
+            for (int c = 0; c < REPAIR_CANDIDATES; c++) {
+                double z[3];
+                repair_normal3(repair_key(seed, k, s, j, c), z);
+                float o3[3];
+                for (int a = 0; a < 3; a++)
+                    o3[a] = (fixed && fixed[3 * j + a]) ? cur[a] : (float)((double)cur[a] + sigma * z[a]);
+                repair_score sc = incident_score(P, off, s, j, o3);
+                if (score_less(sc, best)) { /* strict: the lowest index wins ties */
+                    best = sc;
+                    best_c = c;
+                    for (int a = 0; a < 3; a++) best_o[a] = o3[a];
+                }
+            }
+            /* P7: apply the best candidate if it strictly improves, else abort the point */
+            if (best_c >= 0 && score_less(best, s0)) {
+                for (int a = 0; a < 3; a++) off[6 * j + 3 * s + a] = best_o[a];
+                (*moved)++;
+            } else {
+                (*aborted)++;
+            }
+        }
+    }
+    free(pts);
+    return 0;
 }
 
 /* per-tet contributions (both sides) for one solution */
@@ -1045,6 +1224,18 @@ void orc_sobol_point(uint64_t k, uint32_t *x4) {
     sobol_point(k, x4);
 }
 double orc_neg_log(uint32_t x) { return neg_log(x); }
+double orc_det_ln(double r) { return det_ln(r); }
+/* n standard normals in consecutive pairs from one key (P5 generator) */
+void orc_gauss(uint64_t key, int n, double *out) {
+    uint64_t ctr = 0;
+    for (int i = 0; i + 1 < n + 1; i += 2) {
+        double a, b;
+        gauss_pair(key, &ctr, &a, &b);
+        out[i] = a;
+        if (i + 1 < n) out[i + 1] = b;
+    }
+}
+double orc_repair_sigma(orc_problem *P, const float *off, int s, int j) { return repair_sigma(P, off, s, j); }
 uint64_t orc_fnv1a64(const unsigned char *b, int64_t n) { return fnv1a64(b, (size_t)n); }
 uint64_t orc_splitmix64(uint64_t z) { return splitmix64(z); }
 uint64_t orc_tet_seed(const int64_t *Q12, uint32_t *mask4) {

@@ -86,6 +86,12 @@ def lib():
         L.orc_tet_seed.restype = ctypes.c_uint64
         L.orc_tet_seed.argtypes = [vp, vp]
         L.orc_sobol_debug.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp]
+        L.orc_det_ln.restype = ctypes.c_double
+        L.orc_det_ln.argtypes = [ctypes.c_double]
+        L.orc_gauss.argtypes = [ctypes.c_uint64, ctypes.c_int, vp]
+        L.orc_repair.argtypes = [vp, vp, vp, ctypes.c_uint64, ctypes.c_int64, vp, vp]
+        L.orc_repair_sigma.restype = ctypes.c_double
+        L.orc_repair_sigma.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -206,6 +212,20 @@ class Oracle:
     def ref_sign(self, t):
         return lib().orc_ref_sign(self.h, int(t))
 
+    def repair(self, offsets_one, seed, k, fixed=None):
+        """NEXT-2 fold repair (P1-P8) of one solution (generator index k); fixed: None or
+        N x 3 bools of axes that must not move.  Returns (offsets, moved, aborted)."""
+        o = np.array(self._off(offsets_one), copy=True)
+        fx = None if fixed is None else np.ascontiguousarray(fixed, dtype=np.uint8).reshape(-1, 3)
+        mv, ab = ctypes.c_int32(0), ctypes.c_int32(0)
+        lib().orc_repair(self.h, _p(o), _p(fx), ctypes.c_uint64(seed % 2 ** 64), int(k),
+                         ctypes.byref(mv), ctypes.byref(ab))
+        return o, mv.value, ab.value
+
+    def repair_sigma(self, offsets_one, side, j):
+        o = self._off(offsets_one)
+        return lib().orc_repair_sigma(self.h, _p(o), int(side), int(j))
+
     def set_sampler(self, mode, rate=1.0):
         """0: exactly-once voxel centres (O3); 1: Sobol points per tet (NEXT-1, S1-S9)."""
         if lib().orc_set_sampler(self.h, int(mode), float(rate)) != 0:
@@ -253,6 +273,16 @@ def sobol_points(n):
 
 def neg_log(x):
     return lib().orc_neg_log(int(x))
+
+
+def det_ln(r):
+    return lib().orc_det_ln(float(r))
+
+
+def gauss(key, n):
+    out = np.zeros(n)
+    lib().orc_gauss(ctypes.c_uint64(key % 2 ** 64), int(n), _p(out))
+    return out
 
 
 def fnv1a64(b: bytes):
