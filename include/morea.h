@@ -188,6 +188,28 @@ int morea_eval_partial(morea_ctx *ctx, int pop, const float *base_offsets,
  * Errors: EINVAL (bad mode / rate), ESTATE (before morea_create finished). */
 int morea_set_sampler(morea_ctx *ctx, int mode, double rate);
 
+/* Fold repair (§4.3.1): "For each
+ * point in a folded tetrahedron, the method mutates the point using a Gaussian
+ * distribution scaled by its estimated distance to the surrounding 3D polygon.
+ * After 64 samples, the change with the best constraint improvement is
+ * selected, if present.  If all samples result in a deterioration, repair is
+ * aborted."  Per solution k, side s in {source, target}: the vertices of the
+ * tets folded on s at the start of the pass, ascending; each gets 64 candidates
+ * o' = o + sigma z (z ~ N(0, I3) from SplitMix64 keys of (seed, sol_base + k, s,
+ * point, candidate), Marsaglia's polar method); sigma = 1/2 min distance (voxels)
+ * to the opposite-face planes of its incident unfolded tets; a candidate scores
+ * (folded incident tets, their severity) lexicographically; the best one is
+ * applied iff it is strictly better, else the point is "aborted".  Readings
+ * P1..P8 in DESIGN.md §3.  Deterministic for a given seed and sol_base.
+ *  offsets: pop*N*6, updated in place (host or device).
+ *  fixed: NULL or N*3 uint8, axes the repair must not move (both sides), e.g.
+ *    hull points kept on their boundary planes.
+ *  moved / aborted: NULL or pop int32: points moved / points without an
+ *    improving candidate.
+ * Re-run morea_check_folds for the remaining folds. */
+int morea_repair(morea_ctx *ctx, int pop, float *offsets, const uint8_t *fixed, uint64_t seed,
+                 int64_t sol_base, int32_t *moved, int32_t *aborted);
+
 /* The dependent tets of the plan of the last morea_eval_partial call: writes
  * up to `cap` tet ids (group order, ascending within a group) into `tets` (host)
  * and the n_groups+1 offsets into `dep_off` (host).  Returns ND (>= 0). */

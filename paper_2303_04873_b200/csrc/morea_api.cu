@@ -75,6 +75,8 @@ struct morea_ctx {
   int sampler = MOREA_SAMPLER_VOXEL;
   double rate = 1.0;
   DevBuf dil, sobolv;
+  // fold repair (NEXT-2): device incidence CSR, staging
+  DevBuf d_inc_off, d_inc, st_fixed, st_rep;
   int blocks_per_sm_sobol = 1, blocks_per_sm_sobol_tex = 1;
   // texture-gather copies (tall 2D arrays) of I_s, I_t and the maps
   bool use_tex = false;
@@ -572,7 +574,7 @@ void morea_destroy(morea_ctx* ctx) {
     cudaEventDestroy(p.second);
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
-                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->dil, &ctx->sobolv, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
+                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
                     &ctx->full_sched, &ctx->full_group_off, &ctx->geom, &ctx->scal, &ctx->hgn,
                     &ctx->counter, &ctx->stats, &ctx->st_off, &ctx->st_nv, &ctx->st_cache_in,
                     &ctx->st_base_acc, &ctx->st_obj, &ctx->st_acc, &ctx->st_cache_out,
@@ -738,6 +740,13 @@ int morea_set_mesh(morea_ctx* ctx, int n_points, const float* base_xyz, int n_te
   ctx->h_tets = t;
   ctx->inc_off = inc_off;
   ctx->inc = inc;
+  CK(ctx->d_inc_off.ensure(inc_off.size() * sizeof(int32_t)));
+  CK(ctx->d_inc.ensure(std::max<size_t>(1, inc.size()) * sizeof(int32_t)));
+  CK(cudaMemcpyAsync(ctx->d_inc_off.p, inc_off.data(), inc_off.size() * sizeof(int32_t),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  if (!inc.empty())
+    CK(cudaMemcpyAsync(ctx->d_inc.p, inc.data(), inc.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                       ctx->stream));
   ctx->tet_size = size;
   std::vector<int> order(n_tets);
   std::iota(order.begin(), order.end(), 0);
@@ -900,6 +909,29 @@ int morea_set_sampler(morea_ctx* ctx, int mode, double rate) {
   ctx->sampler = mode;
   ctx->rate = rate;
   CK(ensure_dil(ctx));
+  return MOREA_OK;
+}
+
+int morea_repair(morea_ctx* ctx, int pop, float* offsets, const uint8_t* fixed, uint64_t seed,
+                 int64_t sol_base, int32_t* moved, int32_t* aborted) {
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  if (pop < 0 || (pop > 0 && !offsets) || sol_base < 0) return fail(ctx, MOREA_EINVAL, "bad pop / offsets");
+  if (pop == 0) return MOREA_OK;
+  const size_t bytes = (size_t)pop * ctx->N * 6 * sizeof(float);
+  OutView ov[3];
+  CK(out_dev(offsets, bytes, ctx->st_rep, ov[0]));
+  if (ov[0].copy)  // in/out: bring the host offsets over first
+    CK(cudaMemcpyAsync(ov[0].dev, offsets, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  const unsigned char* fx = nullptr;
+  CK(in_dev(ctx, fixed, (size_t)ctx->N * 3, ctx->st_fixed, (const void**)&fx));
+  CK(out_dev(moved, (size_t)pop * sizeof(int32_t), ctx->st_i32, ov[1]));
+  CK(out_dev(aborted, (size_t)pop * sizeof(int32_t), ctx->st_u8, ov[2]));
+  CK(launch_repair(mesh_of(ctx), ctx->sp, pop, sol_base, (float*)ov[0].dev, fx, ctx->d_inc_off.as<int>(),
+                   ctx->d_inc.as<int>(), seed, (int*)ov[1].dev, (int*)ov[2].dev, ctx->stream));
+  ctx->kernels++;
+  CK(finish_outputs(ctx, ov, 3));
   return MOREA_OK;
 }
 

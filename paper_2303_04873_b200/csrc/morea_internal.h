@@ -153,6 +153,9 @@ cudaError_t launch_raster(const EvalArgs& a, int grid, cudaStream_t s);
 int raster_blocks_per_sm(bool tex);
 cudaError_t launch_sobol(const EvalArgs& a, int grid, cudaStream_t s);
 int sobol_blocks_per_sm(bool tex);
+cudaError_t launch_repair(const MeshDev& m, const double sp[3], int P, long long sol_base, float* offsets,
+                          const unsigned char* fixed, const int* inc_off, const int* inc,
+                          unsigned long long seed, int* moved, int* aborted, cudaStream_t s);
 cudaError_t launch_dilate_band(const unsigned char* band, int nx, int ny, int nz, unsigned char* dil,
                                cudaStream_t s);
 cudaError_t launch_reduce(const EvalArgs& a, int G, const int* group_off, const void* base_acc,

@@ -1263,6 +1263,8 @@ cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, un
   return cudaGetLastError();
 }
 
+#include "morea_repair.cuh"
+
 }  // namespace morea
 
 #include "morea_sobol.cuh"

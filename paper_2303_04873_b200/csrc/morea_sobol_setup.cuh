@@ -32,11 +32,12 @@ __device__ __forceinline__ unsigned long long sb_seed(const int Q[4][3]) {
   return h;
 }
 
-// S5: -log((x + 1/2) 2^-32) by the fixed operation sequence both implementations
-// use (frexp, one division, degree-23 odd series, split ln 2); explicit _rn
-// intrinsics so that nothing is contracted into an FMA.
-__device__ __noinline__ double sb_neg_log(unsigned x) {
-  const double r = __dmul_rn(__dadd_rn((double)x, 0.5), 2.3283064365386963e-10);
+// S5: log r (r > 0) by the fixed operation sequence both implementations use
+// (frexp, one division, degree-23 odd series, split ln 2); explicit _rn
+// intrinsics so that nothing is contracted into an FMA.  -log((x + 1/2) 2^-32)
+// is the Sobol sampler's exponential variate; the repair's Gaussian draws use
+// the same routine.
+__device__ __noinline__ double sb_det_ln(double r) {
   int e;
   double m = frexp(r, &e);
   if (m < 0.70710678118654752440) {
@@ -52,9 +53,12 @@ __device__ __noinline__ double sb_neg_log(unsigned x) {
   for (int i = 1; i < 12; i++) p = __dadd_rn(__dmul_rn(p, t2), c[i]);
   const double lm = __dmul_rn(__dmul_rn(2.0, t), p);
   const double de = (double)e;
-  const double lr = __dadd_rn(__dmul_rn(de, 6.93147180369123816490e-01),
-                              __dadd_rn(__dmul_rn(de, 1.90821492927058770002e-10), lm));
-  return -lr;
+  return __dadd_rn(__dmul_rn(de, 6.93147180369123816490e-01),
+                   __dadd_rn(__dmul_rn(de, 1.90821492927058770002e-10), lm));
+}
+
+__device__ __forceinline__ double sb_neg_log(unsigned x) {
+  return -sb_det_ln(__dmul_rn(__dadd_rn((double)x, 0.5), 2.3283064365386963e-10));
 }
 
 // ---------------------------------------------------------------------------

@@ -31,7 +31,7 @@ assert ACC_DTYPE.itemsize == 48
 EXPORTS = ["morea_create", "morea_destroy", "morea_last_error", "morea_stream", "morea_load_images",
            "morea_set_mesh", "morea_eval_full", "morea_eval_partial", "morea_partial_deps",
            "morea_check_folds", "morea_owner_map", "morea_distance_map", "morea_prof_enable",
-           "morea_prof_read", "morea_kernel_launches", "morea_set_sampler"]
+           "morea_prof_read", "morea_kernel_launches", "morea_set_sampler", "morea_repair"]
 SAMPLER_VOXEL = 0
 SAMPLER_SOBOL = 1
 
@@ -65,6 +65,7 @@ def _load():
     L.morea_distance_map.argtypes = [vp, i32, i32, vp]
     L.morea_prof_enable.argtypes = [vp, i32]
     L.morea_set_sampler.argtypes = [vp, i32, f64]
+    L.morea_repair.argtypes = [vp, i32, vp, vp, ctypes.c_uint64, i64, vp, vp]
     L.morea_kernel_launches.argtypes = [vp]
     L.morea_kernel_launches.restype = i64
     L.morea_prof_read.argtypes = [vp] + [ctypes.POINTER(i64), ctypes.POINTER(f64)] + \
@@ -215,6 +216,17 @@ class Context:
             out = np.empty(self.V, np.float32)
         self._check(_lib.morea_distance_map(self.h, int(side), int(pair), _ptr(out)))
         return out
+
+    def repair(self, offsets, seed, fixed=None, sol_base=0, moved=None, aborted=None):
+        """Fold repair (§4.3.1) of `offsets` (P x N x 6, torch CUDA or numpy,
+        updated in place); fixed: None or N x 3 axes that must not move."""
+        P = int(offsets.shape[0])
+        fx = None if fixed is None else (fixed if _is_torch(fixed) else _np(fixed, np.uint8))
+        if not _is_torch(offsets):
+            assert offsets.dtype == np.float32 and offsets.flags["C_CONTIGUOUS"]
+        self._check(_lib.morea_repair(self.h, P, _ptr(offsets), _ptr(fx), ctypes.c_uint64(int(seed) % 2 ** 64),
+                                      int(sol_base), _ptr(moved), _ptr(aborted)))
+        return offsets
 
     def set_sampler(self, mode, rate=1.0):
         """SAMPLER_VOXEL (exactly-once voxel centres) or SAMPLER_SOBOL (App. A.2
