@@ -298,6 +298,10 @@ def main():
     ctx.set_sampler(morea.SAMPLER_SOBOL, 1.0)
     t_sobol = timed(lambda: ctx.eval_full(off_d, obj_d, acc_d, None))
     ctx.set_sampler(morea.SAMPLER_VOXEL)
+    # NEXT-2: fold repair of the whole population (on a copy of the offsets)
+    rep_off = off_d.clone()
+    fixed_d = torch.from_numpy(w.fixed_axes.astype("uint8")).to(dev)
+    t_repair = timed(lambda: ctx.repair(rep_off.copy_(off_d), 2024, fixed_d, s0), reps=1)
 
     # ---- roofline of the dominant kernel (k_raster), SURVEY.md §8(d) algorithmic bytes
     peak, peak_src = measured_hbm_peak()
@@ -375,6 +379,7 @@ def main():
                 "partial_nocache_evals_per_s": P * G * 1e3 / t_part_nc,
                 "sobol_full_evals_per_s": P * 1e3 / t_sobol,
                 "sobol_full_ms": t_sobol,
+                "repair_population_ms": t_repair,
                 "samples_per_launch": prof["samples"] / max(prof["launches"], 1),
                 "band_entries_per_launch": prof["band_entries"] / max(prof["launches"], 1),
                 "per_gpu_note": "breakdown figures are this rank's (per GPU)",

@@ -50,7 +50,7 @@ def test_repair_bitexact_workload(wl, idx):
     w = wl(idx)
     ctx = _ctx(w)
     orc = Oracle.from_workload(w)
-    offs = w.offsets if idx == 1 else _heavy(w, 0.8, 3)[:24]
+    offs = w.offsets if idx == 1 else _heavy(w, 5.0, 3)[:24]
     new, mv, ab = _gpu_repair(ctx, offs, w.fixed_axes)
     n_moved = 0
     for k in range(offs.shape[0]):
@@ -64,7 +64,7 @@ def test_repair_bitexact_workload(wl, idx):
 def test_repair_reduces_folds_and_sharding(wl):
     w = wl(2)
     ctx = _ctx(w)
-    offs = _heavy(w, 1.0, 5)[:32]
+    offs = _heavy(w, 5.0, 5)[:32]
     new, mv, ab = _gpu_repair(ctx, offs, w.fixed_axes)
     # sol_base keys the generator by global solution index: a shard reproduces its rows
     part, mv2, ab2 = _gpu_repair(ctx, offs[8:16], w.fixed_axes, sol_base=8)
