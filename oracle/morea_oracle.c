@@ -24,7 +24,8 @@
  *   f_magnitude, 10 edges incl. 4 spokes     §4.1.1 eq. L251-259              (O9)
  *   partial evaluation (delta on dependents) §1, §4.2.1 L400-410        (O10)
  *   Sobol-in-tetrahedron sampler (NEXT-1)    App. A.2 L744-751                (S1..S9)
- *   batched fold repair (NEXT-2)             §4.3.1 L429-437                  (P1..P7)
+ *   batched fold repair (NEXT-2)             §4.3.1 L429-437                  (P1..P8)
+ *   elasticity from masks, DVF (NEXT-4)      App. A.1, §5.4 L616     (E1..E3)
  *
  * Everything that decides an integer (ownership, fold, the h case split, band
  * membership) is decided exactly in integer arithmetic (int64 / __int128) or
@@ -1157,6 +1158,110 @@ int orc_owner_map(orc_problem *P, const float *offsets_one, int side, int32_t *o
         if (!tet_coords(P, offsets_one, t, Q)) continue;
         tet_side_samples(P, side, Q, NULL, NULL, NULL, owner, t);
     }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* NEXT-4: rasterizer reuse (App. A.1; §5.4).  Readings    */
+/* E1..E3.                                                   */
+/* ------------------------------------------------------------------ */
+/* E1: label of a voxel from an object bitmask byte: 1 + index of the lowest set
+ * bit below M (objects in priority order), 0 = no object */
+static int voxel_label(uint8_t m, int M) {
+    for (int b = 0; b < M; b++)
+        if ((m >> b) & 1) return b + 1;
+    return 0;
+}
+
+/* E1: per tet, the number of owned voxel centres (O3) of each label on side s;
+ * counts: T*(M+1), offsets NULL = the base mesh */
+int orc_label_counts(orc_problem *P, const float *offsets_one, int s, const uint8_t *masks, int M,
+                     int64_t *counts) {
+    if (M < 0 || M > 8) return -1;
+    memset(counts, 0, sizeof(int64_t) * (size_t)P->T * (M + 1));
+    for (int t = 0; t < P->T; t++) {
+        int64_t Q[2][4][3];
+        if (!tet_coords(P, offsets_one, t, Q)) continue;
+        tet_faces F;
+        if (!make_faces(Q[s], &F)) continue;
+        int64_t lo[3], hi[3];
+        tet_bbox(P, Q[s], lo, hi);
+        for (int64_t z = lo[2]; z <= hi[2]; z++)
+            for (int64_t y = lo[1]; y <= hi[1]; y++)
+                for (int64_t x = lo[0]; x <= hi[0]; x++) {
+                    int64_t q[3] = {x, y, z};
+                    i128 e[4];
+                    if (!owns(&F, q, e)) continue;
+                    counts[(int64_t)t * (M + 1) + voxel_label(masks[vidx(P, x, y, z)], M)]++;
+                }
+    }
+    return 0;
+}
+
+/* E2: c_delta = mean over the tet's owned source voxels (base mesh) of the factor of
+ * their label (1.0 for no object): = sum_m frac_m f_m + (1 - sum_m frac_m) 1.0
+ * (App. A.1); 1.0 for a tet that owns no voxel */
+int orc_elasticity(orc_problem *P, const uint8_t *masks, int M, const float *factors, float *c_out) {
+    int64_t *cnt = (int64_t *)malloc(sizeof(int64_t) * (size_t)P->T * (M + 1));
+    int rc = orc_label_counts(P, NULL, 0, masks, M, cnt);
+    if (rc) { free(cnt); return rc; }
+    for (int t = 0; t < P->T; t++) {
+        int64_t tot = 0;
+        double acc = 0.0;
+        for (int b = 0; b <= M; b++) {
+            int64_t c = cnt[(int64_t)t * (M + 1) + b];
+            tot += c;
+            acc += (double)c * (b == 0 ? 1.0 : (double)factors[b - 1]);
+        }
+        c_out[t] = tot > 0 ? (float)(acc / (double)tot) : 1.0f;
+    }
+    free(cnt);
+    return 0;
+}
+
+/* E3: deformation vector field of side s: at every voxel centre q owned on side s,
+ * T(q) - q in mm (O4 transform, exact numerator, one fp64 rounding, then x spacing,
+ * rounded to fp32); the owner is the lowest tet id when a fold makes several;
+ * uncovered voxels get 0 and cov = 0 */
+int orc_dvf(orc_problem *P, const float *offsets_one, int s, float *dvf, uint8_t *cov) {
+    int32_t *own = (int32_t *)malloc(sizeof(int32_t) * P->V);
+    for (int64_t v = 0; v < P->V; v++) own[v] = -1;
+    memset(dvf, 0, sizeof(float) * 3 * P->V);
+    if (cov) memset(cov, 0, P->V);
+    for (int pass = 0; pass < 2; pass++)
+        for (int t = 0; t < P->T; t++) {
+            int64_t Q[2][4][3];
+            if (!tet_coords(P, offsets_one, t, Q)) continue;
+            tet_faces F;
+            if (!make_faces(Q[s], &F)) continue;
+            int so = 1 - s;
+            i128 U[4][3];
+            for (int k = 0; k < 4; k++)
+                for (int a = 0; a < 3; a++) U[k][a] = (i128)(Q[so][k][a] - Q[s][k][a]);
+            int64_t lo[3], hi[3];
+            tet_bbox(P, Q[s], lo, hi);
+            for (int64_t z = lo[2]; z <= hi[2]; z++)
+                for (int64_t y = lo[1]; y <= hi[1]; y++)
+                    for (int64_t x = lo[0]; x <= hi[0]; x++) {
+                        int64_t q[3] = {x, y, z};
+                        i128 e[4];
+                        if (!owns(&F, q, e)) continue;
+                        int64_t v = vidx(P, x, y, z);
+                        if (pass == 0) {
+                            if (own[v] == -1 || t < own[v]) own[v] = t;
+                            continue;
+                        }
+                        if (own[v] != t) continue;
+                        for (int a = 0; a < 3; a++) {
+                            i128 Nn = 0;
+                            for (int k = 0; k < 4; k++) Nn += e[k] * U[k][a];
+                            double u = (double)Nn / ((double)F.absdet * 1024.0);
+                            dvf[3 * v + a] = (float)(u * P->sp[a]);
+                        }
+                        if (cov) cov[v] = 1;
+                    }
+        }
+    free(own);
     return 0;
 }
 

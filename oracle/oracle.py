@@ -86,6 +86,9 @@ def lib():
         L.orc_tet_seed.restype = ctypes.c_uint64
         L.orc_tet_seed.argtypes = [vp, vp]
         L.orc_sobol_debug.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp]
+        L.orc_label_counts.argtypes = [vp, vp, ctypes.c_int, vp, ctypes.c_int, vp]
+        L.orc_elasticity.argtypes = [vp, vp, ctypes.c_int, vp, vp]
+        L.orc_dvf.argtypes = [vp, vp, ctypes.c_int, vp, vp]
         L.orc_det_ln.restype = ctypes.c_double
         L.orc_det_ln.argtypes = [ctypes.c_double]
         L.orc_gauss.argtypes = [ctypes.c_uint64, ctypes.c_int, vp]
@@ -211,6 +214,32 @@ class Oracle:
 
     def ref_sign(self, t):
         return lib().orc_ref_sign(self.h, int(t))
+
+    def label_counts(self, offsets_one, side, masks, M):
+        """NEXT-4 (E1): per tet, owned voxel counts per label (T x (M+1))."""
+        o = None if offsets_one is None else self._off(offsets_one)
+        m = np.ascontiguousarray(masks, dtype=np.uint8).reshape(-1)
+        out = np.zeros((self.T, M + 1), dtype=np.int64)
+        if lib().orc_label_counts(self.h, _p(o), int(side), _p(m), int(M), _p(out)) != 0:
+            raise ValueError("bad M")
+        return out
+
+    def elasticity(self, masks, factors):
+        """NEXT-4 (E2): c_delta per tet from object masks (bit m = object m) and factors."""
+        f = np.ascontiguousarray(factors, dtype=np.float32)
+        m = np.ascontiguousarray(masks, dtype=np.uint8).reshape(-1)
+        out = np.zeros(self.T, dtype=np.float32)
+        if lib().orc_elasticity(self.h, _p(m), len(f), _p(f), _p(out)) != 0:
+            raise ValueError("bad M")
+        return out
+
+    def dvf(self, offsets_one, side):
+        """NEXT-4 (E3): displacement field (V x 3, mm) and coverage (V) of one side."""
+        o = self._off(offsets_one)
+        d = np.zeros((self.V, 3), dtype=np.float32)
+        c = np.zeros(self.V, dtype=np.uint8)
+        lib().orc_dvf(self.h, _p(o), int(side), _p(d), _p(c))
+        return d, c
 
     def repair(self, offsets_one, seed, k, fixed=None):
         """NEXT-2 fold repair (P1-P8) of one solution (generator index k); fixed: None or
