@@ -210,6 +210,30 @@ int morea_set_sampler(morea_ctx *ctx, int mode, double rate);
 int morea_repair(morea_ctx *ctx, int pop, float *offsets, const uint8_t *fixed, uint64_t seed,
                  int64_t sol_base, int32_t *moved, int32_t *aborted);
 
+/* Rasterizer reuse.
+ * Object counts per tet (App. A.1: "We compute the overlap
+ * that each object mask has with the tetrahedron ... which produces one fraction
+ * per object"): for the solution offsets_one (N*6; NULL = the base mesh), the
+ * voxel centres each tet owns on `side` (O3, exactly once) are counted per
+ * label: masks is a V byte volume (x-fastest), bit m = object m (m < M <= 8);
+ * a voxel's label is 1 + its lowest set bit (objects in priority order), 0 if
+ * none.  counts: T*(M+1) int64 (host or device).  Readings E1..E3. */
+int morea_label_counts(morea_ctx *ctx, const float *offsets_one, int side, const uint8_t *masks, int M,
+                       int64_t *counts);
+/* Elasticity factors (App. A.1: "These object fractions are multiplied
+ * by pre-determined elasticity factors ... yielding an overall element-specific
+ * factor"): c_delta[t] = sum_m frac_m factors[m] + (1 - sum_m frac_m) * 1.0 over
+ * the base mesh's source-side voxel centres (1.0 for a tet owning none).  Feed
+ * the result to morea_set_mesh.  c_delta: T floats, host or device. */
+int morea_elasticity(morea_ctx *ctx, const uint8_t *masks, int M, const float *factors, float *c_delta);
+/* Deformation vector field of one side (§5.4, "a forward and an inverse
+ * DVF"): at every voxel centre q owned on `side` by some tet, T(q) - q in mm
+ * (O4 with the exact numerator, bit-identical to the oracle; the lowest tet id
+ * wins where a fold gives several owners); 0 elsewhere.  side 0 = forward
+ * (source voxels), 1 = inverse.  dvf: V*3 float (x-fastest voxels, xyz per
+ * voxel); coverage: NULL or V bytes, 1 where owned. */
+int morea_dvf(morea_ctx *ctx, const float *offsets_one, int side, float *dvf, uint8_t *coverage);
+
 /* The dependent tets of the plan of the last morea_eval_partial call: writes
  * up to `cap` tet ids (group order, ascending within a group) into `tets` (host)
  * and the n_groups+1 offsets into `dep_off` (host).  Returns ND (>= 0). */

@@ -77,6 +77,8 @@ struct morea_ctx {
   DevBuf dil, sobolv;
   // fold repair (NEXT-2): device incidence CSR, staging
   DevBuf d_inc_off, d_inc, st_fixed, st_rep;
+  // rasterizer exports (NEXT-4)
+  DevBuf st_masks, st_counts, st_dvf, st_cov, scratch_owner, zero_off;
   int blocks_per_sm_sobol = 1, blocks_per_sm_sobol_tex = 1;
   // texture-gather copies (tall 2D arrays) of I_s, I_t and the maps
   bool use_tex = false;
@@ -574,7 +576,8 @@ void morea_destroy(morea_ctx* ctx) {
     cudaEventDestroy(p.second);
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
-                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
+                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->st_masks, &ctx->st_counts, &ctx->st_dvf, &ctx->st_cov,
+                    &ctx->scratch_owner, &ctx->zero_off, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
                     &ctx->full_sched, &ctx->full_group_off, &ctx->geom, &ctx->scal, &ctx->hgn,
                     &ctx->counter, &ctx->stats, &ctx->st_off, &ctx->st_nv, &ctx->st_cache_in,
                     &ctx->st_base_acc, &ctx->st_obj, &ctx->st_acc, &ctx->st_cache_out,
@@ -932,6 +935,98 @@ int morea_repair(morea_ctx* ctx, int pop, float* offsets, const uint8_t* fixed, 
                    ctx->d_inc.as<int>(), seed, (int*)ov[1].dev, (int*)ov[2].dev, ctx->stream));
   ctx->kernels++;
   CK(finish_outputs(ctx, ov, 3));
+  return MOREA_OK;
+}
+
+// one-solution geometry (voxel-centre mode) for the rasterizer exports
+static int export_args(morea_ctx* ctx, const float* offsets_one, EvalArgs& a) {
+  const float* off = nullptr;
+  if (offsets_one) {
+    CK(in_dev(ctx, offsets_one, (size_t)ctx->N * 6 * sizeof(float), ctx->st_off, (const void**)&off));
+  } else {
+    CK(ctx->zero_off.ensure((size_t)ctx->N * 6 * sizeof(float)));
+    CK(cudaMemsetAsync(ctx->zero_off.p, 0, (size_t)ctx->N * 6 * sizeof(float), ctx->stream));
+    off = ctx->zero_off.as<float>();
+  }
+  std::memset(&a, 0, sizeof(a));
+  a.vol = volumes_of(ctx);
+  a.mesh = mesh_of(ctx);
+  a.P = 1;
+  a.offsets = off;
+  a.n_entries = ctx->T;
+  a.sched = ctx->full_sched.as<int>();
+  a.n_setup_versions = 1;
+  a.n_raster_versions = 1;
+  a.expect[0] = a.expect[1] = -1;
+  CK(eval_scratch(ctx, a));
+  return MOREA_OK;
+}
+
+int morea_label_counts(morea_ctx* ctx, const float* offsets_one, int side, const uint8_t* masks, int M,
+                       int64_t* counts) {
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  if ((side != 0 && side != 1) || M < 0 || M > 8 || !masks || !counts)
+    return fail(ctx, MOREA_EINVAL, "bad side / M / buffers");
+  EvalArgs a;
+  rc = export_args(ctx, offsets_one, a);
+  if (rc) return rc;
+  const unsigned char* m = nullptr;
+  CK(in_dev(ctx, masks, (size_t)ctx->V, ctx->st_masks, (const void**)&m));
+  OutView ov[1];
+  CK(out_dev(counts, (size_t)ctx->T * (M + 1) * sizeof(int64_t), ctx->st_counts, ov[0]));
+  CK(launch_label_counts(a, side, m, M, (long long*)ov[0].dev, ctx->stream));
+  ctx->kernels += 2;
+  CK(finish_outputs(ctx, ov, 1));
+  return MOREA_OK;
+}
+
+int morea_elasticity(morea_ctx* ctx, const uint8_t* masks, int M, const float* factors, float* c_delta) {
+  if (!ctx) return MOREA_EINVAL;
+  if (M < 0 || M > 8 || (M > 0 && !factors) || !c_delta) return fail(ctx, MOREA_EINVAL, "bad M / buffers");
+  std::vector<int64_t> cnt((size_t)ctx->T * (M + 1));
+  int rc = morea_label_counts(ctx, nullptr, 0, masks, M, cnt.data());
+  if (rc) return rc;
+  std::vector<float> f;
+  CK(to_host(ctx, factors, (size_t)M, f));
+  std::vector<float> c(ctx->T);
+  for (int t = 0; t < ctx->T; t++) {  // E2, in the oracle's order
+    int64_t tot = 0;
+    double acc = 0.0;
+    for (int b = 0; b <= M; b++) {
+      const int64_t n = cnt[(size_t)t * (M + 1) + b];
+      tot += n;
+      acc += (double)n * (b == 0 ? 1.0 : (double)f[b - 1]);
+    }
+    c[t] = tot > 0 ? (float)(acc / (double)tot) : 1.0f;
+  }
+  if (is_device_ptr(c_delta)) {
+    CK(cudaMemcpyAsync(c_delta, c.data(), c.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  } else {
+    std::memcpy(c_delta, c.data(), c.size() * sizeof(float));
+  }
+  return MOREA_OK;
+}
+
+int morea_dvf(morea_ctx* ctx, const float* offsets_one, int side, float* dvf, uint8_t* coverage) {
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  if ((side != 0 && side != 1) || !dvf) return fail(ctx, MOREA_EINVAL, "bad side / buffers");
+  EvalArgs a;
+  rc = export_args(ctx, offsets_one, a);
+  if (rc) return rc;
+  OutView ov[2];
+  CK(out_dev(dvf, (size_t)ctx->V * 3 * sizeof(float), ctx->st_dvf, ov[0]));
+  CK(ctx->st_cov.ensure((size_t)ctx->V));
+  CK(out_dev(coverage, (size_t)ctx->V, ctx->st_cov, ov[1]));
+  unsigned char* cov = ov[1].dev ? (unsigned char*)ov[1].dev : ctx->st_cov.as<unsigned char>();
+  CK(ctx->scratch_owner.ensure((size_t)ctx->V * sizeof(int)));
+  CK(launch_dvf(a, side, ctx->scratch_owner.as<int>(), (float*)ov[0].dev, cov, ctx->stream));
+  ctx->kernels += 4;
+  CK(finish_outputs(ctx, ov, 2));
   return MOREA_OK;
 }
 

@@ -156,6 +156,10 @@ int sobol_blocks_per_sm(bool tex);
 cudaError_t launch_repair(const MeshDev& m, const double sp[3], int P, long long sol_base, float* offsets,
                           const unsigned char* fixed, const int* inc_off, const int* inc,
                           unsigned long long seed, int* moved, int* aborted, cudaStream_t s);
+cudaError_t launch_label_counts(const EvalArgs& a, int side, const unsigned char* masks, int M,
+                                long long* counts, cudaStream_t s);
+cudaError_t launch_dvf(const EvalArgs& a, int side, int* owner, float* dvf, unsigned char* cov,
+                       cudaStream_t s);
 cudaError_t launch_dilate_band(const unsigned char* band, int nx, int ny, int nz, unsigned char* dil,
                                cudaStream_t s);
 cudaError_t launch_reduce(const EvalArgs& a, int G, const int* group_off, const void* base_acc,

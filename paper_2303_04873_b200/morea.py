@@ -31,7 +31,7 @@ assert ACC_DTYPE.itemsize == 48
 EXPORTS = ["morea_create", "morea_destroy", "morea_last_error", "morea_stream", "morea_load_images",
            "morea_set_mesh", "morea_eval_full", "morea_eval_partial", "morea_partial_deps",
            "morea_check_folds", "morea_owner_map", "morea_distance_map", "morea_prof_enable",
-           "morea_prof_read", "morea_kernel_launches", "morea_set_sampler", "morea_repair"]
+           "morea_prof_read", "morea_kernel_launches", "morea_set_sampler", "morea_repair", "morea_label_counts", "morea_elasticity", "morea_dvf"]
 SAMPLER_VOXEL = 0
 SAMPLER_SOBOL = 1
 
@@ -66,6 +66,9 @@ def _load():
     L.morea_prof_enable.argtypes = [vp, i32]
     L.morea_set_sampler.argtypes = [vp, i32, f64]
     L.morea_repair.argtypes = [vp, i32, vp, vp, ctypes.c_uint64, i64, vp, vp]
+    L.morea_label_counts.argtypes = [vp, vp, i32, vp, i32, vp]
+    L.morea_elasticity.argtypes = [vp, vp, i32, vp, vp]
+    L.morea_dvf.argtypes = [vp, vp, i32, vp, vp]
     L.morea_kernel_launches.argtypes = [vp]
     L.morea_kernel_launches.restype = i64
     L.morea_prof_read.argtypes = [vp] + [ctypes.POINTER(i64), ctypes.POINTER(f64)] + \
@@ -227,6 +230,33 @@ class Context:
         self._check(_lib.morea_repair(self.h, P, _ptr(offsets), _ptr(fx), ctypes.c_uint64(int(seed) % 2 ** 64),
                                       int(sol_base), _ptr(moved), _ptr(aborted)))
         return offsets
+
+    def label_counts(self, offsets_one, side, masks, M, counts=None):
+        """Owned voxel counts per tet and object label (T x (M+1) int64)."""
+        if counts is None:
+            counts = np.zeros((self.T, M + 1), np.int64)
+        o = None if offsets_one is None else (offsets_one if _is_torch(offsets_one) else _np(offsets_one, np.float32))
+        m = masks if _is_torch(masks) else _np(masks, np.uint8)
+        self._check(_lib.morea_label_counts(self.h, _ptr(o), int(side), _ptr(m), int(M), _ptr(counts)))
+        return counts
+
+    def elasticity(self, masks, factors):
+        """c_delta per tet from object masks (bit m = object m) and their factors."""
+        f = _np(factors, np.float32)
+        m = masks if _is_torch(masks) else _np(masks, np.uint8)
+        out = np.zeros(self.T, np.float32)
+        self._check(_lib.morea_elasticity(self.h, _ptr(m), len(f), _ptr(f), _ptr(out)))
+        return out
+
+    def dvf(self, offsets_one, side, dvf=None, coverage=None):
+        """T(q) - q (mm) at the voxel centres owned on `side` (V x 3) and coverage (V)."""
+        if dvf is None:
+            dvf = np.zeros((self.V, 3), np.float32)
+        if coverage is None:
+            coverage = np.zeros(self.V, np.uint8)
+        o = offsets_one if _is_torch(offsets_one) else _np(offsets_one, np.float32)
+        self._check(_lib.morea_dvf(self.h, _ptr(o), int(side), _ptr(dvf), _ptr(coverage)))
+        return dvf, coverage
 
     def set_sampler(self, mode, rate=1.0):
         """SAMPLER_VOXEL (exactly-once voxel centres) or SAMPLER_SOBOL (App. A.2
