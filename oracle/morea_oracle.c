@@ -26,6 +26,7 @@
  *   Sobol-in-tetrahedron sampler (NEXT-1)    App. A.2 L744-751                (S1..S9)
  *   batched fold repair (NEXT-2)             §4.3.1 L429-437                  (P1..P8)
  *   elasticity from masks, DVF (NEXT-4)      App. A.1, §5.4 L616     (E1..E3)
+ *   optimal mixing of a colour class (NEXT-3) §3 L231-233                      (M1..M7)
  *
  * Everything that decides an integer (ownership, fold, the h case split, band
  * membership) is decided exactly in integer arithmetic (int64 / __int128) or
@@ -1126,6 +1127,89 @@ int orc_eval_partial(orc_problem *P, const float *base_offsets_one, const orc_ac
     return 0;
 }
 
+/* ------------------------------------------------------------------ */
+/* NEXT-3: optimal mixing of one FOS colour class (§3).        */
+/* "Variation then proceeds by considering variables in FOS elements    */
+/* jointly in a procedure called optimal mixing.  In this step,         */
+/* distributions are estimated for each FOS element in each cluster, and */
+/* new, partial solutions are sampled from these distributions.  Newly  */
+/* sampled partial solutions are evaluated and accepted if their        */
+/* insertion into the parent solution results in a solution that        */
+/* dominates the parent solution or that is non-dominated in the current */
+/* elitist archive."  Readings M1..M7.  The distributions   */
+/* (mean, Cholesky factor) are inputs: estimating them is the caller's.  */
+/* ------------------------------------------------------------------ */
+static uint64_t mix_key(uint64_t seed, int64_t gen, int64_t k, int g) {
+    uint64_t h = splitmix64(seed + (uint64_t)gen);
+    h = splitmix64(h + (uint64_t)k);
+    return splitmix64(h + (uint64_t)g);
+}
+
+/* a dominates b: no worse in every objective, better in one (minimisation) */
+static int dominates(const double a[3], const double b[3]) {
+    int better = 0;
+    for (int i = 0; i < 3; i++) {
+        if (a[i] > b[i]) return 0;
+        if (a[i] < b[i]) better = 1;
+    }
+    return better;
+}
+
+/* M1-M7 for one solution (global index k, model of its cluster: mu = sum_g d_g
+ * doubles, L = sum_g d_g^2 doubles, row-major lower triangles, d_g = 6 |S_g|);
+ * off, acc and obj are updated in place; accepted: G flags */
+int orc_mix(orc_problem *P, float *off, orc_acc *acc, double obj[3], int G, const int32_t *grp_off,
+            const int32_t *changed, const double *mu, const double *L, const uint8_t *fixed, int A,
+            const double *archive, double steer_max, uint64_t seed, int64_t gen, int64_t k,
+            uint8_t *accepted) {
+    int64_t mo = 0, lo = 0;
+    for (int g = 0; g < G; g++) {
+        int ns = grp_off[g + 1] - grp_off[g];
+        int d = 6 * ns;
+        const int32_t *S = changed + grp_off[g];
+        accepted[g] = 0;
+        /* M1: z ~ N(0, I_d), pairs from the P5 generator keyed by (seed, gen, k, g) */
+        double *z = (double *)malloc(sizeof(double) * (d + 1));
+        uint64_t key = mix_key(seed, gen, k, g), ctr = 0;
+        for (int i = 0; i < d; i += 2) gauss_pair(key, &ctr, &z[i], &z[i + 1]);
+        /* M2/M3: x = mu + L z (ascending j), rounded to fp32; fixed axes keep the parent */
+        float *nv = (float *)malloc(sizeof(float) * (d > 0 ? d : 1));
+        for (int i = 0; i < d; i++) {
+            double x = mu[mo + i];
+            for (int j = 0; j <= i; j++) x = x + L[lo + (int64_t)i * d + j] * z[j];
+            int pt = S[i / 6], c = i % 6;
+            nv[i] = (fixed && fixed[3 * pt + c % 3]) ? off[6 * pt + c] : (float)x;
+        }
+        mo += d;
+        lo += (int64_t)d * d;
+        /* partial evaluation of the candidate against the current parent */
+        double cobj[3];
+        orc_acc cacc;
+        int rc = orc_eval_partial(P, off, acc, ns, S, nv, cobj, &cacc);
+        int ok = rc == 0 && cacc.folds == 0 && !(cacc.flags & (ORC_F_DOMAIN | ORC_F_EMPTY)); /* M4 */
+        if (ok && steer_max > 0.0 && !(cobj[2] <= steer_max)) ok = 0;                       /* M5 */
+        if (ok) {                                                                             /* M5 */
+            int acc_ok = dominates(cobj, obj);
+            if (!acc_ok) {
+                acc_ok = 1;
+                for (int a = 0; a < A; a++)
+                    if (dominates(archive + 3 * a, cobj)) { acc_ok = 0; break; }
+            }
+            ok = acc_ok;
+        }
+        if (ok) { /* M6: commit; the next group sees the updated parent */
+            for (int i = 0; i < ns; i++)
+                for (int c = 0; c < 6; c++) off[6 * S[i] + c] = nv[6 * i + c];
+            *acc = cacc;
+            for (int i = 0; i < 3; i++) obj[i] = cobj[i];
+            accepted[g] = 1;
+        }
+        free(z);
+        free(nv);
+    }
+    return 0;
+}
+
 /* fold flags per (side, tet) + count and severity (O2; row a9) */
 int orc_check_folds(orc_problem *P, const float *offsets_one, int32_t *count, double *severity,
                     uint8_t *flags /* 2*T or NULL */) {
@@ -1343,6 +1427,19 @@ void orc_gauss(uint64_t key, int n, double *out) {
 double orc_repair_sigma(orc_problem *P, const float *off, int s, int j) { return repair_sigma(P, off, s, j); }
 uint64_t orc_fnv1a64(const unsigned char *b, int64_t n) { return fnv1a64(b, (size_t)n); }
 uint64_t orc_splitmix64(uint64_t z) { return splitmix64(z); }
+/* M1/M2 sampler alone: x = mu + L z for (seed, gen, k, g), d variables (fp64) */
+void orc_mix_sample(const double *mu, const double *L, int d, uint64_t seed, int64_t gen, int64_t k, int g,
+                    double *x) {
+    double *z = (double *)malloc(sizeof(double) * (d + 2));
+    uint64_t key = mix_key(seed, gen, k, g), ctr = 0;
+    for (int i = 0; i < d; i += 2) gauss_pair(key, &ctr, &z[i], &z[i + 1]);
+    for (int i = 0; i < d; i++) {
+        double v = mu[i];
+        for (int j = 0; j <= i; j++) v = v + L[(int64_t)i * d + j] * z[j];
+        x[i] = v;
+    }
+    free(z);
+}
 uint64_t orc_tet_seed(const int64_t *Q12, uint32_t *mask4) {
     int64_t Q[4][3];
     for (int k = 0; k < 4; k++)

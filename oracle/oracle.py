@@ -89,6 +89,10 @@ def lib():
         L.orc_label_counts.argtypes = [vp, vp, ctypes.c_int, vp, ctypes.c_int, vp]
         L.orc_elasticity.argtypes = [vp, vp, ctypes.c_int, vp, vp]
         L.orc_dvf.argtypes = [vp, vp, ctypes.c_int, vp, vp]
+        L.orc_mix.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp, vp, vp, vp, vp, ctypes.c_int, vp,
+                              ctypes.c_double, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, vp]
+        L.orc_mix_sample.argtypes = [vp, vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
+                                     ctypes.c_int, vp]
         L.orc_det_ln.restype = ctypes.c_double
         L.orc_det_ln.argtypes = [ctypes.c_double]
         L.orc_gauss.argtypes = [ctypes.c_uint64, ctypes.c_int, vp]
@@ -241,6 +245,26 @@ class Oracle:
         lib().orc_dvf(self.h, _p(o), int(side), _p(d), _p(c))
         return d, c
 
+    def mix(self, offsets_one, acc, obj, grp_off, changed, mu, Lc, fixed, archive, steer_max, seed, gen, k):
+        """NEXT-3 optimal mixing (M1-M7) of one solution over one colour class; returns
+        (offsets, acc, obj, accepted flags)."""
+        o = np.array(self._off(offsets_one), copy=True)
+        a = Acc()
+        ctypes.memmove(ctypes.byref(a), ctypes.byref(acc), ctypes.sizeof(Acc))
+        ob = np.array(obj, dtype=np.float64, copy=True)
+        go = np.ascontiguousarray(grp_off, dtype=np.int32)
+        ch = np.ascontiguousarray(changed, dtype=np.int32)
+        m = np.ascontiguousarray(mu, dtype=np.float64)
+        l = np.ascontiguousarray(Lc, dtype=np.float64)
+        fx = None if fixed is None else np.ascontiguousarray(fixed, dtype=np.uint8)
+        ar = np.ascontiguousarray(archive, dtype=np.float64).reshape(-1, 3)
+        G = len(go) - 1
+        accd = np.zeros(G, dtype=np.uint8)
+        lib().orc_mix(self.h, _p(o), ctypes.byref(a), _p(ob), G, _p(go), _p(ch), _p(m), _p(l), _p(fx),
+                      len(ar), _p(ar), float(steer_max), ctypes.c_uint64(seed % 2 ** 64), int(gen), int(k),
+                      _p(accd))
+        return o, a, ob, accd
+
     def repair(self, offsets_one, seed, k, fixed=None):
         """NEXT-2 fold repair (P1-P8) of one solution (generator index k); fixed: None or
         N x 3 bools of axes that must not move.  Returns (offsets, moved, aborted)."""
@@ -312,6 +336,14 @@ def gauss(key, n):
     out = np.zeros(n)
     lib().orc_gauss(ctypes.c_uint64(key % 2 ** 64), int(n), _p(out))
     return out
+
+
+def mix_sample(mu, Lc, seed, gen, k, g):
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    Lc = np.ascontiguousarray(Lc, dtype=np.float64)
+    x = np.zeros(len(mu))
+    lib().orc_mix_sample(_p(mu), _p(Lc), len(mu), ctypes.c_uint64(seed % 2 ** 64), int(gen), int(k), int(g), _p(x))
+    return x
 
 
 def fnv1a64(b: bytes):
