@@ -210,6 +210,38 @@ int morea_set_sampler(morea_ctx *ctx, int mode, double rate);
 int morea_repair(morea_ctx *ctx, int pop, float *offsets, const uint8_t *fixed, uint64_t seed,
                  int64_t sol_base, int32_t *moved, int32_t *aborted);
 
+/* Optimal mixing of one FOS colour class on the device (
+ * PAPER.md §3: "distributions are estimated for each FOS element in
+ * each cluster, and new, partial solutions are sampled from these distributions.
+ * Newly sampled partial solutions are evaluated and accepted if their insertion
+ * into the parent solution results in a solution that dominates the parent
+ * solution or that is non-dominated in the current elitist archive").
+ * The groups (grp_off / changed_pts, HOST arrays as for morea_eval_partial) must
+ * be one colour class: pairwise disjoint dependent tets.  Per solution k and
+ * group g: z ~ N(0, I_d) (d = 6 |S_g|, SplitMix64 keys of (seed, gen,
+ * sol_base + k, g), Marsaglia's polar method); x = mu + L z with the model of
+ * cluster[k] (mu: n_clusters blocks of sum_g d_g doubles, group after group; L:
+ * n_clusters blocks of sum_g d_g^2 doubles, row-major lower triangles); the new
+ * point values are fp32(x) (point order of changed_pts, then src xyz, tgt xyz),
+ * axes flagged in `fixed` (NULL or N*3) keep the parent's value.  Each candidate
+ * is evaluated partially (per-tet cache); groups are then accepted in id order,
+ * each against the solution as updated by the earlier accepted groups: a
+ * candidate with folds, a DOMAIN/EMPTY flag or (steer_max > 0) f_guidance >
+ * steer_max is rejected; otherwise it is accepted iff it dominates the parent
+ * or no archive member (n_archive x 3 objectives, fixed during the call)
+ * dominates it.  Accepted groups are committed: offsets, acc, obj and the
+ * tet_cache rows of their dependent tets.  Readings M1..M7 in DESIGN.md §3.
+ *  offsets (pop*N*6), acc (pop), obj (pop*3), tet_cache (pop*T*4): the
+ *    population state, updated in place (host or device; obj / acc / cache must
+ *    be those of offsets, e.g. from morea_eval_full).
+ *  accepted: NULL or pop*n_groups bytes.
+ * Archive insertion and model estimation are the caller's. */
+int morea_mix_class(morea_ctx *ctx, int pop, float *offsets, morea_acc *acc, double *obj, double *tet_cache,
+                    int n_groups, const int32_t *grp_off, const int32_t *changed_pts, const int32_t *cluster,
+                    int n_clusters, const double *mu, const double *L, const uint8_t *fixed, int n_archive,
+                    const double *archive, double steer_max, uint64_t seed, int64_t gen, int64_t sol_base,
+                    uint8_t *accepted);
+
 /* Rasterizer reuse.
  * Object counts per tet (App. A.1: "We compute the overlap
  * that each object mask has with the tetrahedron ... which produces one fraction

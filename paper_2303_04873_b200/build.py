@@ -11,7 +11,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libmorea.so")
 SOURCES = ["morea_kernels.cu", "morea_api.cu"]
-HEADERS = [os.path.join(CSRC, h) for h in ("morea_internal.h", "morea_sobol_setup.cuh", "morea_sobol.cuh", "morea_repair.cuh", "morea_export.cuh")] + \
+HEADERS = [os.path.join(CSRC, h) for h in ("morea_internal.h", "morea_sobol_setup.cuh", "morea_sobol.cuh", "morea_repair.cuh", "morea_export.cuh", "morea_mix.cuh")] + \
     [os.path.join(INCLUDE, "morea.h")]
 
 NVCC_FLAGS = [

@@ -79,6 +79,9 @@ struct morea_ctx {
   DevBuf d_inc_off, d_inc, st_fixed, st_rep;
   // rasterizer exports (NEXT-4)
   DevBuf st_masks, st_counts, st_dvf, st_cov, scratch_owner, zero_off;
+  // optimal mixing (NEXT-3)
+  DevBuf mx_off, mx_acc, mx_obj, mx_cache, mx_nv, mx_pobj, mx_pacc, mx_dep, mx_base, mx_accepted, mx_cluster,
+      mx_mu, mx_L, mx_arch, mx_moff, mx_fixed;
   int blocks_per_sm_sobol = 1, blocks_per_sm_sobol_tex = 1;
   // texture-gather copies (tall 2D arrays) of I_s, I_t and the maps
   bool use_tex = false;
@@ -263,6 +266,8 @@ MeshDev mesh_of(const morea_ctx* c) {
   m.spoke_mode = c->spoke_mode;
   return m;
 }
+
+constexpr long long kMixMaxDimHost = 192;  // = kMixMaxDim (morea_mix.cuh)
 
 int raster_grid(morea_ctx* ctx, long long n_items) {
   long long g = (long long)ctx->n_sm * (ctx->use_tex ? ctx->blocks_per_sm_tex : ctx->blocks_per_sm);
@@ -577,7 +582,10 @@ void morea_destroy(morea_ctx* ctx) {
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
                     &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->st_masks, &ctx->st_counts, &ctx->st_dvf, &ctx->st_cov,
-                    &ctx->scratch_owner, &ctx->zero_off, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
+                    &ctx->scratch_owner, &ctx->zero_off, &ctx->mx_off, &ctx->mx_acc,
+                    &ctx->mx_obj, &ctx->mx_cache, &ctx->mx_nv, &ctx->mx_pobj, &ctx->mx_pacc, &ctx->mx_dep,
+                    &ctx->mx_base, &ctx->mx_accepted, &ctx->mx_cluster, &ctx->mx_mu, &ctx->mx_L, &ctx->mx_arch,
+                    &ctx->mx_moff, &ctx->mx_fixed, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
                     &ctx->full_sched, &ctx->full_group_off, &ctx->geom, &ctx->scal, &ctx->hgn,
                     &ctx->counter, &ctx->stats, &ctx->st_off, &ctx->st_nv, &ctx->st_cache_in,
                     &ctx->st_base_acc, &ctx->st_obj, &ctx->st_acc, &ctx->st_cache_out,
@@ -852,6 +860,37 @@ int morea_eval_full(morea_ctx* ctx, int pop, const float* offsets, double* obj, 
   return MOREA_OK;
 }
 
+// a8 on device buffers: the plan of ctx->plan, base offsets/acc, new values,
+// optional cache; outputs per (solution, group) and the dependent-tet cache rows
+static cudaError_t partial_core(morea_ctx* ctx, int pop, int G, const float* off, const morea_acc* bacc,
+                                const float* nv, const double* cin, double* obj, morea_acc* acc,
+                                double* dep_out) {
+  const Plan& P = ctx->plan;
+  EvalArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.vol = volumes_of(ctx);
+  a.mesh = mesh_of(ctx);
+  a.P = pop;
+  a.offsets = off;
+  a.n_entries = P.n_entries;
+  a.canon_tet = P.canon_tet.as<int>();
+  a.canon_slots = P.canon_slots.as<int4>();
+  a.sched = P.sched.as<int>();
+  a.new_vals = nv;
+  a.S_total = P.S;
+  a.partial = 1;
+  a.n_setup_versions = 2;
+  a.n_raster_versions = cin ? 1 : 2;
+  a.expect[0] = a.expect[1] = -1;
+  set_sampler_args(ctx, a);
+  cudaError_t e = run_eval(ctx, a);
+  if (e != cudaSuccess) return e;
+  e = launch_reduce(a, G, P.group_off.as<int>(), bacc, cin, dep_out, P.changed.as<int>(), P.grp_off.as<int>(),
+                    obj, acc, ctx->stream);
+  ctx->kernels++;
+  return e;
+}
+
 int morea_eval_partial(morea_ctx* ctx, int pop, const float* base_offsets,
                        const morea_acc* base_acc, int n_groups, const int32_t* grp_off,
                        const int32_t* changed_pts, const float* new_vals, const double* tet_cache,
@@ -878,27 +917,8 @@ int morea_eval_partial(morea_ctx* ctx, int pop, const float* base_offsets,
   CK(out_dev(obj, (size_t)pop * G * 3 * sizeof(double), ctx->st_obj, ov[0]));
   CK(out_dev(acc, (size_t)pop * G * sizeof(morea_acc), ctx->st_acc, ov[1]));
   CK(out_dev(dep_cache_out, (size_t)pop * P.n_entries * 4 * sizeof(double), ctx->st_cache_out, ov[2]));
-  EvalArgs a;
-  std::memset(&a, 0, sizeof(a));
-  a.vol = volumes_of(ctx);
-  a.mesh = mesh_of(ctx);
-  a.P = pop;
-  a.offsets = off;
-  a.n_entries = P.n_entries;
-  a.canon_tet = P.canon_tet.as<int>();
-  a.canon_slots = P.canon_slots.as<int4>();
-  a.sched = P.sched.as<int>();
-  a.new_vals = nv;
-  a.S_total = P.S;
-  a.partial = 1;
-  a.n_setup_versions = 2;
-  a.n_raster_versions = cin ? 1 : 2;
-  a.expect[0] = a.expect[1] = -1;
-  set_sampler_args(ctx, a);
-  CK(run_eval(ctx, a));
-  CK(launch_reduce(a, G, P.group_off.as<int>(), bacc, cin, (double*)ov[2].dev, P.changed.as<int>(),
-                   P.grp_off.as<int>(), (double*)ov[0].dev, ov[1].dev, ctx->stream));
-  ctx->kernels++;
+  CK(partial_core(ctx, pop, G, off, bacc, nv, cin, (double*)ov[0].dev, (morea_acc*)ov[1].dev,
+                  (double*)ov[2].dev));
   CK(finish_outputs(ctx, ov, 3));
   return MOREA_OK;
 }
@@ -1027,6 +1047,107 @@ int morea_dvf(morea_ctx* ctx, const float* offsets_one, int side, float* dvf, ui
   CK(launch_dvf(a, side, ctx->scratch_owner.as<int>(), (float*)ov[0].dev, cov, ctx->stream));
   ctx->kernels += 4;
   CK(finish_outputs(ctx, ov, 2));
+  return MOREA_OK;
+}
+
+// in/out array: device view, host arrays staged in and (by finish_outputs) back out
+static cudaError_t inout_dev(morea_ctx* ctx, void* p, size_t bytes, DevBuf& st, OutView& v) {
+  cudaError_t e = out_dev(p, bytes, st, v);
+  if (e != cudaSuccess || !v.copy) return e;
+  return cudaMemcpyAsync(v.dev, p, bytes, cudaMemcpyHostToDevice, ctx->stream);
+}
+
+int morea_mix_class(morea_ctx* ctx, int pop, float* offsets, morea_acc* acc, double* obj, double* tet_cache,
+                    int n_groups, const int32_t* grp_off, const int32_t* changed_pts, const int32_t* cluster,
+                    int n_clusters, const double* mu, const double* L, const uint8_t* fixed, int n_archive,
+                    const double* archive, double steer_max, uint64_t seed, int64_t gen, int64_t sol_base,
+                    uint8_t* accepted) {
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  if (pop < 0 || n_groups < 0 || !grp_off || n_clusters < 1 || n_archive < 0 || sol_base < 0)
+    return fail(ctx, MOREA_EINVAL, "bad pop / groups / clusters / archive");
+  if (pop > 0 && (!offsets || !acc || !obj || !tet_cache || !cluster || !mu || !L))
+    return fail(ctx, MOREA_EINVAL, "null state or model");
+  if (n_archive > 0 && !archive) return fail(ctx, MOREA_EINVAL, "null archive");
+  rc = build_plan(ctx, n_groups, grp_off, changed_pts);
+  if (rc) return rc;
+  if (pop == 0 || n_groups == 0) return MOREA_OK;
+  const Plan& P = ctx->plan;
+  const int N = ctx->N, T = ctx->T, G = n_groups;
+  // model layout: per cluster, mu_g (d_g) then the next group's; L_g (d_g^2) likewise
+  std::vector<long long> moff(2 * G);
+  long long mu_stride = 0, L_stride = 0;
+  for (int g = 0; g < G; g++) {
+    const long long d = 6LL * (P.key_off[g + 1] - P.key_off[g]);
+    if (d > kMixMaxDimHost) return fail(ctx, MOREA_EINVAL, "FOS element %d has more than 32 points", g);
+    moff[2 * g] = mu_stride;
+    moff[2 * g + 1] = L_stride;
+    mu_stride += d;
+    L_stride += d * d;
+  }
+  std::vector<int32_t> cl;
+  CK(to_host(ctx, cluster, (size_t)pop, cl));
+  for (int k = 0; k < pop; k++)
+    if (cl[k] < 0 || cl[k] >= n_clusters) return fail(ctx, MOREA_EINVAL, "cluster[%d] out of range", k);
+  OutView ov[5];
+  CK(inout_dev(ctx, offsets, (size_t)pop * N * 6 * sizeof(float), ctx->mx_off, ov[0]));
+  CK(inout_dev(ctx, acc, (size_t)pop * sizeof(morea_acc), ctx->mx_acc, ov[1]));
+  CK(inout_dev(ctx, obj, (size_t)pop * 3 * sizeof(double), ctx->mx_obj, ov[2]));
+  CK(inout_dev(ctx, tet_cache, (size_t)pop * T * 4 * sizeof(double), ctx->mx_cache, ov[3]));
+  CK(ctx->mx_accepted.ensure((size_t)pop * G));
+  CK(out_dev(accepted, (size_t)pop * G, ctx->mx_accepted, ov[4]));
+  unsigned char* acc_flags = ov[4].dev ? (unsigned char*)ov[4].dev : ctx->mx_accepted.as<unsigned char>();
+  const int* cl_d = nullptr;
+  const double *mu_d = nullptr, *L_d = nullptr, *ar_d = nullptr;
+  const unsigned char* fx_d = nullptr;
+  CK(in_dev(ctx, cluster, (size_t)pop * sizeof(int32_t), ctx->mx_cluster, (const void**)&cl_d));
+  CK(in_dev(ctx, mu, (size_t)n_clusters * mu_stride * sizeof(double), ctx->mx_mu, (const void**)&mu_d));
+  CK(in_dev(ctx, L, (size_t)n_clusters * L_stride * sizeof(double), ctx->mx_L, (const void**)&L_d));
+  CK(in_dev(ctx, archive, (size_t)n_archive * 3 * sizeof(double), ctx->mx_arch, (const void**)&ar_d));
+  CK(in_dev(ctx, fixed, (size_t)N * 3, ctx->mx_fixed, (const void**)&fx_d));
+  CK(ctx->mx_moff.ensure(moff.size() * sizeof(long long)));
+  CK(cudaMemcpyAsync(ctx->mx_moff.p, moff.data(), moff.size() * sizeof(long long), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(ctx->mx_nv.ensure(std::max<size_t>(1, (size_t)pop * P.S * 6) * sizeof(float)));
+  CK(ctx->mx_pobj.ensure((size_t)pop * G * 3 * sizeof(double)));
+  CK(ctx->mx_pacc.ensure((size_t)pop * G * sizeof(morea_acc)));
+  CK(ctx->mx_dep.ensure(std::max<size_t>(1, (size_t)pop * P.n_entries * 4) * sizeof(double)));
+  CK(ctx->mx_base.ensure((size_t)pop * sizeof(morea_acc)));
+  // M1-M3: sample every (solution, group) of the class
+  MixArgs m;
+  m.P = pop; m.G = G; m.N = N; m.T = T; m.S_total = P.S; m.n_entries = P.n_entries;
+  m.sol_base = sol_base;
+  m.offsets = (const float*)ov[0].dev;
+  m.new_vals = ctx->mx_nv.as<float>();
+  m.grp_off = P.grp_off.as<int>();
+  m.changed = P.changed.as<int>();
+  m.model_off = ctx->mx_moff.as<long long>();
+  m.mu_stride = mu_stride;
+  m.L_stride = L_stride;
+  m.cluster = cl_d;
+  m.mu = mu_d;
+  m.L = L_d;
+  m.fixed = fx_d;
+  m.seed = seed;
+  m.gen = gen;
+  CK(launch_mix_sample(m, ctx->stream));
+  ctx->kernels++;
+  // a8: every candidate against the class-start state, with the per-tet cache
+  CK(cudaMemcpyAsync(ctx->mx_base.p, ov[1].dev, (size_t)pop * sizeof(morea_acc), cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  CK(partial_core(ctx, pop, G, (const float*)ov[0].dev, ctx->mx_base.as<morea_acc>(), ctx->mx_nv.as<float>(),
+                  (const double*)ov[3].dev, ctx->mx_pobj.as<double>(), ctx->mx_pacc.as<morea_acc>(),
+                  ctx->mx_dep.as<double>()));
+  // M4-M6: acceptance in group order, then commit
+  CK(launch_mix_accept(pop, G, T, ctx->mx_base.as<morea_acc>(), ctx->mx_pacc.as<morea_acc>(),
+                       (morea_acc*)ov[1].dev, (double*)ov[2].dev, ar_d, n_archive, steer_max, acc_flags,
+                       ctx->stream));
+  CK(launch_mix_commit(pop, G, N, T, P.S, P.n_entries, acc_flags, P.grp_off.as<int>(), P.changed.as<int>(),
+                       P.group_off.as<int>(), P.canon_tet.as<int>(), ctx->mx_nv.as<float>(),
+                       ctx->mx_dep.as<double>(), (float*)ov[0].dev, (double*)ov[3].dev, ctx->stream));
+  ctx->kernels += 2;
+  CK(finish_outputs(ctx, ov, 5));
   return MOREA_OK;
 }
 

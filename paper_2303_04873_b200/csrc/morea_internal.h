@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "morea.h"
+
 namespace morea {
 
 constexpr int kMaxPairs = 8;
@@ -160,6 +162,31 @@ cudaError_t launch_label_counts(const EvalArgs& a, int side, const unsigned char
                                 long long* counts, cudaStream_t s);
 cudaError_t launch_dvf(const EvalArgs& a, int side, int* owner, float* dvf, unsigned char* cov,
                        cudaStream_t s);
+// NEXT-3 sampling arguments (morea_mix.cuh)
+struct MixArgs {
+  int P, G, N, T, S_total, n_entries;
+  long long sol_base;
+  const float* offsets;        // P*N*6 (parent state)
+  float* new_vals;             // P*S_total*6 (sampled)
+  const int* grp_off;          // G+1 (device)
+  const int* changed;          // S_total (device)
+  const long long* model_off;  // G x 2: offsets of mu_g and L_g inside one cluster's block
+  long long mu_stride, L_stride;  // doubles per cluster
+  const int* cluster;          // P
+  const double* mu;
+  const double* L;
+  const unsigned char* fixed;  // N*3 or nullptr
+  unsigned long long seed;
+  long long gen;
+};
+cudaError_t launch_mix_sample(const MixArgs& a, cudaStream_t s);
+cudaError_t launch_mix_accept(int P, int G, int T, const morea_acc* base, const morea_acc* pacc, morea_acc* acc,
+                              double* obj, const double* archive, int A_n, double steer_max,
+                              unsigned char* accepted, cudaStream_t s);
+cudaError_t launch_mix_commit(int P, int G, int N, int T, int S_total, int n_entries,
+                              const unsigned char* accepted, const int* grp_off, const int* changed,
+                              const int* group_off, const int* canon_tet, const float* new_vals,
+                              const double* dep_cache, float* offsets, double* tet_cache, cudaStream_t s);
 cudaError_t launch_dilate_band(const unsigned char* band, int nx, int ny, int nz, unsigned char* dil,
                                cudaStream_t s);
 cudaError_t launch_reduce(const EvalArgs& a, int G, const int* group_off, const void* base_acc,

@@ -1265,6 +1265,7 @@ cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, un
 
 #include "morea_repair.cuh"
 #include "morea_export.cuh"
+#include "morea_mix.cuh"
 
 }  // namespace morea
 

@@ -31,7 +31,8 @@ assert ACC_DTYPE.itemsize == 48
 EXPORTS = ["morea_create", "morea_destroy", "morea_last_error", "morea_stream", "morea_load_images",
            "morea_set_mesh", "morea_eval_full", "morea_eval_partial", "morea_partial_deps",
            "morea_check_folds", "morea_owner_map", "morea_distance_map", "morea_prof_enable",
-           "morea_prof_read", "morea_kernel_launches", "morea_set_sampler", "morea_repair", "morea_label_counts", "morea_elasticity", "morea_dvf"]
+           "morea_prof_read", "morea_kernel_launches", "morea_set_sampler", "morea_repair", "morea_label_counts", "morea_elasticity", "morea_dvf",
+           "morea_mix_class"]
 SAMPLER_VOXEL = 0
 SAMPLER_SOBOL = 1
 
@@ -69,6 +70,8 @@ def _load():
     L.morea_label_counts.argtypes = [vp, vp, i32, vp, i32, vp]
     L.morea_elasticity.argtypes = [vp, vp, i32, vp, vp]
     L.morea_dvf.argtypes = [vp, vp, i32, vp, vp]
+    L.morea_mix_class.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, i32, vp, vp, vp, i32, vp, f64,
+                                  ctypes.c_uint64, i64, i64, vp]
     L.morea_kernel_launches.argtypes = [vp]
     L.morea_kernel_launches.restype = i64
     L.morea_prof_read.argtypes = [vp] + [ctypes.POINTER(i64), ctypes.POINTER(f64)] + \
@@ -257,6 +260,26 @@ class Context:
         o = offsets_one if _is_torch(offsets_one) else _np(offsets_one, np.float32)
         self._check(_lib.morea_dvf(self.h, _ptr(o), int(side), _ptr(dvf), _ptr(coverage)))
         return dvf, coverage
+
+    def mix_class(self, offsets, acc, obj, tet_cache, grp_off, changed, cluster, mu, L, fixed=None,
+                  archive=None, steer_max=0.0, seed=0, gen=0, sol_base=0, accepted=None):
+        """Optimal mixing of one FOS colour class (§3); the population state
+        (offsets, acc, obj, tet_cache) is updated in place."""
+        P = int(offsets.shape[0])
+        go = _np(grp_off, np.int32)
+        ch = _np(changed, np.int32)
+        cl = cluster if _is_torch(cluster) else _np(cluster, np.int32)
+        mu_ = mu if _is_torch(mu) else _np(mu, np.float64)
+        L_ = L if _is_torch(L) else _np(L, np.float64)
+        fx = None if fixed is None else (fixed if _is_torch(fixed) else _np(fixed, np.uint8))
+        ar = np.zeros((0, 3)) if archive is None else archive
+        ar = ar if _is_torch(ar) else _np(ar, np.float64)
+        n_clusters = max(1, int(mu_.numel() if _is_torch(mu_) else mu_.size) // max(1, 6 * len(ch)))
+        self._check(_lib.morea_mix_class(self.h, P, _ptr(offsets), _ptr(acc), _ptr(obj), _ptr(tet_cache),
+                                         len(go) - 1, _ptr(go), _ptr(ch), _ptr(cl), n_clusters, _ptr(mu_),
+                                         _ptr(L_), _ptr(fx), int(ar.shape[0]), _ptr(ar), float(steer_max),
+                                         ctypes.c_uint64(int(seed) % 2 ** 64), int(gen), int(sol_base),
+                                         _ptr(accepted)))
 
     def set_sampler(self, mode, rate=1.0):
         """SAMPLER_VOXEL (exactly-once voxel centres) or SAMPLER_SOBOL (App. A.2
