@@ -271,7 +271,8 @@ constexpr long long kMixMaxDimHost = 192;  // = kMixMaxDim (morea_mix.cuh)
 
 int raster_grid(morea_ctx* ctx, long long n_items) {
   long long g = (long long)ctx->n_sm * (ctx->use_tex ? ctx->blocks_per_sm_tex : ctx->blocks_per_sm);
-  long long need = (n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int bw = raster_block_warps();
+  long long need = (n_items + bw - 1) / bw;
   return (int)std::max<long long>(1, std::min(g, need));
 }
 

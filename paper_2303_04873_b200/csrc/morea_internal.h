@@ -153,6 +153,7 @@ cudaError_t launch_own_records(const float* I, const unsigned char* band, long l
 cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s);
 cudaError_t launch_raster(const EvalArgs& a, int grid, cudaStream_t s);
 int raster_blocks_per_sm(bool tex);
+int raster_block_warps();
 cudaError_t launch_sobol(const EvalArgs& a, int grid, cudaStream_t s);
 int sobol_blocks_per_sm(bool tex);
 cudaError_t launch_repair(const MeshDev& m, const double sp[3], int P, long long sol_base, float* offsets,

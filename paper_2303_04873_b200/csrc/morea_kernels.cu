@@ -35,6 +35,10 @@
 #define MOREA_ABLATE 0  // dev experiments only (4: no guidance evaluation, 5: no band loads)
 #endif
 
+#ifndef MOREA_SM_BLOCK
+#define MOREA_SM_BLOCK 28  // > 0: k_raster as one block of this many warps per SM (0: 2-warp blocks)
+#endif
+
 #ifndef MOREA_SOBOL_MINB
 #define MOREA_SOBOL_MINB 14  // k_sobol: resident 64-thread blocks per SM
 #endif
@@ -872,9 +876,27 @@ __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int l
 // ---------------------------------------------------------------------------
 // k_raster: persistent warps over the item queue (a4 + a5 + a6 + per-tet a7).
 // ---------------------------------------------------------------------------
+#if MOREA_SM_BLOCK
+// one block per SM: its warps take consecutive items (the same tet for
+// consecutive solutions) together, so their footprints share the SM's L1
+constexpr int kRasterBlockWarps = MOREA_SM_BLOCK;
+constexpr int kRasterBlockThreads = 32 * kRasterBlockWarps;
+#define RASTER_BOUNDS __launch_bounds__(kRasterBlockThreads, 1)
+#else
+constexpr int kRasterBlockWarps = kWarpsPerBlock;
+constexpr int kRasterBlockThreads = kRasterThreads;
+#define RASTER_BOUNDS __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB)
+#endif
+
 template <bool TEX>
-__global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(const EvalArgs A) {
+__global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
+#if MOREA_SM_BLOCK
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpSmem* smem = reinterpret_cast<WarpSmem*>(smem_raw);
+  __shared__ unsigned long long chunk;
+#else
   __shared__ WarpSmem smem[kWarpsPerBlock];
+#endif
   // warp index and lane through volatile asm: kept in registers instead of being
   // re-derived from special registers at every use
   int warp, lane;
@@ -886,9 +908,18 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
   if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0ull;
   while (true) {
     unsigned long long item = 0;
+#if MOREA_SM_BLOCK
+    __syncthreads();
+    if (threadIdx.x == 0) chunk = atomicAdd(A.counter, (unsigned long long)kRasterBlockWarps);
+    __syncthreads();
+    if ((long long)chunk >= n_items) break;  // block-uniform
+    item = chunk + warp;
+    if ((long long)item >= n_items) continue;
+#else
     if (lane == 0) item = atomicAdd(A.counter, 1ULL);
     item = __shfl_sync(FULLMASK, item, 0);
     if ((long long)item >= n_items) break;
+#endif
     const int v = (int)(item / (unsigned long long)per_v);
     const long long rem = (long long)item - (long long)v * per_v;
     const int es = (int)(rem / A.P);
@@ -932,17 +963,27 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_RASTER_MINB) k_raster(co
   }
 }
 
+constexpr size_t kRasterDynSmem = MOREA_SM_BLOCK ? sizeof(WarpSmem) * kRasterBlockWarps : 0;
+
 int raster_blocks_per_sm(bool tex) {
+  if (kRasterDynSmem) {
+    cudaFuncSetAttribute(k_raster<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRasterDynSmem);
+    cudaFuncSetAttribute(k_raster<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRasterDynSmem);
+  }
   int nb = 0;
-  cudaError_t e = tex ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_raster<true>, kRasterThreads, 0)
-                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_raster<false>, kRasterThreads, 0);
+  cudaError_t e = tex ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_raster<true>, kRasterBlockThreads,
+                                                                      kRasterDynSmem)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_raster<false>, kRasterBlockThreads,
+                                                                      kRasterDynSmem);
   if (e != cudaSuccess) return 1;
   return nb > 0 ? nb : 1;
 }
 
+int raster_block_warps() { return kRasterBlockWarps; }
+
 cudaError_t launch_raster(const EvalArgs& a, int grid, cudaStream_t s) {
-  if (a.vol.use_tex) k_raster<true><<<grid, kRasterThreads, 0, s>>>(a);
-  else k_raster<false><<<grid, kRasterThreads, 0, s>>>(a);
+  if (a.vol.use_tex) k_raster<true><<<grid, kRasterBlockThreads, kRasterDynSmem, s>>>(a);
+  else k_raster<false><<<grid, kRasterBlockThreads, kRasterDynSmem, s>>>(a);
   return cudaGetLastError();
 }
 
