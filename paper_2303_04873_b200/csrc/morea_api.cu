@@ -324,7 +324,7 @@ cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
   if (a.sampler == MOREA_SAMPLER_SOBOL) {
     const long long g = (long long)ctx->n_sm *
                         (ctx->use_tex ? ctx->blocks_per_sm_sobol_tex : ctx->blocks_per_sm_sobol);
-    const long long need = (n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const long long need = (n_items + sobol_block_warps() - 1) / sobol_block_warps();
     e = launch_sobol(a, (int)std::max<long long>(1, std::min(g, need)), ctx->stream);
   } else {
     e = launch_raster(a, raster_grid(ctx, n_items), ctx->stream);

@@ -156,6 +156,7 @@ int raster_blocks_per_sm(bool tex);
 int raster_block_warps();
 cudaError_t launch_sobol(const EvalArgs& a, int grid, cudaStream_t s);
 int sobol_blocks_per_sm(bool tex);
+int sobol_block_warps();
 cudaError_t launch_repair(const MeshDev& m, const double sp[3], int P, long long sol_base, float* offsets,
                           const unsigned char* fixed, const int* inc_off, const int* inc,
                           unsigned long long seed, int* moved, int* aborted, cudaStream_t s);

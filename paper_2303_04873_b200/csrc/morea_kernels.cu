@@ -39,8 +39,8 @@
 #define MOREA_SM_BLOCK 28  // > 0: k_raster as one block of this many warps per SM (0: 2-warp blocks)
 #endif
 
-#ifndef MOREA_SOBOL_MINB
-#define MOREA_SOBOL_MINB 14  // k_sobol: resident 64-thread blocks per SM
+#ifndef MOREA_SOBOL_WARPS
+#define MOREA_SOBOL_WARPS 28  // k_sobol: warps of its one block per SM
 #endif
 
 #ifndef MOREA_RASTER_MINB

@@ -152,9 +152,15 @@ __device__ __forceinline__ float sb_trilinear(const Volumes& V, unsigned long lo
                   P.fz, gz);
 }
 
+// one block of kSobolWarps warps per SM; the warps take consecutive items (the
+// same tet for consecutive solutions) together, so their texel footprints share L1
+constexpr int kSobolWarps = MOREA_SOBOL_WARPS;
+constexpr int kSobolThreads = 32 * kSobolWarps;
+
 template <bool TEX>
-__global__ void __launch_bounds__(kRasterThreads, MOREA_SOBOL_MINB) k_sobol(const EvalArgs A) {
-  __shared__ SobolWarp smem[kWarpsPerBlock];
+__global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
+  __shared__ SobolWarp smem[kSobolWarps];
+  __shared__ unsigned long long chunk;
   __shared__ unsigned sV[4][32];
   int warp, lane;
   asm volatile("shr.u32 %0, %1, 5;" : "=r"(warp) : "r"(threadIdx.x));
@@ -181,10 +187,12 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_SOBOL_MINB) k_sobol(cons
   const long long n_items = per_v * A.n_raster_versions;
   if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0ull;
   while (true) {
-    unsigned long long item = 0;
-    if (lane == 0) item = atomicAdd(A.counter, 1ULL);
-    item = __shfl_sync(FULLMASK, item, 0);
-    if ((long long)item >= n_items) break;
+    __syncthreads();
+    if (threadIdx.x == 0) chunk = atomicAdd(A.counter, (unsigned long long)kSobolWarps);
+    __syncthreads();
+    if ((long long)chunk >= n_items) break;  // block-uniform
+    const unsigned long long item = chunk + warp;
+    if ((long long)item >= n_items) continue;
     const int ver = (int)(item / (unsigned long long)per_v);
     const long long rem = (long long)item - (long long)ver * per_v;
     const int es = (int)(rem / A.P);
@@ -314,17 +322,19 @@ __global__ void __launch_bounds__(kRasterThreads, MOREA_SOBOL_MINB) k_sobol(cons
   }
 }
 
+int sobol_block_warps() { return kSobolWarps; }
+
 int sobol_blocks_per_sm(bool tex) {
   int nb = 0;
-  cudaError_t e = tex ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sobol<true>, kRasterThreads, 0)
-                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sobol<false>, kRasterThreads, 0);
+  cudaError_t e = tex ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sobol<true>, kSobolThreads, 0)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sobol<false>, kSobolThreads, 0);
   if (e != cudaSuccess) return 1;
   return nb > 0 ? nb : 1;
 }
 
 cudaError_t launch_sobol(const EvalArgs& a, int grid, cudaStream_t s) {
-  if (a.vol.use_tex) k_sobol<true><<<grid, kRasterThreads, 0, s>>>(a);
-  else k_sobol<false><<<grid, kRasterThreads, 0, s>>>(a);
+  if (a.vol.use_tex) k_sobol<true><<<grid, kSobolThreads, 0, s>>>(a);
+  else k_sobol<false><<<grid, kSobolThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
