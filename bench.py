@@ -178,6 +178,11 @@ def run_reference(args, rank, world):
     return 0
 
 
+def _fin(x):
+    """None for a skipped (NaN) breakdown figure."""
+    return x if x == x else None
+
+
 # --------------------------------------------------------------------------- GPU leg
 def main():
     ap = argparse.ArgumentParser()
@@ -187,6 +192,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--class-index", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the Sobol / repair / mixing breakdown timings (for ncu launch lists)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: at least 3 untimed warm-up steps
@@ -294,38 +301,41 @@ def main():
     t_full = timed(lambda: ctx.eval_full(off_d, obj_d, acc_d, cache_d))
     t_part = timed(lambda: ctx.eval_partial(off_d, acc_d, go, ch, nv_d, cache_d, pobj_d, pacc_d))
     t_part_nc = timed(lambda: ctx.eval_partial(off_d, acc_d, go, ch, nv_d, None, pobj_d, pacc_d))
-    # NEXT-1: the paper's Sobol-in-tetrahedron sample set (App. A.2), rate 1 sample / voxel
-    ctx.set_sampler(morea.SAMPLER_SOBOL, 1.0)
-    t_sobol = timed(lambda: ctx.eval_full(off_d, obj_d, acc_d, None))
-    ctx.set_sampler(morea.SAMPLER_VOXEL)
-    # NEXT-2: fold repair of the whole population (on a copy of the offsets)
-    rep_off = off_d.clone()
-    fixed_d = torch.from_numpy(w.fixed_axes.astype("uint8")).to(dev)
-    t_repair = timed(lambda: ctx.repair(rep_off.copy_(off_d), 2024, fixed_d, s0), reps=1)
-    # NEXT-3: optimal mixing of colour class 0 on the device (model: this shard's
-    # population mean and covariance per FOS element, one cluster), on copies of the state
-    import numpy as _np
-    offs_h = w.offsets[s0:s1]
-    mus, Ls = [], []
-    for g in range(G):
-        X = offs_h[:, ch[go[g]:go[g + 1]], :].reshape(offs_h.shape[0], -1).astype(_np.float64)
-        C = _np.cov(X.T, bias=True) + 1e-4 * _np.eye(X.shape[1])
-        mus.append(X.mean(0))
-        Ls.append(_np.linalg.cholesky(C).ravel())
-    mu_d = torch.from_numpy(_np.concatenate(mus)).to(dev)
-    L_d = torch.from_numpy(_np.concatenate(Ls)).to(dev)
-    cl_d = torch.zeros(P, dtype=torch.int32, device=dev)
-    ctx.eval_full(off_d, obj_d, acc_d, cache_d)  # voxel-mode state of off_d (the Sobol run overwrote it)
-    mx_off, mx_acc, mx_obj, mx_tc = off_d.clone(), acc_d.clone(), obj_d.clone(), cache_d.clone()
-    mx_flags = torch.zeros((P, G), dtype=torch.uint8, device=dev)
+    t_sobol = t_repair = t_mix = float("nan")
+    mix_accept_frac = float("nan")
+    if not args.no_extras:
+        # NEXT-1: the paper's Sobol-in-tetrahedron sample set (App. A.2), rate 1 sample / voxel
+        ctx.set_sampler(morea.SAMPLER_SOBOL, 1.0)
+        t_sobol = timed(lambda: ctx.eval_full(off_d, obj_d, acc_d, None))
+        ctx.set_sampler(morea.SAMPLER_VOXEL)
+        # NEXT-2: fold repair of the whole population (on a copy of the offsets)
+        rep_off = off_d.clone()
+        fixed_d = torch.from_numpy(w.fixed_axes.astype("uint8")).to(dev)
+        t_repair = timed(lambda: ctx.repair(rep_off.copy_(off_d), 2024, fixed_d, s0), reps=1)
+        # NEXT-3: optimal mixing of colour class 0 on the device (model: this shard's
+        # population mean and covariance per FOS element, one cluster), on copies of the state
+        import numpy as _np
+        offs_h = w.offsets[s0:s1]
+        mus, Ls = [], []
+        for g in range(G):
+            X = offs_h[:, ch[go[g]:go[g + 1]], :].reshape(offs_h.shape[0], -1).astype(_np.float64)
+            C = _np.cov(X.T, bias=True) + 1e-4 * _np.eye(X.shape[1])
+            mus.append(X.mean(0))
+            Ls.append(_np.linalg.cholesky(C).ravel())
+        mu_d = torch.from_numpy(_np.concatenate(mus)).to(dev)
+        L_d = torch.from_numpy(_np.concatenate(Ls)).to(dev)
+        cl_d = torch.zeros(P, dtype=torch.int32, device=dev)
+        ctx.eval_full(off_d, obj_d, acc_d, cache_d)  # voxel-mode state of off_d (the Sobol run overwrote it)
+        mx_off, mx_acc, mx_obj, mx_tc = off_d.clone(), acc_d.clone(), obj_d.clone(), cache_d.clone()
+        mx_flags = torch.zeros((P, G), dtype=torch.uint8, device=dev)
 
-    def mix_once():
-        mx_off.copy_(off_d); mx_acc.copy_(acc_d); mx_obj.copy_(obj_d); mx_tc.copy_(cache_d)
-        ctx.mix_class(mx_off, mx_acc, mx_obj, mx_tc, go, ch, cl_d, mu_d, L_d, fixed_d, None, 0.0, 2024, 0, s0,
-                      mx_flags)
-    mix_once()  # first call allocates the mixing scratch
-    t_mix = timed(mix_once, reps=2)
-    mix_accept_frac = float(mx_flags.float().mean().item())
+        def mix_once():
+            mx_off.copy_(off_d); mx_acc.copy_(acc_d); mx_obj.copy_(obj_d); mx_tc.copy_(cache_d)
+            ctx.mix_class(mx_off, mx_acc, mx_obj, mx_tc, go, ch, cl_d, mu_d, L_d, fixed_d, None, 0.0, 2024, 0, s0,
+                          mx_flags)
+        mix_once()  # first call allocates the mixing scratch
+        t_mix = timed(mix_once, reps=2)
+        mix_accept_frac = float(mx_flags.float().mean().item())
 
     # ---- roofline of the dominant kernel (k_raster), SURVEY.md §8(d) algorithmic bytes
     peak, peak_src = measured_hbm_peak()
@@ -401,12 +411,12 @@ def main():
                 "full_evals_per_s": P * 1e3 / t_full, "full_ms": t_full,
                 "partial_evals_per_s": P * G * 1e3 / t_part, "partial_ms": t_part,
                 "partial_nocache_evals_per_s": P * G * 1e3 / t_part_nc,
-                "sobol_full_evals_per_s": P * 1e3 / t_sobol,
-                "sobol_full_ms": t_sobol,
-                "repair_population_ms": t_repair,
-                "mix_class_ms": t_mix,
-                "mix_class_evals_per_s": P * G * 1e3 / t_mix,
-                "mix_class_accept_frac": mix_accept_frac,
+                "sobol_full_evals_per_s": _fin(P * 1e3 / t_sobol),
+                "sobol_full_ms": _fin(t_sobol),
+                "repair_population_ms": _fin(t_repair),
+                "mix_class_ms": _fin(t_mix),
+                "mix_class_evals_per_s": _fin(P * G * 1e3 / t_mix),
+                "mix_class_accept_frac": _fin(mix_accept_frac),
                 "samples_per_launch": prof["samples"] / max(prof["launches"], 1),
                 "band_entries_per_launch": prof["band_entries"] / max(prof["launches"], 1),
                 "per_gpu_note": "breakdown figures are this rank's (per GPU)",
