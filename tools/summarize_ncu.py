@@ -32,11 +32,18 @@ for r in rows[h + 1:]:
     seq.append((int(r[iid]), name, t))
 tot = sum(sum(v) for v in per.values())
 out = [f"# ncu launch list ({os.path.basename(launches)}): gpu__time_duration.sum, --clock-control none,",
-       "# cold-cache serialised launches of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline`",
+       "# cold-cache serialised launches of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras`",
        f"# total {tot/1e6:.3f} ms over {len(seq)} launches", "",
        f"{'kernel':28s} {'launches':>8s} {'total ms':>10s} {'mean ms':>9s} {'share':>7s}"]
 for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
     out.append(f"{k:28s} {len(v):8d} {sum(v)/1e6:10.3f} {sum(v)/len(v)/1e6:9.3f} {100*sum(v)/tot:6.1f}%")
+load_time = {"k_distance_maps", "k_band_mask", "k_own_records", "k_validate_volume", "k_fill_int"}
+step_tot = sum(sum(v) for k, v in per.items() if k not in load_time and not k.startswith("void at::"))
+out += ["", "# share of the per-step kernels (load-time and torch fill kernels excluded)"]
+for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
+    if k in load_time or k.startswith("void at::"):
+        continue
+    out.append(f"{k:28s} {100*sum(v)/step_tot:6.1f}%")
 out += ["", "# launch sequence (id, kernel, ms)"] + [f"{i:5d} {n:28s} {t/1e6:10.4f}" for i, n, t in seq]
 open(os.path.join(prof, f"{tag}_launches.txt"), "w").write("\n".join(out) + "\n")
 
