@@ -1,0 +1,92 @@
+"""GPU edge cases (run with -m gpu): long rows that overflow one row-start
+bitmap window (more than 4096 samples per 32-row chunk), the minimum volume,
+sizes at the gather-texture limits of the layout, background-only volumes, and
+empty requests.  Same bar as tests/test_gpu_parity.py."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes, skipped there
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from synth import kuhn_lattice_mesh, random_tiny_mesh  # noqa: E402
+from tests.helpers import blob_volume, make_oracle  # noqa: E402
+from tests.test_gpu_parity import DEV, _assert_acc, _assert_obj, _ctx_raw, _gpu_full  # noqa: E402
+
+
+def _check(dims, I_s, I_t, base, tets, offs, cs=None, ct=None):
+    ctx = _ctx_raw(dims, I_s, I_t, base, tets, cs, ct)
+    orc = make_oracle(dims, I_s, I_t, base, tets, cs=cs, ct=ct)
+    obj, acc, _, _, _ = _gpu_full(ctx, offs)
+    for k in range(offs.shape[0]):
+        o_obj, o_acc = orc.eval(offs[k])
+        _assert_acc(acc[k], o_acc, f"sol {k}")
+        _assert_obj(obj[k], o_obj, f"sol {k}")
+    for side in (0, 1):
+        own = np.empty(ctx.V, np.int32)
+        ctx.owner_map(offs[-1], side, own)
+        assert np.array_equal(own, orc.owner_map(offs[-1], side))
+    return ctx
+
+
+def _offsets(base, P, seed, scale, fixed=None):
+    rng = np.random.default_rng(seed)
+    offs = np.round(rng.normal(0, scale, size=(P, len(base), 6)) * 1024) / 1024
+    if fixed is not None:
+        offs[:, fixed] = 0.0
+    offs[0] = 0.0
+    return offs.astype(np.float32)
+
+
+def test_long_rows_span_several_bitmap_windows():
+    """dims 700 x 6 x 5 with tets spanning hundreds of voxels in x: a 32-row chunk
+    holds > 4096 samples, so the row-start bitmap is swept in several windows."""
+    dims = (700, 6, 5)
+    g = [np.linspace(-0.5, d - 0.5, 3) for d in dims]
+    base, tets = kuhn_lattice_mesh(*g)
+    base = base.astype(np.float32)
+    hull = (np.abs(base + 0.5) < 1e-6) | (np.abs(base - (np.array(dims) - 0.5)) < 1e-6)
+    I_s = blob_volume(dims, 11)
+    I_t = blob_volume(dims, 12)
+    offs = _offsets(base, 4, 3, 0.4)
+    offs[:, :, :3][:, hull] = 0.0
+    offs[:, :, 3:][:, hull] = 0.0
+    _check(dims, I_s, I_t, base, tets, offs)
+
+
+def test_minimum_volume():
+    dims = (2, 2, 2)
+    base = np.array([[x, y, z] for z in (-0.5, 1.5) for y in (-0.5, 1.5) for x in (-0.5, 1.5)], np.float32)
+    from scipy.spatial import Delaunay
+    tets = Delaunay(base.astype(np.float64)).simplices.astype(np.int32)
+    I = np.array([0.0, 0.5, 0.25, 0.0, 1.0, 0.0, 0.75, 0.125], np.float32).reshape(2, 2, 2)
+    offs = np.zeros((2, 8, 6), np.float32)
+    offs[1, :, 3:] = 0.25
+    _check(dims, I, I[::-1].copy(), base, tets, offs)
+
+
+def test_background_only_and_guidance_pairs():
+    dims = (20, 18, 16)
+    base, tets = random_tiny_mesh(dims, 12, 5)
+    I0 = np.zeros(dims[::-1], np.float32)
+    rng = np.random.default_rng(4)
+    cs = [rng.uniform(3, 14, size=(30, 3)).astype(np.float32) for _ in range(3)]
+    ct = [(c + rng.normal(0, 0.5, size=c.shape)).astype(np.float32) for c in cs]
+    offs = _offsets(base, 3, 6, 0.2)
+    offs[:, :8] = 0.0
+    _check(dims, I0, I0, base, tets, offs, cs, ct)
+
+
+def test_empty_requests_are_noops(wl):
+    w = wl(1)
+    ctx = _ctx_raw(w.dims, w.I_s, w.I_t, w.base, w.tets)
+    obj = torch.full((1, 3), 7.0, dtype=torch.float64, device=DEV)
+    acc = torch.zeros((1, 6), dtype=torch.int64, device=DEV)
+    off = torch.zeros((0, w.N, 6), dtype=torch.float32, device=DEV)
+    ctx.eval_full(off, obj, acc, None)
+    ctx.eval_partial(off, acc, np.array([0], np.int32), np.zeros(0, np.int32), torch.zeros(0, device=DEV),
+                     None, obj, acc)
+    torch.cuda.synchronize()
+    assert float(obj[0, 0]) == 7.0
