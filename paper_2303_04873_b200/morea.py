@@ -126,7 +126,8 @@ class Context:
 
     def close(self):
         if getattr(self, "h", None):
-            _lib.morea_destroy(self.h)
+            if _lib is not None:  # the module may already be torn down at interpreter exit
+                _lib.morea_destroy(self.h)
             self.h = None
 
     def __del__(self):
