@@ -6,8 +6,8 @@
 //   a2 per-tet geometry + fold  k_setup (build_side, folds, severity)
 //   a3 magnitude                k_setup (magnitude)
 //   a4 ownership rasterizer     k_raster: row_interval() + raster() (exact intervals)
-//   a5 map + sample + h         k_raster: SampleFast / SampleGeneral (exact case split)
-//   a6 guidance term            k_raster: guidance() (band mask + trilinear of the other map)
+//   a5 map + sample + h         k_raster: Sample<>::sample (exact case split, exact_fg)
+//   a6 guidance term            k_raster: Sample<>::enqueue / entry (band bits, per-warp queue)
 //   a7 reductions               warp shuffles (fixed order), k_reduce
 //   a8 partial evaluation       version 0/1 items + k_reduce with base_acc
 //   a9 fold check               k_check_folds
@@ -15,11 +15,15 @@
 //
 // Work decomposition.  k_setup: one thread per (version, tet,
 // solution) computes the exact integer geometry of both sides (int64/int128)
-// and writes a 448-byte SideRec per side.  k_raster: persistent warps pull
-// items from a global queue in solution-minor order (consecutive items = same
-// tet, next solution, so gathered bricks stay L1/L2-resident; large tets
-// first).  Inside an item the 32 lanes compute the exact x-intervals of 32 bbox
-// rows, prefix-sum their lengths and sweep the flattened samples 32 at a time.
+// and writes a 384-byte SideRec per side.  k_raster: one 28-warp block per SM
+// pulls items from a global queue in solution-minor order, 28 at a time
+// (consecutive items = same tet, next solution, so the warps of an SM share
+// their texel and record footprints in L1; large tets first).  Inside an item
+// the 32 lanes compute the exact x-intervals of 32 bbox rows, prefix-sum their
+// lengths and sweep the flattened samples 32 at a time.
+// Further sm_100a kernels: morea_sobol*.cuh (NEXT-1 Sobol sampler),
+// morea_repair.cuh (NEXT-2 fold repair), morea_mix.cuh (NEXT-3 optimal
+// mixing), morea_export.cuh (NEXT-4 object counts and DVF).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -44,7 +48,7 @@
 #endif
 
 #ifndef MOREA_RASTER_MINB
-#define MOREA_RASTER_MINB 14  // resident 64-thread blocks per SM: 28 warps at 72 registers
+#define MOREA_RASTER_MINB 14  // MOREA_SM_BLOCK == 0 only: resident 2-warp blocks per SM
 #endif
 
 namespace morea {
@@ -486,8 +490,8 @@ __device__ __forceinline__ int warp_search(int incl, int idx) {
 // enumerated per z-slice over the slice's y range, 32 rows per step (lanes
 // compute the exact x-intervals); non-empty rows are compacted into shared
 // memory and their flattened samples are swept 32 per step.  A lane finds its
-// row from the mask of row starts inside the 32-sample window (one redux.or and
-// a popc).  Lanes past the end evaluate sample 0 of the last row with
+// row from the shared-memory bitmap of row starts: one broadcast word per
+// 32-sample window and a popc.  Lanes past the end evaluate sample 0 of the last row with
 // valid = false (no divergence).  All lanes of the warp must call it.
 template <class F>
 __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int loff, WarpSmem& S,
