@@ -301,6 +301,33 @@ def main():
     t_full = timed(lambda: ctx.eval_full(off_d, obj_d, acc_d, cache_d))
     t_part = timed(lambda: ctx.eval_partial(off_d, acc_d, go, ch, nv_d, cache_d, pobj_d, pacc_d))
     t_part_nc = timed(lambda: ctx.eval_partial(off_d, acc_d, go, ch, nv_d, None, pobj_d, pacc_d))
+    # partial-evaluation sweep over FOS sizes (BASELINE.json configs[3]):
+    # 1 edge, 4 and 16 edges of colour class `class_index`, the whole class as one
+    # group, all points as one group; cached old contributions; k_raster algorithmic
+    # GB/s of the call from the kernel's own counters and CUDA events
+    sweep = {}
+    peak, peak_src = measured_hbm_peak()
+    for kind in ("class", "edges4", "edges16", "wholeclass", "all"):
+        sgo, sch, snv = partial_request(w, plan, kind, args.class_index)
+        sG = len(sgo) - 1
+        snv_d = torch.from_numpy(snv[s0:s1].copy()).to(dev)
+        spo = torch.empty((P * sG, 3), dtype=torch.float64, device=dev)
+        spa = torch.empty((P * sG, 6), dtype=torch.int64, device=dev)
+        run = (lambda sgo=sgo, sch=sch, snv_d=snv_d, spo=spo, spa=spa:
+               ctx.eval_partial(off_d, acc_d, sgo, sch, snv_d, cache_d, spo, spa))
+        run()
+        torch.cuda.synchronize()
+        ctx.prof_enable(True)
+        ctx.prof_read()
+        t_k = timed(run)
+        sp = ctx.prof_read()
+        ctx.prof_enable(False)
+        sb = 8 * sp["samples"] + 12 * sp["band_entries"] + 32 * sp["items"]
+        gbs = sb / (sp["ms"] / 1e3) / 1e9 if sp["ms"] > 0 else None
+        sweep[kind] = {"groups": sG, "points_per_group": round(len(sch) / sG, 2),
+                       "evals_per_s": P * sG * 1e3 / t_k, "ms": t_k,
+                       "k_raster_gbs": gbs, "k_raster_frac": (gbs / peak) if gbs else None,
+                       "samples_per_eval": sp["samples"] / max(sp["launches"], 1) / (P * sG)}
     t_sobol = t_repair = t_mix = float("nan")
     mix_accept_frac = float("nan")
     if not args.no_extras:
@@ -338,7 +365,6 @@ def main():
         mix_accept_frac = float(mx_flags.float().mean().item())
 
     # ---- roofline of the dominant kernel (k_raster), SURVEY.md §8(d) algorithmic bytes
-    peak, peak_src = measured_hbm_peak()
     alg_bytes = 8 * prof["samples"] + 12 * prof["band_entries"] + 32 * prof["items"]
     achieved = alg_bytes / (prof["ms"] / 1e3) / 1e9 if prof["ms"] > 0 else None
     per_launch_bytes = alg_bytes / max(prof["launches"], 1)
@@ -419,6 +445,7 @@ def main():
                 "mix_class_accept_frac": _fin(mix_accept_frac),
                 "samples_per_launch": prof["samples"] / max(prof["launches"], 1),
                 "band_entries_per_launch": prof["band_entries"] / max(prof["launches"], 1),
+                "partial_fos_sweep": sweep,
                 "per_gpu_note": "breakdown figures are this rank's (per GPU)",
             },
         }

@@ -502,8 +502,9 @@ def partial_request(w: Workload, plan, kind="class", class_index=0, seed=31, sig
     """Build a multi-group partial-evaluation request (SURVEY.md §8(d) partial sweep).
 
     kind: "class" (each element of one colour class is a group of 2 points),
-    "edges4"/"edges16" (groups of 4/16 edges of one colour class), "all" (one
-    group with every point).  New values = base offsets + N(0, sigma^2) on all
+    "edges4"/"edges16" (groups of 4/16 edges of one colour class), "wholeclass"
+    (one group with every point of the colour class), "all" (one group with
+    every point).  New values = base offsets + N(0, sigma^2) on all
     6 coordinates (pinned hull coordinates unchanged).
     Returns (grp_off int32 (G+1,), changed_pts int32 (S,), new_vals float32 (P, S, 6)).
     """
@@ -513,7 +514,7 @@ def partial_request(w: Workload, plan, kind="class", class_index=0, seed=31, sig
     else:
         cls = plan["classes"][class_index % len(plan["classes"])]
         elems = plan["edges"][cls]
-        per = {"class": 1, "edges4": 4, "edges16": 16}[kind]
+        per = {"class": 1, "edges4": 4, "edges16": 16, "wholeclass": len(elems)}[kind]
         groups = []
         for i in range(0, len(elems), per):
             groups.append(np.unique(elems[i:i + per].ravel()))
