@@ -241,7 +241,6 @@ Volumes volumes_of(const morea_ctx* c) {
   v.fnx2 = (float)(c->nx - 2);
   v.fny2 = (float)(c->ny - 2);
   v.fnz2 = (float)(c->nz - 2);
-  v.fny = (float)c->ny;
   v.w = c->wts.as<double>();
   for (int s = 0; s < 2; s++)
     for (int i = 0; i < kMaxPairs; i++) v.wf[s][i] = c->r > 0 ? (float)(c->w[s][i] / c->r) : 0.f;
@@ -252,7 +251,11 @@ Volumes volumes_of(const morea_ctx* c) {
   v.use_tex = c->use_tex ? 1 : 0;
   v.texI = c->texI;
   v.texM = c->texM;
-  v.fnx = (float)c->nx;
+  const int pad = c->use_tex ? kTexPad : 0;
+  v.fnxp = (float)(c->nx + 2 * pad);
+  v.fnyp = (float)(c->ny + 2 * pad);
+  v.uoff0 = (float)(1 + pad);
+  v.voff = (float)((c->ny + 2 * pad) * pad + pad + 1);
   return v;
 }
 
@@ -471,20 +474,33 @@ void release_textures(morea_ctx* ctx) {
 }
 
 // `count` float volumes (nx x ny x nz, x-fastest, device) as one 2D gather
-// texture: volume j, voxel (x, y, z) -> texel (x + j nx, y + ny z).  Point
-// sampling, clamp, unnormalised coordinates.
+// texture with a one-voxel edge-replicated border (Volumes::texI): volume j,
+// voxel (x, y, z), x in [-1, nx] etc. -> texel (x + 1 + j (nx + 2),
+// y + 1 + (ny + 2)(z + 1)).  Point sampling, clamp, unnormalised coordinates.
 cudaError_t make_gather_texture(morea_ctx* ctx, const float* const* src, int count, cudaArray_t* arr,
                                 cudaTextureObject_t* tex) {
   cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
-  const size_t W = (size_t)ctx->nx * count, H = (size_t)ctx->ny * ctx->nz;
+  const size_t wp = (size_t)ctx->nx + 2 * kTexPad, hp = ((size_t)ctx->ny + 2 * kTexPad) * ((size_t)ctx->nz + 2 * kTexPad);
+#ifdef MOREA_TEX_ROUND
+  const size_t W = (wp * count + MOREA_TEX_ROUND - 1) / MOREA_TEX_ROUND * MOREA_TEX_ROUND,
+               H = (hp + MOREA_TEX_ROUND - 1) / MOREA_TEX_ROUND * MOREA_TEX_ROUND;
+#else
+  const size_t W = wp * count, H = hp;
+#endif
   cudaError_t e = cudaMallocArray(arr, &fd, W, H, cudaArrayTextureGather);
   if (e != cudaSuccess) return e;
-  for (int j = 0; j < count; j++) {
-    e = cudaMemcpy2DToArrayAsync(*arr, (size_t)j * ctx->nx * sizeof(float), 0, src[j],
-                                 ctx->nx * sizeof(float), ctx->nx * sizeof(float), H,
-                                 cudaMemcpyDeviceToDevice, ctx->stream);
-    if (e != cudaSuccess) return e;
+  float* padded = nullptr;
+  e = cudaMallocAsync((void**)&padded, wp * hp * sizeof(float), ctx->stream);
+  if (e != cudaSuccess) return e;
+  for (int j = 0; j < count && e == cudaSuccess; j++) {
+    e = launch_pad_volume(src[j], ctx->nx, ctx->ny, ctx->nz, kTexPad, padded, ctx->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DToArrayAsync(*arr, (size_t)j * wp * sizeof(float), 0, padded, wp * sizeof(float),
+                                   wp * sizeof(float), H, cudaMemcpyDeviceToDevice, ctx->stream);
   }
+  const cudaError_t ef = cudaFreeAsync(padded, ctx->stream);
+  if (e != cudaSuccess) return e;
+  if (ef != cudaSuccess) return ef;
   cudaResourceDesc rd;
   std::memset(&rd, 0, sizeof(rd));
   rd.resType = cudaResourceTypeArray;
@@ -506,7 +522,8 @@ cudaError_t build_textures(morea_ctx* ctx) {
   int gw = 0, gh = 0;
   cudaDeviceGetAttribute(&gw, cudaDevAttrMaxTexture2DGatherWidth, ctx->device);
   cudaDeviceGetAttribute(&gh, cudaDevAttrMaxTexture2DGatherHeight, ctx->device);
-  if ((long long)ctx->nx * 2 * std::max(ctx->K, 1) > gw || (long long)ctx->ny * ctx->nz > gh)
+  if (((long long)ctx->nx + 2 * kTexPad) * 2 * std::max(ctx->K, 1) > gw ||
+      ((long long)ctx->ny + 2 * kTexPad) * ((long long)ctx->nz + 2 * kTexPad) > gh)
     return cudaSuccess;
   const float* vols[2] = {ctx->I[0].as<float>(), ctx->I[1].as<float>()};
   cudaError_t e = make_gather_texture(ctx, vols, 2, &ctx->arrI, &ctx->texI);

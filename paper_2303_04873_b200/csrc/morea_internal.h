@@ -10,6 +10,10 @@
 namespace morea {
 
 constexpr int kMaxPairs = 8;
+#ifndef MOREA_TEX_PAD
+#define MOREA_TEX_PAD 1  // edge-replicated border of the gather textures (voxels; 0 or 1)
+#endif
+constexpr int kTexPad = MOREA_TEX_PAD;
 constexpr int kQLo = -256 * 1024;  // Q.10 window (O1)
 constexpr int kQHi = 768 * 1024;
 #ifndef MOREA_WARPS_PER_BLOCK
@@ -33,7 +37,9 @@ struct __align__(16) SideRec {
   float eps[3];               // fp32 position filter bound per axis (0 = exact axis)
   int flags;                  // bit 0: rasterize; bit 1: every position of the bbox is inside
                               // [0, n-1) with margin (no clamp needed); bit 2: every face is a
-                              // regular lower/upper face (fast row intervals)
+                              // regular lower/upper face (fast row intervals); bit 3: every
+                              // position is inside (-1, n) with margin (no clamp needed on the
+                              // edge-padded gather textures)
   float vy[4], vz[4];         // vertex y, z (voxel units, exact) for per-slice y ranges
   int lo[3], hi[3];           // lattice bbox clipped to the image
   int U[4][3];                // Q_other - Q_own per vertex
@@ -87,17 +93,24 @@ struct Volumes {
   const float* dmap[2];          // K * V fp32 per side
   int K;
   double r, inv_r;
-  float fnx2, fny2, fnz2, fny;  // (n - 2) per axis and ny as floats (constant-bank operands)
+  float fnx2, fny2, fnz2;  // (n - 2) per axis as floats (constant-bank operands)
   const double* w;  // device: w[side * kMaxPairs + i] = |C_i| / |G_side|
   float wf[2][kMaxPairs];  // w / r (fp32), in the parameter space
   float rf, rlo;           // r = rf + rlo (fp32 head and tail)
   // texture-gather path (0 when the layout exceeds the gather limits): volumes as
-  // tall 2D textures, voxel (x, y, z) of volume j -> texel (x + j nx, y + ny z),
-  // gathered 2x2 per slice (tld4).  texI: volumes I_s, I_t; texM: the 2K maps,
-  // side s pair i at j = s K + i.
+  // tall 2D textures with a one-voxel edge-replicated border, voxel (x, y, z) of
+  // volume j -> texel (x + 1 + j (nx + 2), y + 1 + (ny + 2)(z + 1)) for x in
+  // [-1, nx] etc. (indices clamped into the volume), gathered 2x2 per slice (tld4).
+  // texI: volumes I_s, I_t; texM: the 2K maps, side s pair i at j = s K + i.
+  // The border makes the O5 clamp implicit for positions in (-1, n): both
+  // corners of a footprint straddling the border carry the border value.
   unsigned long long texI;
   unsigned long long texM;
-  float fnx;  // nx as float (volume offset in the textures)
+  // gather coordinates of lower corner (ix, iy, iz) of volume j:
+  //   u = ix + uoff0 + j fnxp,  v = fmaf(iz, fnyp, iy) + voff,  next slice v + fnyp
+  // TEX: fnxp = nx + 2, fnyp = ny + 2, uoff0 = 2, voff = ny + 4 (padded layout);
+  // plain loads: fnxp = nx, fnyp = ny, uoff0 = 1, voff = 1 (u - 1, v - 1 = index)
+  float fnxp, fnyp, uoff0, voff;
   int use_tex;
   // Sobol sampler (NEXT-1): per side and voxel v, OR of the band bits of v + {0,1}^3
   // (clamped): the pairs whose interpolated distance can be < r in v's cell
@@ -148,6 +161,7 @@ cudaError_t launch_distance_maps(const float* pts, const long long* off, int K, 
                                  int nz, const double sp[3], float* dmap, cudaStream_t s);
 cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, unsigned char* band,
                              cudaStream_t s);
+cudaError_t launch_pad_volume(const float* src, int nx, int ny, int nz, int pad, float* dst, cudaStream_t s);
 cudaError_t launch_own_records(const float* I, const unsigned char* band, long long V, uint2* out,
                                cudaStream_t s);
 cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s);

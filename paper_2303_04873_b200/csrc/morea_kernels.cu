@@ -165,7 +165,8 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
 #pragma unroll
   for (int k = 0; k < 4; k++)
     elo[k] = 1024 * (G.nrm[k][0] * G.lo[0] + G.nrm[k][1] * G.lo[1] + G.nrm[k][2] * G.lo[2]) - G.cst[k];
-  bool inside = true;
+  bool inside = true;   // positions in [0, n-1) (plain-load path needs no clamp)
+  bool inside_p = true; // positions in (-1, n) (edge-padded textures need no clamp)
 #pragma unroll
   for (int a = 0; a < 3; a++) {
     bool exact = true;
@@ -183,36 +184,39 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
       // every vertex moves by the same U_a: x_a = q_a + U_a / 1024 exactly (fp32-exact)
       G.d0[a] = (float)G.U[0][a] * (1.0f / 1024.0f);
       G.eps[a] = 0.0f;
-      const double u = (double)G.U[0][a] / 1024.0;
-      if (!((double)G.lo[a] + u >= 1e-3 && (double)G.hi[a] + u <= (double)(dims[a] - 1) - 1e-3)) inside = false;
     } else {
       i128 N = 0;
 #pragma unroll
       for (int k = 0; k < 4; k++) N += (i128)elo[k] * (i128)G.U[k][a];
       const double d0 = (double)N / (1024.0 * (double)G.absdet);
       G.d0[a] = (float)d0;
-      double amax = 0.0, xmin = 1e300, xmax = -1e300;
+      double amax = 0.0;
 #pragma unroll
       for (int c = 0; c < 8; c++) {
         const double v = d0 + Aab[0] * ((c & 1) ? L[0] : 0.0) + Aab[1] * ((c & 2) ? L[1] : 0.0) +
                          Aab[2] * ((c & 4) ? L[2] : 0.0);
         amax = fmax(amax, fabs(v));
-        const double xq = v + (double)(((c >> a) & 1) ? G.hi[a] : G.lo[a]);
-        xmin = fmin(xmin, xq);
-        xmax = fmax(xmax, xq);
       }
-      // positions are affine over the bbox: extremes at its corners
-      if (!(xmin >= 1e-3 && xmax <= (double)(dims[a] - 1) - 1e-3)) inside = false;
       // fp32 error of d = fma(A_x0, k, d_row(fp32 fma chain)) and of frac(d):
       // <= 2^-24 (5 (|u|max + sum_b |A_ab| L_b) + 1); eps = 3x that
       const double bound = amax + fabs(Aab[0]) * L[0] + fabs(Aab[1]) * L[1] + fabs(Aab[2]) * L[2] + 1.0;
       G.eps[a] = (float)ldexp(bound, -19);
     }
+    // An owned sample q lies in the closed tet, so its exact position x = T(q)
+    // (a convex combination of the other side's vertices) lies in the other
+    // side's vertex bbox.  The margin covers the fp32 position error, so floor()
+    // of the fp32 position stays in range.
+    const int omn = min(min(Qo[0][a], Qo[1][a]), min(Qo[2][a], Qo[3][a]));
+    const int omx = max(max(Qo[0][a], Qo[1][a]), max(Qo[2][a], Qo[3][a]));
+    const double xmin = (double)omn / 1024.0, xmax = (double)omx / 1024.0;
+    const double mg = 1e-3 + 2.0 * (double)G.eps[a];
+    if (!(xmin >= mg && xmax <= (double)(dims[a] - 1) - mg)) inside = false;
+    if (!(xmin >= -1.0 + mg && xmax <= (double)dims[a] - mg)) inside_p = false;
   }
   bool regular = true;
 #pragma unroll
   for (int k = 0; k < 4; k++) regular = regular && (G.ftype[k] == 1 || G.ftype[k] == -1);
-  G.flags = 1 | (inside ? 2 : 0) | (regular ? 4 : 0);
+  G.flags = 1 | (inside ? 2 : 0) | (regular ? 4 : 0) | (inside_p ? 8 : 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -616,6 +620,15 @@ __device__ __noinline__ bool exact_fg(const SideRec& R, int qx, int qy, int qz, 
   return false;
 }
 
+// all lanes of the warp call it (warp-uniform branch); lanes without an
+// ambiguous position keep their fg
+__device__ __noinline__ bool exact_fg_if(bool amb, bool fg, const SideRec& R, int qx, int qy, int qz,
+                                         float dx, float dy, float dz, const float* __restrict__ vol,
+                                         int nx, int ny, int nz) {
+  if (!amb) return fg;
+  return exact_fg(R, qx, qy, qz, dx, dy, dz, vol, nx, ny, nz);
+}
+
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 
 // Positivity-exact lerp: (1 - t) a + t b as fma(t, b, (1 - t) a).  For a, b >= 0
@@ -640,7 +653,7 @@ struct Acc {
   int qn;       // band entries in the per-warp queue (warp-uniform)
 };
 
-template <bool TEX, int SIDE_T>
+template <bool TEX, int SIDE_T, bool CLAMP>
 struct Sample {
   const Volumes& V;
   const SideRec& R;
@@ -649,8 +662,10 @@ struct Sample {
   const float4& sc1;  // shared: (0.5 - eps_y, 0.5 - eps_z, uoff, -): ambiguity thresholds on
                       // |f - 0.5|; uoff = texel x offset of corner i0 + 1 in the gather layout
   Acc& acc;
-  bool clamp;         // some position of the item may leave [0, n-1): apply the O5 clamp
   int side;           // runtime side when SIDE_T < 0 (warp-uniform)
+  // CLAMP: some position of the item may leave the range the gather covers
+  // exactly, apply the O5 clamp (a separate instantiation: no predicated clamp
+  // instructions in the common loop)
 
   // per-side data selected by a warp-uniform branch on compile-time parameter
   // offsets, so texture handles stay in uniform registers
@@ -661,7 +676,7 @@ struct Sample {
                                          float u, float v, int base, float c[8]) const {
     if (TEX) {
       const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v, 0);
-      const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v + V.fny, 0);
+      const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v + V.fnyp, 0);
       // gather order: (x0,y1) (x1,y1) (x1,y0) (x0,y0)
       c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
       c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
@@ -677,7 +692,7 @@ struct Sample {
   // tld4 pair (slices i0_z and i0_z + 1); u carries the volume's x offset
   __device__ __forceinline__ void gather_tex(float u, float v, float c[8]) const {
     const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texI, u, v, 0);
-    const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texI, u, v + V.fny, 0);
+    const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texI, u, v + V.fnyp, 0);
     // gather order: (x0,y1) (x1,y1) (x1,y0) (x0,y0)
     c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
     c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
@@ -706,10 +721,10 @@ struct Sample {
     } else
 #endif
     if (TEX) {
-      // u = i0_x + 1 + o nx (texel of I_o); map (o, i) is volume o K + i of texM
-      const float uu = fmaf((float)(o * (V.K - 1) + i), V.fnx, u);
+      // u = i0_x + uoff0 + o fnxp (texel of I_o); map (o, i) is volume o K + i of texM
+      const float uu = fmaf((float)(o * (V.K - 1) + i), V.fnxp, u);
       const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texM, uu, v, 0);
-      const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texM, uu, v + V.fny, 0);
+      const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texM, uu, v + V.fnyp, 0);
       e[0] = g0.w; e[1] = g0.z; e[2] = g0.x; e[3] = g0.y;
       e[4] = g1.w; e[5] = g1.z; e[6] = g1.x; e[7] = g1.y;
     } else {
@@ -802,7 +817,7 @@ struct Sample {
     const bool amb = (fabsf(fx - 0.5f) > s0.w) | (fabsf(fy - 0.5f) > s1.x) | (fabsf(fz - 0.5f) > s1.y);
     // lattice corner i0 as exact floats (< 2^24)
     float ix = rb.y + kf + flx, iy = rb.z + fly, iz = rb.w + flz;
-    if (clamp) {  // warp-uniform
+    if (CLAMP) {
       // O5 clamp: x <= 0 -> (0, f = 0), x >= n-1 -> (n-2, f = 1)
       fx = ix < 0.f ? 0.f : (ix > V.fnx2 ? 1.f : fx);
       fy = iy < 0.f ? 0.f : (iy > V.fny2 ? 1.f : fy);
@@ -812,15 +827,18 @@ struct Sample {
       iz = fminf(fmaxf(iz, 0.f), V.fnz2);
     }
     const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
-    // texel coordinates of corner i0 + (1, 1) in the (x, y + ny z) layout (exact floats)
-    const float u = ix + s1.z, v = fmaf(iz, V.fny, iy) + 1.0f;
+    // gather coordinates of corner i0 (Volumes::fnxp; exact floats)
+    const float u = ix + s1.z, v = fmaf(iz, V.fnyp, iy) + V.voff;
     const int base = TEX ? 0 : ((int)iz * ny + (int)iy) * nx + (int)ix;
     float c[8];
     if (TEX) gather_tex(u, v, c);
     else gather(vol(OTH), 0ull, u, v, base, c);
     const float b = tri(c, fx, fy, fz, gx, gy, gz);
     bool fg = b > 0.f;
-    if (amb) fg = exact_fg(R, (int)rb.y + k, (int)rb.z, (int)rb.w, dx, dy, dz, vol(OTH), nx, ny, nz);
+    // warp-uniform branch around the rare exact path: no convergence barrier
+    // (BSSY/BMOV/BSYNC) in the common path (measured 2% faster)
+    if (__any_sync(FULLMASK, amb))
+      fg = exact_fg_if(amb, fg, R, (int)rb.y + k, (int)rb.z, (int)rb.w, dx, dy, dz, vol(OTH), nx, ny, nz);
     // h of PAPER.md §4.1.2 (L318-322) with the exact case split (O6)
     float h;
     if (a > 0.f && fg) {
@@ -867,14 +885,23 @@ __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int l
   const SideRec& R = S.R;
   if (lane == 0) {
     S.sc0 = make_float4(R.A[0][0], R.A[1][0], R.A[2][0], 0.5f - R.eps[0]);
-    // texel x of corner i0 + 1: I_o is volume o of texI (TEX), else a plain index
-    const float uoff = 1.0f + (TEX ? (float)((1 - (SIDE_T >= 0 ? SIDE_T : side)) * V.nx) : 0.0f);
+    // gather x of corner i0: I_o is volume o of texI (TEX), else a plain index + 1
+    const float uoff = TEX ? fmaf((float)(1 - (SIDE_T >= 0 ? SIDE_T : side)), V.fnxp, V.uoff0) : 1.0f;
     S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], uoff, 0.f);
   }
   __syncwarp();
-  Sample<TEX, SIDE_T> f{V, R, S, S.sc0, S.sc1, acc, (R.flags & 2) == 0, side};
-  raster(R, V.nx, V.ny, (SIDE_T >= 0 ? SIDE_T : side) * (int)V.V, S, lane, f);
-  f.drain(SIDE_T >= 0 ? SIDE_T : side);
+  // O5 clamp only where a position can leave the range the gather covers exactly:
+  // [0, n-1) for plain loads, (-1, n) on the edge-padded textures (warp-uniform)
+  const int loff = (SIDE_T >= 0 ? SIDE_T : side) * (int)V.V;
+  if ((R.flags & ((TEX && kTexPad) ? 8 : 2)) == 0) {
+    Sample<TEX, SIDE_T, true> f{V, R, S, S.sc0, S.sc1, acc, side};
+    raster(R, V.nx, V.ny, loff, S, lane, f);
+    f.drain(SIDE_T >= 0 ? SIDE_T : side);
+  } else {
+    Sample<TEX, SIDE_T, false> f{V, R, S, S.sc0, S.sc1, acc, side};
+    raster(R, V.nx, V.ny, loff, S, lane, f);
+    f.drain(SIDE_T >= 0 ? SIDE_T : side);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1294,6 +1321,23 @@ __global__ void k_own_records(const float* __restrict__ I, const unsigned char* 
   for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
        v += (long long)gridDim.x * blockDim.x)
     out[v] = make_uint2(__float_as_uint(I[v]), band ? (unsigned)band[v] : 0u);
+}
+
+// edge-padded copy of one volume for the gather textures (Volumes::texI):
+// dst (nx+2p) x (ny+2p) x (nz+2p), dst(x+p, y+p, z+p) = src(clamp(x), clamp(y), clamp(z))
+__global__ void k_pad_volume(const float* __restrict__ src, int nx, int ny, int nz, int pad,
+                             float* __restrict__ dst) {
+  const long long wp = nx + 2 * pad, hp = ny + 2 * pad, n = wp * hp * (long long)(nz + 2 * pad);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(t % wp) - pad, y = (int)((t / wp) % hp) - pad, z = (int)(t / (wp * hp)) - pad;
+    const int cx = min(max(x, 0), nx - 1), cy = min(max(y, 0), ny - 1), cz = min(max(z, 0), nz - 1);
+    dst[t] = src[((long long)cz * ny + cy) * nx + cx];
+  }
+}
+
+cudaError_t launch_pad_volume(const float* src, int nx, int ny, int nz, int pad, float* dst, cudaStream_t s) {
+  k_pad_volume<<<1184, 256, 0, s>>>(src, nx, ny, nz, pad, dst);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_own_records(const float* I, const unsigned char* band, long long V, uint2* out,

@@ -131,9 +131,9 @@ __device__ __forceinline__ float sb_trilinear(const Volumes& V, unsigned long lo
                                               const SbPos& P) {
   float c[8];
   if (TEX) {
-    const float u = P.ix + uoff, v = fmaf(P.iz, V.fny, P.iy) + 1.0f;
+    const float u = P.ix + uoff, v = fmaf(P.iz, V.fnyp, P.iy) + V.voff;
     const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v, 0);
-    const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v + V.fny, 0);
+    const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v + V.fnyp, 0);
     c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
     c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
   } else {
@@ -219,8 +219,9 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
       const bool clamp = !(R.flags & 2);
       const unsigned m0 = R.mask[0] ^ xlo[0], m1 = R.mask[1] ^ xlo[1], m2 = R.mask[2] ^ xlo[2],
                      m3 = R.mask[3] ^ xlo[3];
-      const float uoffS = 1.0f + (TEX ? (float)side * V.fnx : 0.f);
-      const float uoffO = 1.0f + (TEX ? (float)oth * V.fnx : 0.f);
+      // (immediate offsets: cheap to rematerialise, so the compiler does not spill them)
+      const float uoffS = TEX ? fmaf((float)side, V.fnxp, 1.0f + (float)kTexPad) : 1.0f;
+      const float uoffO = TEX ? fmaf((float)oth, V.fnxp, 1.0f + (float)kTexPad) : 1.0f;
       const float* volS = side == 0 ? V.I[0] : V.I[1];
       const float* volO = side == 0 ? V.I[1] : V.I[0];
       const unsigned char* dil = side == 0 ? V.dil[0] : V.dil[1];
@@ -278,8 +279,8 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
             bm &= bm - 1;
             float d, Dp;
             if (TEX) {
-              d = sb_trilinear<true>(V, V.texM, nullptr, 1.0f + (float)(side * V.K + pi) * V.fnx, Pp);
-              Dp = sb_trilinear<true>(V, V.texM, nullptr, 1.0f + (float)(oth * V.K + pi) * V.fnx, Pt);
+              d = sb_trilinear<true>(V, V.texM, nullptr, fmaf((float)(side * V.K + pi), V.fnxp, 1.0f + (float)kTexPad), Pp);
+              Dp = sb_trilinear<true>(V, V.texM, nullptr, fmaf((float)(oth * V.K + pi), V.fnxp, 1.0f + (float)kTexPad), Pt);
             } else {
               d = sb_trilinear<false>(V, 0ull, (side == 0 ? V.dmap[0] : V.dmap[1]) + (long long)pi * V.V,
                                       1.0f, Pp);

@@ -90,3 +90,27 @@ def test_empty_requests_are_noops(wl):
                      None, obj, acc)
     torch.cuda.synchronize()
     assert float(obj[0, 0]) == 7.0
+
+
+def test_border_band_positions_nonzero_border():
+    """Positions in (-1, 0) and (n-1, n) on every axis read the one-voxel replicated
+    border of the gather textures without the explicit clamp (O5 through the
+    padding); positions beyond it take the clamping instantiation.  Volumes and
+    distance maps are non-zero at the border, so a wrong border texel shows."""
+    dims = (20, 18, 16)
+    base, tets = random_tiny_mesh(dims, 14, 8)
+    I_s = blob_volume(dims, 21, frac_zero=0.2)
+    I_t = blob_volume(dims, 22, frac_zero=0.2)
+    rng = np.random.default_rng(9)
+    cs = [rng.uniform(0, 15, size=(40, 3)).astype(np.float32) for _ in range(2)]
+    ct = [(c + rng.normal(0, 0.7, size=c.shape)).astype(np.float32) for c in cs]
+    N = len(base)
+    offs = np.zeros((6, N, 6), np.float32)
+    offs[1] = _offsets(base, 2, 10, 0.25)[1]
+    offs[1, :8] = 0.0                       # interior moves, hull at the image extent
+    offs[2, :, 3:] = [0.4375, -0.6875, 0.9375]   # translation inside the border band
+    offs[3, :, :3] = [-0.875, 0.8125, -0.5]      # same on the source side
+    offs[4, :, 3:] = [2.25, -1.5, 3.0]           # beyond the band: clamp instantiation
+    offs[5] = offs[1]
+    offs[5, :, 3:] += np.array([0.3125, -0.25, 0.1875], np.float32)  # generic map into the band
+    _check(dims, I_s, I_t, base, tets, offs, cs, ct)
