@@ -37,7 +37,7 @@ out = [f"# ncu launch list ({os.path.basename(launches)}): gpu__time_duration.su
        f"{'kernel':28s} {'launches':>8s} {'total ms':>10s} {'mean ms':>9s} {'share':>7s}"]
 for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
     out.append(f"{k:28s} {len(v):8d} {sum(v)/1e6:10.3f} {sum(v)/len(v)/1e6:9.3f} {100*sum(v)/tot:6.1f}%")
-load_time = {"k_distance_maps", "k_band_mask", "k_own_records", "k_validate_volume", "k_fill_int"}
+load_time = {"k_distance_maps", "k_band_mask", "k_own_records", "k_validate_volume", "k_fill_int", "k_pad_volume", "k_dilate_band"}
 step_tot = sum(sum(v) for k, v in per.items() if k not in load_time and not k.startswith("void at::"))
 out += ["", "# share of the per-step kernels (load-time and torch fill kernels excluded)"]
 for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
