@@ -364,6 +364,26 @@ def main():
         t_mix = timed(mix_once, reps=2)
         mix_accept_frac = float(mx_flags.float().mean().item())
 
+    # plain-load path (volumes beyond the 2D gather-texture limits, e.g. 512 x 512 x 128):
+    # the same full evaluation with MOREA_NO_TEX on a second context
+    t_plain = float("nan")
+    if not args.no_extras:
+        os.environ["MOREA_NO_TEX"] = "1"
+        ctx_plain = morea.Context.from_workload(w, device=local_rank)
+        del os.environ["MOREA_NO_TEX"]
+        stream_plain = torch.cuda.ExternalStream(ctx_plain.stream_handle, device=dev)
+        ctx_plain.eval_full(off_d, obj_d, acc_d, None)
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream_plain)
+        for _ in range(3):
+            ctx_plain.eval_full(off_d, obj_d, acc_d, None)
+        a1.record(stream_plain)
+        torch.cuda.synchronize()
+        t_plain = a0.elapsed_time(a1) / 3
+        ctx_plain.close()
+
     # ---- roofline of the dominant kernel (k_raster), SURVEY.md §8(d) algorithmic bytes
     alg_bytes = 8 * prof["samples"] + 12 * prof["band_entries"] + 32 * prof["items"]
     achieved = alg_bytes / (prof["ms"] / 1e3) / 1e9 if prof["ms"] > 0 else None
@@ -446,6 +466,8 @@ def main():
                 "samples_per_launch": prof["samples"] / max(prof["launches"], 1),
                 "band_entries_per_launch": prof["band_entries"] / max(prof["launches"], 1),
                 "partial_fos_sweep": sweep,
+                "plain_load_full_evals_per_s": _fin(P * 1e3 / t_plain),
+                "plain_load_full_ms": _fin(t_plain),
                 "per_gpu_note": "breakdown figures are this rank's (per GPU)",
             },
         }

@@ -114,3 +114,49 @@ def test_border_band_positions_nonzero_border():
     offs[5] = offs[1]
     offs[5, :, 3:] += np.array([0.3125, -0.25, 0.1875], np.float32)  # generic map into the band
     _check(dims, I_s, I_t, base, tets, offs, cs, ct)
+
+
+def test_plain_load_path_parity(wl, monkeypatch):
+    """Volumes beyond the 2D gather-texture limits (e.g. 512 x 512 x 128: (ny+2)(nz+2)
+    rows > 32768) run k_raster / k_sobol with plain loads and the explicit O5 clamp.
+    MOREA_NO_TEX forces that path on C2: full and partial evaluation, owner maps and
+    the Sobol sampler against the oracle."""
+    from oracle.oracle import Oracle
+    from paper_2303_04873_b200 import morea
+    from synth import fos_plan, partial_request
+    w = wl(2)
+    monkeypatch.setenv("MOREA_NO_TEX", "1")
+    ctx = morea.Context.from_workload(w, device=0)
+    orc = Oracle.from_workload(w)
+    obj, acc, tc, off, acc_d = _gpu_full(ctx, w.offsets, cache=True)
+    sols = (0, 1, 7, 23, w.P - 1)
+    for k in sols:
+        o_obj, o_acc = orc.eval(w.offsets[k])
+        _assert_acc(acc[k], o_acc, f"plain C2 sol {k}")
+        _assert_obj(obj[k], o_obj, f"plain C2 sol {k}")
+    for side in (0, 1):
+        own = np.empty(ctx.V, np.int32)
+        ctx.owner_map(w.offsets[1], side, own)
+        assert np.array_equal(own, orc.owner_map(w.offsets[1], side))
+    plan = fos_plan(w.tets, w.N)
+    go, ch, nv = partial_request(w, plan, "edges4", 0)
+    G = len(go) - 1
+    pobj = torch.empty((w.P * G, 3), dtype=torch.float64, device=DEV)
+    pacc = torch.empty((w.P * G, 6), dtype=torch.int64, device=DEV)
+    ctx.eval_partial(off, acc_d, go, ch, torch.from_numpy(nv).to(DEV), torch.from_numpy(tc).to(DEV), pobj, pacc)
+    torch.cuda.synchronize()
+    p_obj, p_acc = pobj.cpu().numpy(), morea.acc_to_numpy(pacc)
+    for k in (1, 7):
+        base_o = orc.eval(w.offsets[k])[1]
+        for g in (0, G - 1):
+            S = ch[go[g]:go[g + 1]]
+            o_obj, o_acc = orc.eval_partial(w.offsets[k], base_o, S, nv[k, go[g]:go[g + 1]])
+            _assert_acc(p_acc[k * G + g], o_acc, f"plain partial sol {k} group {g}")
+            _assert_obj(p_obj[k * G + g], o_obj, f"plain partial sol {k} group {g}")
+    ctx.set_sampler(morea.SAMPLER_SOBOL, 1.0)
+    orc.set_sampler(morea.SAMPLER_SOBOL, 1.0)
+    obj, acc, _, _, _ = _gpu_full(ctx, w.offsets[:8])
+    for k in (0, 1, 5):
+        o_obj, o_acc = orc.eval(w.offsets[k])
+        _assert_acc(acc[k], o_acc, f"plain Sobol sol {k}")
+        _assert_obj(obj[k], o_obj, f"plain Sobol sol {k}")
