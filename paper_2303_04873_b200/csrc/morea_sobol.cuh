@@ -182,7 +182,6 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
       xlo[j] = v;
     }
   }
-  const unsigned vlane[4] = {sV[0][lane], sV[1][lane], sV[2][lane], sV[3][lane]};
   const long long per_v = (long long)A.n_entries * A.P;
   const long long n_items = per_v * A.n_raster_versions;
   if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0ull;
@@ -227,15 +226,19 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
       const unsigned char* dil = side == 0 ? V.dil[0] : V.dil[1];
       float hf = 0.f, gf = 0.f;
       int step = 0;
+      // S2: x(g(s0)) ^ x(g(lane)) ^ mask, updated per step: for s0 = 32 m,
+      // g(s0 + 32) ^ g(s0) = 2^4 ^ 2^(5 + ctz(m + 1)), so two direction numbers
+      // per dimension change (warp-uniform)
+      unsigned x0 = m0, x1 = m1, x2 = m2, x3 = m3;
 #pragma unroll 1
       for (long long s0 = 0; s0 < N; s0 += 32) {
-        // S2: x(g(s0)) by one XOR reduction per dimension (bit b of g(s0) <-> lane b)
-        const unsigned long long gs = (unsigned long long)s0 ^ ((unsigned long long)s0 >> 1);
-        const bool bit = (gs >> lane) & 1ull;
-        const unsigned x0 = __reduce_xor_sync(FULLMASK, bit ? vlane[0] : 0u) ^ m0;
-        const unsigned x1 = __reduce_xor_sync(FULLMASK, bit ? vlane[1] : 0u) ^ m1;
-        const unsigned x2 = __reduce_xor_sync(FULLMASK, bit ? vlane[2] : 0u) ^ m2;
-        const unsigned x3 = __reduce_xor_sync(FULLMASK, bit ? vlane[3] : 0u) ^ m3;
+        if (s0 > 0) {
+          const int b = 4 + __ffs((int)(s0 >> 5));  // 5 + ctz(m + 1), m + 1 = s0 / 32
+          x0 ^= sV[0][4] ^ sV[0][b];
+          x1 ^= sV[1][4] ^ sV[1][b];
+          x2 ^= sV[2][4] ^ sV[2][b];
+          x3 ^= sV[3][4] ^ sV[3][b];
+        }
         const bool valid = s0 + lane < N;
         // S5/S7 fast path: e = -lg2 u (the ln 2 factor cancels in the normalisation)
         const float e0 = -__log2f(fmaf((float)x0, 0x1.0p-32f, 0x1.0p-33f));
