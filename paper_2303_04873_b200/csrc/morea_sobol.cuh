@@ -125,6 +125,18 @@ __device__ __forceinline__ bool sb_locate(float x, float y, float z, const float
   return amb;
 }
 
+// all lanes call it (warp-uniform branch); lanes with ex = false keep fab
+// (bit 0: a > 0, bit 1: b > 0)
+__device__ __noinline__ unsigned exact_sobol_if(bool ex, unsigned fab, const SobolRec& R, unsigned x0, unsigned x1,
+                                                unsigned x2, unsigned x3, const float* volS, const float* volO,
+                                                int nx, int ny, int nz) {
+  if (!ex) return fab;
+  const unsigned xm[4] = {x0, x1, x2, x3};
+  bool fa, fb;
+  exact_sobol(R, xm, volS, volO, nx, ny, nz, fa, fb);
+  return (fa ? 1u : 0u) | (fb ? 2u : 0u);
+}
+
 template <bool TEX>
 __device__ __forceinline__ float sb_trilinear(const Volumes& V, unsigned long long tex,
                                               const float* __restrict__ vol, float uoff,
@@ -261,9 +273,14 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
         const float a = sb_trilinear<TEX>(V, V.texI, volS, uoffS, Pp);
         const float b = sb_trilinear<TEX>(V, V.texI, volO, uoffO, Pt);
         bool fa = a > 0.f, fb = b > 0.f;
-        if ((amb || A.sobol_force_exact) && valid) {
-          const unsigned xm[4] = {x0, x1, x2, x3};
-          exact_sobol(R, xm, volS, volO, V.nx, V.ny, V.nz, fa, fb);
+        // warp-uniform branch around the rare exact path: no convergence barrier
+        // in the common loop
+        const bool ex = (amb || A.sobol_force_exact) && valid;
+        if (__any_sync(FULLMASK, ex)) {
+          const unsigned fab = exact_sobol_if(ex, (fa ? 1u : 0u) | (fb ? 2u : 0u), R, x0, x1, x2, x3, volS,
+                                              volO, V.nx, V.ny, V.nz);
+          fa = fab & 1u;
+          fb = (fab >> 1) & 1u;
         }
         // h with both cases decided exactly (S8)
         const float h = (fa && fb) ? (a - b) * (a - b) : ((!fa && !fb) ? 0.f : 1.f);
