@@ -528,17 +528,26 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       const unsigned ne = __ballot_sync(FULLMASK, len > 0);
       const int start = incl - len;
       __syncwarp();
-      if (len > 0) {
+      {
+        // every lane computes its row record; lanes with a non-empty row store it
+        // (predicated stores: no divergent branch)
         const int c = __popc(ne & lt_mask);
         const float ox = (float)(xl - R.lo[0]), oy = (float)(y - R.lo[1]), oz = (float)(z - R.lo[2]);
         float4 drow;
         drow.x = fmaf(R.A[0][2], oz, fmaf(R.A[0][1], oy, fmaf(R.A[0][0], ox, R.d0[0])));
         drow.y = fmaf(R.A[1][2], oz, fmaf(R.A[1][1], oy, fmaf(R.A[1][0], ox, R.d0[1])));
         drow.z = fmaf(R.A[2][2], oz, fmaf(R.A[2][1], oy, fmaf(R.A[2][0], ox, R.d0[2])));
-        drow.w = 0.f;
-        S.row_a[c] = make_int4(start, (z * ny + y) * nx + xl + loff, __float_as_int(drow.x),
-                               __float_as_int(drow.y));
-        S.row_b[c] = make_float4(drow.z, (float)xl, (float)y, (float)z);
+        const unsigned ra_addr = (unsigned)__cvta_generic_to_shared(&S.row_a[c]);
+        const unsigned rb_addr = (unsigned)__cvta_generic_to_shared(&S.row_b[c]);
+        asm volatile(
+            "{\n .reg .pred p;\n setp.gt.s32 p, %0, 0;\n"
+            " @p st.shared.v4.b32 [%1], {%3, %4, %5, %6};\n"
+            " @p st.shared.v4.f32 [%2], {%7, %8, %9, %10};\n}"
+            :
+            : "r"(len), "r"(ra_addr), "r"(rb_addr), "r"(start), "r"((z * ny + y) * nx + xl + loff),
+              "r"(__float_as_int(drow.x)), "r"(__float_as_int(drow.y)), "f"(drow.z), "f"((float)xl),
+              "f"((float)y), "f"((float)z)
+            : "memory");
       }
       f.count_only(lane == 0 ? total : 0);
 #if MOREA_ABLATE == 6
@@ -554,7 +563,9 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       for (int base = 0; base < total; base += 32 * kStartWords) {
         const int nw = min(kStartWords, (total - base + 31) >> 5);
         __syncwarp();
-        for (int w = lane; w < nw; w += 32) S.starts[w] = 0u;
+        // clear the whole bitmap window: one 16-byte store per lane
+        static_assert(kStartWords == 128, "one uint4 per lane clears the window");
+        reinterpret_cast<uint4*>(S.starts)[lane] = make_uint4(0u, 0u, 0u, 0u);
         __syncwarp();
         if (len > 0 && start >= base && start < base + 32 * kStartWords)
           atomicOr(&S.starts[(start - base) >> 5], 1u << (start & 31));
@@ -753,15 +764,25 @@ struct Sample {
 #if MOREA_ABLATE == 9
       if (lane == 0) S.stat[2] += 1;
 #endif
-      if (bm) {
+      {
+        // computed by every lane, stored by lanes with a bit: predicated stores,
+        // no divergent branch (no convergence barrier per round)
         const int i = __ffs(bm) - 1;
         const int pos = acc.qn + __popc(take & ((1u << lane) - 1u));
-        S.qa[pos] = make_float4(u, v, fx, fy);
-        S.qb[pos] = make_int4(__float_as_int(fz), lin, i, 0);
-        bm &= bm - 1;
+        const unsigned qa_addr = (unsigned)__cvta_generic_to_shared(&S.qa[pos]);
+        const unsigned qb_addr = (unsigned)__cvta_generic_to_shared(&S.qb[pos]);
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n"
+            " @p st.shared.v4.f32 [%1], {%3, %4, %5, %6};\n"
+            " @p st.shared.v4.b32 [%2], {%7, %8, %9, %10};\n}"
+            :
+            : "r"(bm), "r"(qa_addr), "r"(qb_addr), "f"(u), "f"(v), "f"(fx), "f"(fy),
+              "r"(__float_as_int(fz)), "r"(lin), "r"(i), "r"(0)
+            : "memory");
+        bm &= bm - 1u;
       }
       acc.qn += __popc(take);
-      if (acc.qn >= 32) {
+      if (__all_sync(FULLMASK, acc.qn >= 32)) {  // warp-uniform (VOTE): no BSSY
         acc.qn -= 32;
         __syncwarp();
         const float4 ea = S.qa[acc.qn + lane];
