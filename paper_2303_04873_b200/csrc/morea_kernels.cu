@@ -395,12 +395,21 @@ __device__ __noinline__ void row_interval_exact(const SideRec& R, int y, int z, 
   }
 }
 
+// all lanes call it (warp-uniform branch); lanes with ex = false keep (xl, xh)
+__device__ __noinline__ int2 row_interval_exact_if(bool ex, const SideRec& R, int y, int z, int xl, int xh) {
+  if (ex) row_interval_exact(R, y, z, xl, xh);
+  return make_int2(xl, xh);
+}
+
 // Fast path for items whose four faces are regular (n_x != 0, small crossing
 // error bound): four fp32 crossings; the exact routine only when a crossing is
-// within its bound of an integer.
-__device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, int& xl, int& xh) {
-  if (!(R.flags & 4)) {
-    row_interval_exact(R, y, z, xl, xh);
+// within its bound of an integer.  Warp-collective: every lane calls it (rv:
+// the lane's row is real), the exact routine runs under a warp-uniform branch.
+__device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, bool rv, int& xl, int& xh) {
+  if (__all_sync(FULLMASK, !(R.flags & 4))) {  // item-uniform (R in shared memory)
+    const int2 r = row_interval_exact_if(rv, R, y, z, R.lo[0], R.hi[0]);
+    xl = r.x;
+    xh = r.y;
     return;
   }
   const int lo = R.lo[0], hi = R.hi[0];
@@ -419,12 +428,14 @@ __device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, int
     if (tk[k] > 0) l = max(l, c);
     else h = min(h, c - 1);
   }
-  if (amb) {
-    row_interval_exact(R, y, z, xl, xh);
-    return;
-  }
   xl = l;
   xh = h;
+  amb = amb && rv;
+  if (__any_sync(FULLMASK, amb)) {
+    const int2 r = row_interval_exact_if(amb, R, y, z, xl, xh);
+    xl = r.x;
+    xh = r.y;
+  }
 }
 
 // Conservative y range of the tet's cross-section with the plane z (exact
@@ -503,9 +514,9 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
   const unsigned lt_mask = (1u << lane) - 1u;
   for (int z0 = R.lo[2]; z0 <= R.hi[2]; z0 += 32) {
     const int zl = z0 + lane;
-    int ylo = 0, yhi = -1;
-    if (zl <= R.hi[2]) slice_y_range(R, zl, ylo, yhi);
-    const int cnt = max(0, yhi - ylo + 1);
+    int ylo, yhi;
+    slice_y_range(R, zl, ylo, yhi);  // every lane (no divergent call); masked below
+    const int cnt = zl <= R.hi[2] ? max(0, yhi - ylo + 1) : 0;
     const int zincl = warp_incl_scan(cnt, lane);
     const int nrows = __shfl_sync(FULLMASK, zincl, 31);
     for (int r0 = 0; r0 < nrows; r0 += 32) {
@@ -514,14 +525,12 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       const int zinc = __shfl_sync(FULLMASK, zincl, zp);
       const int zcnt = __shfl_sync(FULLMASK, cnt, zp);
       const int zylo = __shfl_sync(FULLMASK, ylo, zp);
-      int len = 0, xl = 0;
+      int xl, xh;
       const int z = z0 + zp;
       const int y = zylo + (r - (zinc - zcnt));
-      if (r < nrows) {
-        int xh;
-        row_interval(R, y, z, xl, xh);
-        len = max(0, xh - xl + 1);
-      }
+      const bool rv = r < nrows;
+      row_interval(R, y, z, rv, xl, xh);  // every lane (warp-collective)
+      const int len = rv ? max(0, xh - xl + 1) : 0;
       const int incl = warp_incl_scan(len, lane);
       const int total = __shfl_sync(FULLMASK, incl, 31);
       if (total == 0) continue;
