@@ -579,10 +579,20 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
         if (len > 0 && start >= base && start < base + 32 * kStartWords)
           atomicOr(&S.starts[(start - base) >> 5], 1u << (start & 31));
         __syncwarp();
+#if MOREA_PREFETCH_M
+        // the next bitmap word is loaded one step ahead (off the critical path;
+        // S.starts[128] reads the first word of row_a, never used)
+        unsigned Mn = S.starts[0];
+#endif
         for (int w0 = 0; w0 < nw; w0 += 16) {
           const int wend = min(nw, w0 + 16);
           for (int w = w0; w < wend; w++) {
+#if MOREA_PREFETCH_M
+            const unsigned M = Mn;
+            Mn = S.starts[w + 1];
+#else
             const unsigned M = S.starts[w];
+#endif
             const int row = rprev + __popc(M & le_mask);
             rprev += __popc(M);
             const int idx = base + (w << 5) + lane;
