@@ -59,7 +59,8 @@ struct __align__(16) SobolRec {
   unsigned mask[4];         // digital-shift masks (S3/S4)
   long long N;              // samples of this side (S6)
   float epsA, epsB;         // fast-path position error bound eps = epsA / s + epsB, s = sum -lg2 u
-  int flags;                // bit 0: N > 0; bit 1: every vertex of both sides inside [0, n-1]
+  int flags;                // bit 0: N > 0; bit 1: every vertex of both sides inside [0, n-1];
+                            // bit 2: ... inside [-1 + 1/16, n - 1/16] (edge-padded textures)
   int pad;
 };
 static_assert(sizeof(SobolRec) <= sizeof(SideRec), "SobolRec must fit a SideRec slot");

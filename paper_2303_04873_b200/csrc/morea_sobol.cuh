@@ -137,6 +137,20 @@ __device__ __noinline__ unsigned exact_sobol_if(bool ex, unsigned fab, const Sob
   return (fa ? 1u : 0u) | (fb ? 2u : 0u);
 }
 
+// O5 clamp of a located position (corner into [0, n-2], weights 0 / 1 outside)
+__device__ __forceinline__ void sb_clamp(const Volumes& V, SbPos& P) {
+  P.fx = P.ix < 0.f ? 0.f : (P.ix > V.fnx2 ? 1.f : P.fx);
+  P.fy = P.iy < 0.f ? 0.f : (P.iy > V.fny2 ? 1.f : P.fy);
+  P.fz = P.iz < 0.f ? 0.f : (P.iz > V.fnz2 ? 1.f : P.fz);
+  P.ix = fminf(fmaxf(P.ix, 0.f), V.fnx2);
+  P.iy = fminf(fmaxf(P.iy, 0.f), V.fny2);
+  P.iz = fminf(fmaxf(P.iz, 0.f), V.fnz2);
+}
+
+// SobolRec bit 2 keeps every vertex 2 kSbPadEps inside (-1, n); a sample whose
+// fp32 error bound exceeds kSbPadEps is clamped
+constexpr float kSbPadEps = 0x1.0p-5f;
+
 template <bool TEX>
 __device__ __forceinline__ float sb_trilinear(const Volumes& V, unsigned long long tex,
                                               const float* __restrict__ vol, float uoff,
@@ -227,7 +241,10 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
       const long long N = R.N;
       n_tot += N;
       if (side == 0) n_side0 = N;
-      const bool clamp = !(R.flags & 2);
+      // O5 clamp only where a position can leave the range the gathers cover
+      // exactly: [0, n-1] vertices for plain loads, (-1, n) (bit 2) on the
+      // edge-padded textures; warp-uniform, so the common path skips the clamp
+      const bool clamp = !(R.flags & ((TEX && kTexPad) ? 4 : 2));
       const unsigned m0 = R.mask[0] ^ xlo[0], m1 = R.mask[1] ^ xlo[1], m2 = R.mask[2] ^ xlo[2],
                      m3 = R.mask[3] ^ xlo[3];
       // (immediate offsets: cheap to rematerialise, so the compiler does not spill them)
@@ -268,8 +285,22 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
         const float ty = fmaf(l3, R.Do[2][1], fmaf(l2, R.Do[1][1], fmaf(l1, R.Do[0][1], R.x0o[1])));
         const float tz = fmaf(l3, R.Do[2][2], fmaf(l2, R.Do[1][2], fmaf(l1, R.Do[0][2], R.x0o[2])));
         SbPos Pp, Pt;
-        bool amb = sb_locate(px, py, pz, R.i0, eps, clamp, V, Pp);
-        amb = sb_locate(tx, ty, tz, R.i0o, eps, clamp, V, Pt) || amb;
+        bool amb;
+        if (__all_sync(FULLMASK, !clamp)) {
+          amb = sb_locate(px, py, pz, R.i0, eps, false, V, Pp);
+          amb = sb_locate(tx, ty, tz, R.i0o, eps, false, V, Pt) || amb;
+          // the no-clamp flag holds for positions within kSbPadEps of the exact
+          // ones; a larger fp32 error bound (sum e tiny: never in practice) clamps
+          if (__any_sync(FULLMASK, eps > kSbPadEps)) {
+            if (eps > kSbPadEps) {
+              sb_clamp(V, Pp);
+              sb_clamp(V, Pt);
+            }
+          }
+        } else {
+          amb = sb_locate(px, py, pz, R.i0, eps, true, V, Pp);
+          amb = sb_locate(tx, ty, tz, R.i0o, eps, true, V, Pt) || amb;
+        }
         const float a = sb_trilinear<TEX>(V, V.texI, volS, uoffS, Pp);
         const float b = sb_trilinear<TEX>(V, V.texI, volO, uoffO, Pt);
         bool fa = a > 0.f, fb = b > 0.f;

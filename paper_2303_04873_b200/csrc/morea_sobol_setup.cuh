@@ -75,7 +75,8 @@ __device__ void build_sobol(const int Q[4][3], const int Qo[4][3], const Volumes
 #pragma unroll
   for (int j = 0; j < 4; j++) R.mask[j] = (unsigned)(sb_splitmix64(seed + (unsigned long long)j) >> 32);
   const int dims[3] = {V.nx, V.ny, V.nz};
-  bool inside = true;
+  bool inside = true;    // every vertex of both sides in [0, n-1]
+  bool inside_p = true;  // ... in [-1 + 1/16, n - 1/16]: no clamp on the edge-padded textures
   float dmax = 0.f;
 #pragma unroll
   for (int k = 0; k < 4; k++)
@@ -85,6 +86,8 @@ __device__ void build_sobol(const int Q[4][3], const int Qo[4][3], const Volumes
       R.Qo[k][a] = Qo[k][a];
       inside = inside && Q[k][a] >= 0 && Q[k][a] <= 1024 * (dims[a] - 1) && Qo[k][a] >= 0 &&
                Qo[k][a] <= 1024 * (dims[a] - 1);
+      inside_p = inside_p && Q[k][a] >= -1024 + 64 && Q[k][a] <= 1024 * dims[a] - 64 &&
+                 Qo[k][a] >= -1024 + 64 && Qo[k][a] <= 1024 * dims[a] - 64;
     }
 #pragma unroll
   for (int a = 0; a < 3; a++) {
@@ -109,6 +112,6 @@ __device__ void build_sobol(const int Q[4][3], const int Qo[4][3], const Volumes
   // <= 1.5 2^-23 (1 + 3 D).  eps = 2x the bound, as epsA / s + epsB.
   R.epsA = 2.0f * dmax * 0x1.0p-19f;
   R.epsB = 2.0f * (dmax * 0x1.0p-21f + 1.5f * 0x1.0p-23f * (1.0f + 3.0f * dmax));
-  R.flags = (R.N > 0 ? 1 : 0) | (inside ? 2 : 0);
+  R.flags = (R.N > 0 ? 1 : 0) | (inside ? 2 : 0) | (inside_p ? 4 : 0);
   R.pad = 0;
 }
