@@ -475,6 +475,7 @@ struct WarpSmem {
   int4 row_a[32];    // (exclusive prefix, linear index of row start, dx0, dy0 as float bits)
   float4 row_b[32];  // (dz0, xl, y, z): fp32 displacement z at the row start, row start as floats
   float4 sc0, sc1;   // per-side sample constants (see Sample)
+  int4 slices[32];   // non-empty z-slices of the current 32-slice chunk: (first row, ylo, slice, -)
   unsigned long long stat[3];  // samples, band entries, items of this warp (profiling)
   // band-entry queue of the guidance term (a6): entries are evaluated 32 at a time
   float4 qa[kQueueCap];  // (u, v, fx, fy): footprint texel coordinates and weights
@@ -490,16 +491,6 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
   return v;
 }
 
-// index of the first lane whose inclusive prefix exceeds idx (idx < total)
-__device__ __forceinline__ int warp_search(int incl, int idx) {
-  int pos = 0;
-#pragma unroll
-  for (int b = 16; b; b >>= 1) {
-    const int v = __shfl_sync(FULLMASK, incl, pos + b - 1);
-    if (v <= idx) pos += b;
-  }
-  return pos;
-}
 
 // Generic rasterizer: visits every owned sample of the side.  Rows are
 // enumerated per z-slice over the slice's y range, 32 rows per step (lanes
@@ -519,15 +510,31 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
     const int cnt = zl <= R.hi[2] ? max(0, yhi - ylo + 1) : 0;
     const int zincl = warp_incl_scan(cnt, lane);
     const int nrows = __shfl_sync(FULLMASK, zincl, 31);
+    // non-empty slices of the chunk, compacted: (first row, ylo, slice) by rank
+    const int zstart = zincl - cnt;
+    const bool zne = cnt > 0;
+    {
+      const unsigned nem = __ballot_sync(FULLMASK, zne);
+      const unsigned addr = (unsigned)__cvta_generic_to_shared(&S.slices[__popc(nem & lt_mask)]);
+      __syncwarp();
+      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.shared.v4.b32 [%1], {%2, %3, %4, %5};\n}"
+                   :
+                   : "r"((unsigned)zne), "r"(addr), "r"(zstart), "r"(ylo), "r"(lane), "r"(0)
+                   : "memory");
+      __syncwarp();
+    }
+    const unsigned le_mask0 = (2u << lane) - 1u;
     for (int r0 = 0; r0 < nrows; r0 += 32) {
       const int r = r0 + lane;
-      const int zp = warp_search(zincl, min(r, nrows - 1));
-      const int zinc = __shfl_sync(FULLMASK, zincl, zp);
-      const int zcnt = __shfl_sync(FULLMASK, cnt, zp);
-      const int zylo = __shfl_sync(FULLMASK, ylo, zp);
+      // the lane's slice: rank = (non-empty slices starting before r0) + (slice
+      // starts in [r0, r]) - 1, from one OR-reduction of start bits and a ballot
+      const unsigned sb = __reduce_or_sync(
+          FULLMASK, (zne && zstart >= r0 && zstart < r0 + 32) ? (1u << (zstart - r0)) : 0u);
+      const int before = __popc(__ballot_sync(FULLMASK, zne && zstart < r0));
+      const int4 sl = S.slices[before + __popc(sb & le_mask0) - 1];
       int xl, xh;
-      const int z = z0 + zp;
-      const int y = zylo + (r - (zinc - zcnt));
+      const int z = z0 + sl.z;
+      const int y = sl.y + (r - sl.x);
       const bool rv = r < nrows;
       row_interval(R, y, z, rv, xl, xh);  // every lane (warp-collective)
       const int len = rv ? max(0, xh - xl + 1) : 0;
