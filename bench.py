@@ -65,24 +65,36 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([v.strip() for v in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.1)
+        # one nvidia-smi in loop mode (a sample every 50 ms) rather than one process
+        # per sample, so a sub-second timed region still gets several samples
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                           "--format=csv,noheader,nounits", "-lms", "50"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            for line in self._proc.stdout:
+                if self._stop.is_set():
+                    break
+                line = line.strip()
+                if line:
+                    self.samples.append([v.strip() for v in line.split(",")])
+        except Exception:
+            pass
 
     def __enter__(self):
+        self._proc = None
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.3)  # first sample before the timed region starts
         return self
 
     def __exit__(self, *a):
         self._stop.set()
+        if getattr(self, "_proc", None) is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
         self._t.join(timeout=10)
 
     def summary(self):
