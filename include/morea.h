@@ -183,7 +183,8 @@ int morea_eval_partial(morea_ctx *ctx, int pop, const float *base_offsets,
  *    the guidance term uses d = trilinear D_i^side(p).  Readings S1..S9 in
  *    DESIGN.md §3.  f_int / f_guid normalise by the total sample count.  The
  *    coverage flag is not computed in this mode.
- * rate must be > 0 and finite.  Takes effect for the following morea_eval_*
+ * rate must be in (0, 8]: per-tet sample counts are 32-bit (a tet inside the
+ * Q.10 window spans at most 1.8e8 voxels).  Takes effect for the following morea_eval_*
  * calls (morea_owner_map always uses the voxel-centre rasterizer).
  * Errors: EINVAL (bad mode / rate), ESTATE (before morea_create finished). */
 int morea_set_sampler(morea_ctx *ctx, int mode, double rate);

@@ -945,7 +945,7 @@ int morea_set_sampler(morea_ctx* ctx, int mode, double rate) {
   if (!ctx) return MOREA_EINVAL;
   if (mode != MOREA_SAMPLER_VOXEL && mode != MOREA_SAMPLER_SOBOL)
     return fail(ctx, MOREA_EINVAL, "unknown sampler mode %d", mode);
-  if (!(rate > 0.0) || !std::isfinite(rate)) return fail(ctx, MOREA_EINVAL, "rate must be > 0 and finite");
+  if (!(rate > 0.0 && rate <= 8.0)) return fail(ctx, MOREA_EINVAL, "rate must be in (0, 8] (32-bit per-tet counts)");
   CK(cudaSetDevice(ctx->device));
   ctx->sampler = mode;
   ctx->rate = rate;

@@ -128,12 +128,11 @@ __device__ __forceinline__ bool sb_locate(float x, float y, float z, const float
 // all lanes call it (warp-uniform branch); lanes with ex = false keep fab
 // (bit 0: a > 0, bit 1: b > 0)
 __device__ __noinline__ unsigned exact_sobol_if(bool ex, unsigned fab, const SobolRec& R, unsigned x0, unsigned x1,
-                                                unsigned x2, unsigned x3, const float* volS, const float* volO,
-                                                int nx, int ny, int nz) {
+                                                unsigned x2, unsigned x3, const Volumes& V, int side) {
   if (!ex) return fab;
   const unsigned xm[4] = {x0, x1, x2, x3};
   bool fa, fb;
-  exact_sobol(R, xm, volS, volO, nx, ny, nz, fa, fb);
+  exact_sobol(R, xm, V.I[side], V.I[1 - side], V.nx, V.ny, V.nz, fa, fb);
   return (fa ? 1u : 0u) | (fb ? 2u : 0u);
 }
 
@@ -250,8 +249,9 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
       // (immediate offsets: cheap to rematerialise, so the compiler does not spill them)
       const float uoffS = TEX ? fmaf((float)side, V.fnxp, 1.0f + (float)kTexPad) : 1.0f;
       const float uoffO = TEX ? fmaf((float)oth, V.fnxp, 1.0f + (float)kTexPad) : 1.0f;
-      const float* volS = side == 0 ? V.I[0] : V.I[1];
-      const float* volO = side == 0 ? V.I[1] : V.I[0];
+      // plain-load path only (TEX: the pointers are not kept live in the loop)
+      const float* volS = TEX ? nullptr : (side == 0 ? V.I[0] : V.I[1]);
+      const float* volO = TEX ? nullptr : (side == 0 ? V.I[1] : V.I[0]);
       const unsigned char* dil = side == 0 ? V.dil[0] : V.dil[1];
       float hf = 0.f, gf = 0.f;
       int step = 0;
@@ -259,16 +259,17 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
       // g(s0 + 32) ^ g(s0) = 2^4 ^ 2^(5 + ctz(m + 1)), so two direction numbers
       // per dimension change (warp-uniform)
       unsigned x0 = m0, x1 = m1, x2 = m2, x3 = m3;
+      const int Ni = (int)N;  // < 2^31: rate <= 8 (morea_set_sampler)
 #pragma unroll 1
-      for (long long s0 = 0; s0 < N; s0 += 32) {
+      for (int s0 = 0; s0 < Ni; s0 += 32) {
         if (s0 > 0) {
-          const int b = 4 + __ffs((int)(s0 >> 5));  // 5 + ctz(m + 1), m + 1 = s0 / 32
+          const int b = 4 + __ffs(s0 >> 5);  // 5 + ctz(m + 1), m + 1 = s0 / 32
           x0 ^= sV[0][4] ^ sV[0][b];
           x1 ^= sV[1][4] ^ sV[1][b];
           x2 ^= sV[2][4] ^ sV[2][b];
           x3 ^= sV[3][4] ^ sV[3][b];
         }
-        const bool valid = s0 + lane < N;
+        const bool valid = s0 + lane < Ni;
         // S5/S7 fast path: e = -lg2 u (the ln 2 factor cancels in the normalisation)
         const float e0 = -__log2f(fmaf((float)x0, 0x1.0p-32f, 0x1.0p-33f));
         const float e1 = -__log2f(fmaf((float)x1, 0x1.0p-32f, 0x1.0p-33f));
@@ -308,8 +309,7 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
         // in the common loop
         const bool ex = (amb || A.sobol_force_exact) && valid;
         if (__any_sync(FULLMASK, ex)) {
-          const unsigned fab = exact_sobol_if(ex, (fa ? 1u : 0u) | (fb ? 2u : 0u), R, x0, x1, x2, x3, volS,
-                                              volO, V.nx, V.ny, V.nz);
+          const unsigned fab = exact_sobol_if(ex, (fa ? 1u : 0u) | (fb ? 2u : 0u), R, x0, x1, x2, x3, V, side);
           fa = fab & 1u;
           fb = (fab >> 1) & 1u;
         }
