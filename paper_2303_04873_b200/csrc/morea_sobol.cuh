@@ -125,15 +125,30 @@ __device__ __forceinline__ bool sb_locate(float x, float y, float z, const float
   return amb;
 }
 
-// all lanes call it (warp-uniform branch); lanes with ex = false keep fab
-// (bit 0: a > 0, bit 1: b > 0)
-__device__ __noinline__ unsigned exact_sobol_if(bool ex, unsigned fab, const SobolRec& R, unsigned x0, unsigned x1,
-                                                unsigned x2, unsigned x3, const Volumes& V, int side) {
-  if (!ex) return fab;
-  const unsigned xm[4] = {x0, x1, x2, x3};
-  bool fa, fb;
-  exact_sobol(R, xm, V.I[side], V.I[1 - side], V.nx, V.ny, V.nz, fa, fb);
-  return (fa ? 1u : 0u) | (fb ? 2u : 0u);
+// h from the values and the exact cases (S8)
+__device__ __forceinline__ float sb_h(float a, float b, bool fa, bool fb) {
+  return (fa && fb) ? (a - b) * (a - b) : ((!fa && !fb) ? 0.f : 1.f);
+}
+
+// all lanes call it (warp-uniform branch) and get h; lanes with ex = true take
+// the cases from the exact fp64 positions.  a and b are arguments, so no value
+// stays live across the call.
+__device__ __noinline__ float exact_sobol_h(bool ex, float a, float b, const SobolRec& R, unsigned x0, unsigned x1,
+                                            unsigned x2, unsigned x3, const Volumes& V, int side) {
+  bool fa = a > 0.f, fb = b > 0.f;
+  if (ex) {
+    const unsigned xm[4] = {x0, x1, x2, x3};
+    exact_sobol(R, xm, V.I[side], V.I[1 - side], V.nx, V.ny, V.nz, fa, fb);
+  }
+  return sb_h(a, b, fa, fb);
+}
+
+// -log2 u, u = (x + 1/2) 2^-32 >= 2^-33 (a normal float): MUFU.LG2 without the
+// compiler's denormal fix-up (ftz changes nothing for normal inputs)
+__device__ __forceinline__ float sb_neg_lg2(unsigned x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaf((float)x, 0x1.0p-32f, 0x1.0p-33f)));
+  return -r;
 }
 
 // O5 clamp of a located position (corner into [0, n-2], weights 0 / 1 outside)
@@ -271,10 +286,7 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
         }
         const bool valid = s0 + lane < Ni;
         // S5/S7 fast path: e = -lg2 u (the ln 2 factor cancels in the normalisation)
-        const float e0 = -__log2f(fmaf((float)x0, 0x1.0p-32f, 0x1.0p-33f));
-        const float e1 = -__log2f(fmaf((float)x1, 0x1.0p-32f, 0x1.0p-33f));
-        const float e2 = -__log2f(fmaf((float)x2, 0x1.0p-32f, 0x1.0p-33f));
-        const float e3 = -__log2f(fmaf((float)x3, 0x1.0p-32f, 0x1.0p-33f));
+        const float e0 = sb_neg_lg2(x0), e1 = sb_neg_lg2(x1), e2 = sb_neg_lg2(x2), e3 = sb_neg_lg2(x3);
         const float sum = ((e0 + e1) + e2) + e3;
         const float rs = __frcp_rn(sum);
         const float l1 = e1 * rs, l2 = e2 * rs, l3 = e3 * rs;
@@ -304,17 +316,12 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
         }
         const float a = sb_trilinear<TEX>(V, V.texI, volS, uoffS, Pp);
         const float b = sb_trilinear<TEX>(V, V.texI, volO, uoffO, Pt);
-        bool fa = a > 0.f, fb = b > 0.f;
-        // warp-uniform branch around the rare exact path: no convergence barrier
-        // in the common loop
+        // h with both cases decided exactly (S8); the rare
+        // exact path under a warp-uniform branch (no convergence barrier)
         const bool ex = (amb || A.sobol_force_exact) && valid;
-        if (__any_sync(FULLMASK, ex)) {
-          const unsigned fab = exact_sobol_if(ex, (fa ? 1u : 0u) | (fb ? 2u : 0u), R, x0, x1, x2, x3, V, side);
-          fa = fab & 1u;
-          fb = (fab >> 1) & 1u;
-        }
-        // h with both cases decided exactly (S8)
-        const float h = (fa && fb) ? (a - b) * (a - b) : ((!fa && !fb) ? 0.f : 1.f);
+        float h;
+        if (__any_sync(FULLMASK, ex)) h = exact_sobol_h(ex, a, b, R, x0, x1, x2, x3, V, side);
+        else h = sb_h(a, b, a > 0.f, b > 0.f);
         hf += valid ? h : 0.f;
         // a6 (S9): pairs whose distance can be < r in p's cell
         unsigned bm = 0u;
