@@ -503,6 +503,10 @@ template <class F>
 __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int loff, WarpSmem& S,
                                        int lane, F& f) {
   const unsigned lt_mask = (1u << lane) - 1u;
+#if MOREA_ABLATE == 13
+  f.count_only(1);
+  return;
+#endif
   for (int z0 = R.lo[2]; z0 <= R.hi[2]; z0 += 32) {
     const int zl = z0 + lane;
     int ylo, yhi;
@@ -524,6 +528,10 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       __syncwarp();
     }
     const unsigned le_mask0 = (2u << lane) - 1u;
+#if MOREA_ABLATE == 12
+    f.count_only(nrows);
+    continue;
+#endif
     for (int r0 = 0; r0 < nrows; r0 += 32) {
       const int r = r0 + lane;
       // the lane's slice: rank = (non-empty slices starting before r0) + (slice
@@ -536,7 +544,11 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       const int z = z0 + sl.z;
       const int y = sl.y + (r - sl.x);
       const bool rv = r < nrows;
+#if MOREA_ABLATE == 11
+      xl = R.lo[0] + (y & 1); xh = R.hi[0] - (z & 1);  // rows only, no interval arithmetic
+#else
       row_interval(R, y, z, rv, xl, xh);  // every lane (warp-collective)
+#endif
       const int len = rv ? max(0, xh - xl + 1) : 0;
       const int incl = warp_incl_scan(len, lane);
       const int total = __shfl_sync(FULLMASK, incl, 31);
@@ -566,7 +578,7 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
             : "memory");
       }
       f.count_only(lane == 0 ? total : 0);
-#if MOREA_ABLATE == 6
+#if MOREA_ABLATE == 6 || MOREA_ABLATE == 11
       continue;
 #endif
       // Sweep in windows of 32 kStartWords samples.  The bitmap holds the row

@@ -298,6 +298,11 @@ def test_api_errors():
     with pytest.raises(morea.MoreaError) as e:
         c.set_mesh(flat, np.array([[0, 1, 2, 3]], np.int32))
     assert e.value.code == -3
+    # Sobol rate outside (0, 8]: per-tet point counts must stay 32-bit
+    for bad_rate in (0.0, -1.0, 8.5, float("inf"), float("nan")):
+        with pytest.raises(morea.MoreaError) as e:
+            c.set_sampler(morea.SAMPLER_SOBOL, bad_rate)
+        assert e.value.code == -1
     with pytest.raises(morea.MoreaError) as e:
         c.set_mesh(flat, np.array([[0, 1, 2, 9]], np.int32))
     assert e.value.code == -1
