@@ -121,15 +121,16 @@ def measured_hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """DRAM bytes per k_raster launch from the committed ncu --set full capture (or None)."""
+def ncu_summary():
+    """k_raster figures from the committed ncu --set full captures (profiles/ncu_summary.json):
+    DRAM bytes per launch (the roofline's `traffic`), L2 / L1-tex hit rates and issue
+    utilisation per captured launch (full, partial).  Empty dict if absent."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get("k_raster_dram_bytes_per_launch")
+            return json.load(f)
     except Exception:
-        return None
+        return {}
 
 
 # --------------------------------------------------------------------------- oracle (CPU) legs
@@ -400,7 +401,8 @@ def main():
     alg_bytes = 8 * prof["samples"] + 12 * prof["band_entries"] + 32 * prof["items"]
     achieved = alg_bytes / (prof["ms"] / 1e3) / 1e9 if prof["ms"] > 0 else None
     per_launch_bytes = alg_bytes / max(prof["launches"], 1)
-    traffic = ncu_traffic()
+    ncu = ncu_summary()
+    traffic = ncu.get("k_raster_dram_bytes_per_launch")
 
     # ---- e2e: the same step through the C-ABI with HOST buffers (pinned), copies inside
     off_h = torch.from_numpy(w.offsets[s0:s1].copy()).pin_memory()
@@ -459,7 +461,12 @@ def main():
                          "frac": (achieved / peak) if achieved else None,
                          "traffic": traffic, "kernel": "k_raster",
                          "algorithmic_bytes_per_launch": per_launch_bytes, "peak_source": peak_src,
-                         "launches": prof["launches"], "kernel_ms": prof["ms"]},
+                         "launches": prof["launches"], "kernel_ms": prof["ms"],
+                         "ncu": {"source": ncu.get("source"), "l2_hit_pct": ncu.get("k_raster_l2_hit_pct"),
+                                 "l1tex_hit_pct": ncu.get("k_raster_l1tex_hit_pct"),
+                                 "issue_active_pct": ncu.get("k_raster_issue_active_pct"),
+                                 "note": "per captured launch (full, cached partial); the kernel is "
+                                         "gather-latency bound, DESIGN.md §4.4"}},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},

@@ -89,9 +89,23 @@ for m in data:
         pass
     lines.append("")
 open(os.path.join(prof, f"{tag}_ncu_raster.txt"), "w").write("\n".join(lines) + "\n")
+def _num(m, k):
+    try:
+        v = float(m[k].replace(",", ""))
+        return v if v == v else None
+    except Exception:
+        return None
+
+
+rates = {k: [x for x in (_num(m, k) for m in data) if x is not None]
+         for k in ("lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
+                   "smsp__issue_active.avg.pct_of_peak_sustained_active")}
 summ = {"round": tag, "source": [os.path.basename(r) for r in reps],
         "k_raster_dram_bytes_per_launch": (sum(dram) / len(dram)) if dram else None,
-        "k_raster_dram_bytes_each": dram}
+        "k_raster_dram_bytes_each": dram,
+        "k_raster_l2_hit_pct": rates["lts__t_sector_hit_rate.pct"],
+        "k_raster_l1tex_hit_pct": rates["l1tex__t_sector_hit_rate.pct"],
+        "k_raster_issue_active_pct": rates["smsp__issue_active.avg.pct_of_peak_sustained_active"]}
 json.dump(summ, open(os.path.join(prof, "ncu_summary.json"), "w"), indent=1)
 print("\n".join(out[:14]))
 print("\n".join(lines[:60]))
