@@ -467,7 +467,9 @@ __device__ __noinline__ void slice_y_range(const SideRec& R, int z, int& ylo, in
 }
 
 constexpr int kQueueCap = 64;     // < 32 pending + one round of <= 32
-constexpr int kStartWords = 128;  // row-start bitmap window: 4096 samples
+// per-warp shared memory <= 3.5 KB, so the 28-warp block stays <= 99 KB (the
+// 100 KB carve-out step; see kRasterDynSmem)
+constexpr int kStartWords = 64;  // row-start bitmap window: 2048 samples
 
 struct WarpSmem {
   SideRec R;
@@ -475,11 +477,12 @@ struct WarpSmem {
   int4 row_a[32];    // (exclusive prefix, linear index of row start, dx0, dy0 as float bits)
   float4 row_b[32];  // (dz0, xl, y, z): fp32 displacement z at the row start, row start as floats
   float4 sc0, sc1;   // per-side sample constants (see Sample)
-  int4 slices[32];   // non-empty z-slices of the current 32-slice chunk: (first row, ylo, slice, -)
+  int2 slices[32];   // non-empty z-slices of the current 32-slice chunk: (first row, ylo | slice << 16)
   unsigned long long stat[3];  // samples, band entries, items of this warp (profiling)
   // band-entry queue of the guidance term (a6): entries are evaluated 32 at a time
   float4 qa[kQueueCap];  // (u, v, fx, fy): footprint texel coordinates and weights
-  int4 qb[kQueueCap];    // (fz bits, own linear index, pair i, -)
+  int2 qb[kQueueCap];    // (fz bits, own linear index)
+  unsigned char qi[kQueueCap];  // pair i
 };
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -521,9 +524,10 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       const unsigned nem = __ballot_sync(FULLMASK, zne);
       const unsigned addr = (unsigned)__cvta_generic_to_shared(&S.slices[__popc(nem & lt_mask)]);
       __syncwarp();
-      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.shared.v4.b32 [%1], {%2, %3, %4, %5};\n}"
+      // ylo < 768 (Q.10 window) and the slice index < 32 share one word
+      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.shared.v2.b32 [%1], {%2, %3};\n}"
                    :
-                   : "r"((unsigned)zne), "r"(addr), "r"(zstart), "r"(ylo), "r"(lane), "r"(0)
+                   : "r"((unsigned)zne), "r"(addr), "r"(zstart), "r"(ylo | (lane << 16))
                    : "memory");
       __syncwarp();
     }
@@ -539,10 +543,10 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       const unsigned sb = __reduce_or_sync(
           FULLMASK, (zne && zstart >= r0 && zstart < r0 + 32) ? (1u << (zstart - r0)) : 0u);
       const int before = __popc(__ballot_sync(FULLMASK, zne && zstart < r0));
-      const int4 sl = S.slices[before + __popc(sb & le_mask0) - 1];
+      const int2 sl = S.slices[before + __popc(sb & le_mask0) - 1];
       int xl, xh;
-      const int z = z0 + sl.z;
-      const int y = sl.y + (r - sl.x);
+      const int z = z0 + (sl.y >> 16);
+      const int y = (sl.y & 0xffff) + (r - sl.x);
       const bool rv = r < nrows;
 #if MOREA_ABLATE == 11
       xl = R.lo[0] + (y & 1); xh = R.hi[0] - (z & 1);  // rows only, no interval arithmetic
@@ -592,8 +596,8 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
         const int nw = min(kStartWords, (total - base + 31) >> 5);
         __syncwarp();
         // clear the whole bitmap window: one 16-byte store per lane
-        static_assert(kStartWords == 128, "one uint4 per lane clears the window");
-        reinterpret_cast<uint4*>(S.starts)[lane] = make_uint4(0u, 0u, 0u, 0u);
+        static_assert(kStartWords == 64, "one uint2 per lane clears the window");
+        reinterpret_cast<uint2*>(S.starts)[lane] = make_uint2(0u, 0u);
         __syncwarp();
         if (len > 0 && start >= base && start < base + 32 * kStartWords)
           atomicOr(&S.starts[(start - base) >> 5], 1u << (start & 31));
@@ -809,13 +813,15 @@ struct Sample {
         const int pos = acc.qn + __popc(take & ((1u << lane) - 1u));
         const unsigned qa_addr = (unsigned)__cvta_generic_to_shared(&S.qa[pos]);
         const unsigned qb_addr = (unsigned)__cvta_generic_to_shared(&S.qb[pos]);
+        const unsigned qi_addr = (unsigned)__cvta_generic_to_shared(&S.qi[pos]);
         asm volatile(
             "{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n"
-            " @p st.shared.v4.f32 [%1], {%3, %4, %5, %6};\n"
-            " @p st.shared.v4.b32 [%2], {%7, %8, %9, %10};\n}"
+            " @p st.shared.v4.f32 [%1], {%4, %5, %6, %7};\n"
+            " @p st.shared.v2.b32 [%2], {%8, %9};\n"
+            " @p st.shared.u8 [%3], %10;\n}"
             :
-            : "r"(bm), "r"(qa_addr), "r"(qb_addr), "f"(u), "f"(v), "f"(fx), "f"(fy),
-              "r"(__float_as_int(fz)), "r"(lin), "r"(i), "r"(0)
+            : "r"(bm), "r"(qa_addr), "r"(qb_addr), "r"(qi_addr), "f"(u), "f"(v), "f"(fx), "f"(fy),
+              "r"(__float_as_int(fz)), "r"(lin), "r"(i)
             : "memory");
         bm &= bm - 1u;
       }
@@ -824,8 +830,8 @@ struct Sample {
         acc.qn -= 32;
         __syncwarp();
         const float4 ea = S.qa[acc.qn + lane];
-        const int4 eb = S.qb[acc.qn + lane];
-        entry(ea.x, ea.y, ea.z, ea.w, __int_as_float(eb.x), eb.y, eb.z, s);
+        const int2 eb = S.qb[acc.qn + lane];
+        entry(ea.x, ea.y, ea.z, ea.w, __int_as_float(eb.x), eb.y, (int)S.qi[acc.qn + lane], s);
         __syncwarp();
       }
     }
@@ -846,8 +852,8 @@ struct Sample {
     __syncwarp();
     if (lane < acc.qn) {
       const float4 ea = S.qa[lane];
-      const int4 eb = S.qb[lane];
-      entry(ea.x, ea.y, ea.z, ea.w, __int_as_float(eb.x), eb.y, eb.z, s);
+      const int2 eb = S.qb[lane];
+      entry(ea.x, ea.y, ea.z, ea.w, __int_as_float(eb.x), eb.y, (int)S.qi[lane], s);
     }
     __syncwarp();
     acc.qn = 0;
@@ -1054,6 +1060,12 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
 }
 
 constexpr size_t kRasterDynSmem = MOREA_SM_BLOCK ? sizeof(WarpSmem) * kRasterBlockWarps : 0;
+// shared memory decides the L1/shared carve-out of the SM (steps 100, 132, ...
+// KB, 1 KB per block reserved by the system): at <= 99 KB the carve-out is
+// 100 KB and the texture/L1 cache keeps 156 KB (measured: 8 KB more shared
+// memory, crossing a step, costs 2.3%)
+static_assert(!MOREA_SM_BLOCK || kRasterDynSmem + 1024 + 64 <= 100 * 1024,
+              "k_raster shared memory above the 100 KB carve-out step");
 
 int raster_blocks_per_sm(bool tex) {
   if (kRasterDynSmem) {
