@@ -134,6 +134,20 @@ def ncu_summary():
 
 
 # --------------------------------------------------------------------------- oracle (CPU) legs
+def host_cpu():
+    """CPU model and hardware threads of the host the oracle runs on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"host_cpu": model, "host_threads": os.cpu_count()}
+
+
 def oracle_sample(w, plan_req, sols, n_partial):
     """Time the oracle as it stands on a bounded sample: per solution of `sols`,
     1 full + n_partial partial evaluations."""
@@ -184,7 +198,8 @@ def run_reference(args, rank, world):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(P_PER_GPU * world, G, world, args.class_index, w.T),
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                         **host_cpu()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -449,7 +464,7 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"solutions 1-4 of this C4 workload, each 1 full + {n_part} partial "
                          f"(1-edge groups, FOS class {args.class_index}) evaluations, single thread, "
-                         f"{dt:.1f} s"}
+                         f"{dt:.1f} s", **host_cpu()}
 
     if rank == 0:
         line = {
