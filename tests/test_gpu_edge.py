@@ -1,5 +1,5 @@
 """GPU edge cases (run with -m gpu): long rows that overflow one row-start
-bitmap window (more than 4096 samples per 32-row chunk), the minimum volume,
+bitmap window (more than 2048 samples per 32-row chunk), the minimum volume,
 sizes at the gather-texture limits of the layout, background-only volumes, and
 empty requests.  Same bar as tests/test_gpu_parity.py."""
 import numpy as np
@@ -42,7 +42,7 @@ def _offsets(base, P, seed, scale, fixed=None):
 
 def test_long_rows_span_several_bitmap_windows():
     """dims 700 x 6 x 5 with tets spanning hundreds of voxels in x: a 32-row chunk
-    holds > 4096 samples, so the row-start bitmap is swept in several windows."""
+    holds > 2048 samples (up to ~22 000), so the row-start bitmap is swept in several windows."""
     dims = (700, 6, 5)
     g = [np.linspace(-0.5, d - 0.5, 3) for d in dims]
     base, tets = kuhn_lattice_mesh(*g)
