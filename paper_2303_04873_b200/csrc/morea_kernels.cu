@@ -20,7 +20,12 @@
 // (consecutive items = same tet, next solution, so the warps of an SM share
 // their texel and record footprints in L1; large tets first).  Inside an item
 // the 32 lanes compute the exact x-intervals of 32 bbox rows, prefix-sum their
-// lengths and sweep the flattened samples 32 at a time.
+// lengths and sweep the flattened samples 32 at a time.  The other volume is
+// gathered with tld4 from edge-padded textures (the O5 clamp is needed only by
+// items whose other-side vertices leave (-1, n), a separate instantiation).
+// Hot paths carry no divergent branches: rare exact fallbacks sit behind
+// warp-uniform votes, shared-memory records are written with predicated
+// stores (DESIGN.md §4.4 lists what was measured and why).
 // Further sm_100a kernels: morea_sobol*.cuh (NEXT-1 Sobol sampler),
 // morea_repair.cuh (NEXT-2 fold repair), morea_mix.cuh (NEXT-3 optimal
 // mixing), morea_export.cuh (NEXT-4 object counts and DVF).
