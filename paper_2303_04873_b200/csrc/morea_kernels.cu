@@ -52,6 +52,10 @@
 #define MOREA_SOBOL_WARPS 28  // k_sobol: warps of its one block per SM
 #endif
 
+#ifndef MOREA_CARRY
+#define MOREA_CARRY 0  // 1: raster() carries the < 32-sample tail of a row chunk into the next
+#endif
+
 #ifndef MOREA_RASTER_MINB
 #define MOREA_RASTER_MINB 14  // MOREA_SM_BLOCK == 0 only: resident 2-warp blocks per SM
 #endif
@@ -507,6 +511,139 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 // row from the shared-memory bitmap of row starts: one broadcast word per
 // 32-sample window and a popc.  Lanes past the end evaluate sample 0 of the last row with
 // valid = false (no divergence).  All lanes of the warp must call it.
+#if MOREA_CARRY
+// Same enumeration, but a row chunk's last partial 32-sample step is not swept
+// with idle lanes: its rows (fewer than 32, since each has >= 1 sample) stay at
+// the front of the row table, rebased, and the next chunk's rows are appended
+// (that chunk computes 32 - carried rows).  Only the side's final step can be
+// partial.  The set of (row, sample) visits is unchanged.
+template <class F>
+__device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int loff, WarpSmem& S,
+                                       int lane, F& f) {
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const unsigned le_mask = (2u << lane) - 1u;
+  int z0 = R.lo[2] - 32, nrows = 0, r0 = 0, zstart = 0;
+  bool zne = false;
+  int pendS = 0, pendR = 0;  // samples / rows carried at the front of S.row_a, S.row_b
+  while (true) {
+    // next 32-slice z-chunk with rows left (warp-uniform)
+    while (r0 >= nrows && z0 + 32 <= R.hi[2]) {
+      z0 += 32;
+      r0 = 0;
+      const int zl = z0 + lane;
+      int ylo, yhi;
+      slice_y_range(R, zl, ylo, yhi);
+      const int cnt = zl <= R.hi[2] ? max(0, yhi - ylo + 1) : 0;
+      const int zincl = warp_incl_scan(cnt, lane);
+      nrows = __shfl_sync(FULLMASK, zincl, 31);
+      zstart = zincl - cnt;
+      zne = cnt > 0;
+      const unsigned nem = __ballot_sync(FULLMASK, zne);
+      const unsigned addr = (unsigned)__cvta_generic_to_shared(&S.slices[__popc(nem & lt_mask)]);
+      __syncwarp();
+      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.shared.v2.b32 [%1], {%2, %3};\n}"
+                   :
+                   : "r"((unsigned)zne), "r"(addr), "r"(zstart), "r"(ylo | (lane << 16))
+                   : "memory");
+      __syncwarp();
+    }
+    int total = pendS, nR = pendR;
+    if (r0 < nrows) {
+      const int fresh = 32 - pendR;  // lanes computing new rows
+      const int r = r0 + lane;
+      const unsigned sb = __reduce_or_sync(
+          FULLMASK, (zne && zstart >= r0 && zstart < r0 + 32) ? (1u << (zstart - r0)) : 0u);
+      const int before = __popc(__ballot_sync(FULLMASK, zne && zstart < r0));
+      const int2 sl = S.slices[before + __popc(sb & le_mask) - 1];
+      const int z = z0 + (sl.y >> 16);
+      const int y = (sl.y & 0xffff) + (r - sl.x);
+      const bool rv = r < nrows && lane < fresh;
+      int xl, xh;
+      row_interval(R, y, z, rv, xl, xh);
+      const int len = rv ? max(0, xh - xl + 1) : 0;
+      const int incl = warp_incl_scan(len, lane);
+      const int tot = __shfl_sync(FULLMASK, incl, 31);
+      const unsigned ne = __ballot_sync(FULLMASK, len > 0);
+      const int start = pendS + incl - len;
+      const int c = pendR + __popc(ne & lt_mask);
+      const float ox = (float)(xl - R.lo[0]), oy = (float)(y - R.lo[1]), oz = (float)(z - R.lo[2]);
+      float4 drow;
+      drow.x = fmaf(R.A[0][2], oz, fmaf(R.A[0][1], oy, fmaf(R.A[0][0], ox, R.d0[0])));
+      drow.y = fmaf(R.A[1][2], oz, fmaf(R.A[1][1], oy, fmaf(R.A[1][0], ox, R.d0[1])));
+      drow.z = fmaf(R.A[2][2], oz, fmaf(R.A[2][1], oy, fmaf(R.A[2][0], ox, R.d0[2])));
+      const unsigned ra_addr = (unsigned)__cvta_generic_to_shared(&S.row_a[c & 31]);
+      const unsigned rb_addr = (unsigned)__cvta_generic_to_shared(&S.row_b[c & 31]);
+      __syncwarp();
+      asm volatile(
+          "{\n .reg .pred p;\n setp.gt.s32 p, %0, 0;\n"
+          " @p st.shared.v4.b32 [%1], {%3, %4, %5, %6};\n"
+          " @p st.shared.v4.f32 [%2], {%7, %8, %9, %10};\n}"
+          :
+          : "r"(len), "r"(ra_addr), "r"(rb_addr), "r"(start), "r"((z * ny + y) * nx + xl + loff),
+            "r"(__float_as_int(drow.x)), "r"(__float_as_int(drow.y)), "f"(drow.z), "f"((float)xl),
+            "f"((float)y), "f"((float)z)
+          : "memory");
+      f.count_only(lane == 0 ? tot : 0);
+      total += tot;
+      nR += __popc(ne);
+      r0 += fresh;
+    }
+    // (few values live across the sweep: `last` is recomputed after it and the
+    // row starts are re-read from shared memory, measured against spills)
+    const int sweep = (r0 >= nrows && z0 + 32 > R.hi[2]) ? total : (total & ~31);
+    pendS = total - sweep;
+    __syncwarp();
+    int rprev = -1;
+    for (int base = 0; base < sweep; base += 32 * kStartWords) {
+      const int nw = min(kStartWords, (sweep - base + 31) >> 5);
+      __syncwarp();
+      static_assert(kStartWords == 64, "one uint2 per lane clears the window");
+      reinterpret_cast<uint2*>(S.starts)[lane] = make_uint2(0u, 0u);
+      __syncwarp();
+      const int s = lane < nR ? max(S.row_a[lane].x, 0) : -1;  // a carried row may start before 0
+      if (s >= base && s < base + 32 * kStartWords)
+        atomicOr(&S.starts[(s - base) >> 5], 1u << (s & 31));
+      __syncwarp();
+      for (int w0 = 0; w0 < nw; w0 += 16) {
+        const int wend = min(nw, w0 + 16);
+        for (int w = w0; w < wend; w++) {
+          const unsigned M = S.starts[w];
+          const int row = rprev + __popc(M & le_mask);
+          rprev += __popc(M);
+          const int idx = base + (w << 5) + lane;
+          const bool valid = idx < sweep;
+          const int4 ra = S.row_a[row];
+          f.sample(ra, S.row_b[row], valid ? idx - ra.x : 0, valid);
+        }
+        f.flush_h();
+      }
+    }
+    if (r0 >= nrows && z0 + 32 > R.hi[2]) break;  // that was the side's last step
+    // carry the rows from the one holding sample `sweep` on, rebased to start at 0
+    if (pendS == 0) {
+      pendR = 0;
+      continue;
+    }
+    const int st = lane < nR ? S.row_a[lane].x : 0x7fffffff;
+    const int first = __popc(__ballot_sync(FULLMASK, lane < nR && st <= sweep)) - 1;
+    pendR = nR - first;
+    const bool mv = lane >= first && lane < nR;
+    int4 a = make_int4(0, 0, 0, 0);
+    float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (mv) {
+      a = S.row_a[lane];
+      b = S.row_b[lane];
+    }
+    __syncwarp();
+    if (mv) {
+      a.x -= sweep;
+      S.row_a[lane - first] = a;
+      S.row_b[lane - first] = b;
+    }
+  }
+  __syncwarp();
+}
+#else
 template <class F>
 __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int loff, WarpSmem& S,
                                        int lane, F& f) {
@@ -635,6 +772,7 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
     }
   }
 }
+#endif  // MOREA_CARRY
 
 // ---------------------------------------------------------------------------
 // O6 slow path: exact contributing corner set when the fp32 position is within
