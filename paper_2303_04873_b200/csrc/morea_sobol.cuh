@@ -200,7 +200,12 @@ constexpr int kSobolThreads = 32 * kSobolWarps;
 template <bool TEX>
 __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
   __shared__ SobolWarp smem[kSobolWarps];
+#if MOREA_SOBOL_CLAIM_LOCAL
+  __shared__ BlockQueue bq;
+  bq.init();
+#else
   __shared__ unsigned long long chunk;
+#endif
   __shared__ unsigned sV[4][32];
   int warp, lane;
   asm volatile("shr.u32 %0, %1, 5;" : "=r"(warp) : "r"(threadIdx.x));
@@ -226,12 +231,17 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
   const long long n_items = per_v * A.n_raster_versions;
   if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0ull;
   while (true) {
+#if MOREA_SOBOL_CLAIM_LOCAL
+    const unsigned long long item = bq.claim(A.counter, lane, n_items, kSobolWarps, 1);
+    if ((long long)item >= n_items) break;
+#else
     __syncthreads();
     if (threadIdx.x == 0) chunk = atomicAdd(A.counter, (unsigned long long)kSobolWarps);
     __syncthreads();
     if ((long long)chunk >= n_items) break;  // block-uniform
     const unsigned long long item = chunk + warp;
     if ((long long)item >= n_items) continue;
+#endif
     const int ver = (int)(item / (unsigned long long)per_v);
     const long long rem = (long long)item - (long long)ver * per_v;
     const int es = (int)(rem / A.P);
