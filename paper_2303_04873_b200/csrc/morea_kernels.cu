@@ -61,15 +61,15 @@
 #endif
 
 #ifndef MOREA_SOBOL_CLAIM_LOCAL
-#define MOREA_SOBOL_CLAIM_LOCAL 1  // k_sobol takes items from BlockQueue (chunks of its 28 warps)
+#define MOREA_SOBOL_CLAIM_LOCAL 1  // k_sobol takes items from BlockQueue (same chunk rule as k_raster)
 #endif
 
 #ifndef MOREA_CLAIM_CHUNK
-#define MOREA_CLAIM_CHUNK 112  // k_raster: at most this many items per global claim of BlockQueue
+#define MOREA_CLAIM_CHUNK 112  // k_raster, k_sobol: at most this many items per global claim of BlockQueue
 #endif
 
 #ifndef MOREA_CLAIM_SPREAD
-#define MOREA_CLAIM_SPREAD 16  // k_raster: at least this many claims per block per launch where possible
+#define MOREA_CLAIM_SPREAD 16  // k_raster, k_sobol: at least this many claims per block per launch where possible
 #endif
 
 #ifndef MOREA_RASTER_MINB

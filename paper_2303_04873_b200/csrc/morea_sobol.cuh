@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
   if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0ull;
   while (true) {
 #if MOREA_SOBOL_CLAIM_LOCAL
-    const unsigned long long item = bq.claim(A.counter, lane, n_items, kSobolWarps, 1);
+    const unsigned long long item = bq.claim(A.counter, lane, n_items, MOREA_CLAIM_CHUNK, MOREA_CLAIM_SPREAD);
     if ((long long)item >= n_items) break;
 #else
     __syncthreads();
