@@ -16,7 +16,8 @@
 // Work decomposition.  k_setup: one thread per (version, tet,
 // solution) computes the exact integer geometry of both sides (int64/int128)
 // and writes a 384-byte SideRec per side.  k_raster: one 28-warp block per SM
-// pulls items from a global queue in solution-minor order, 28 at a time
+// pulls chunks of up to 112 items from a global queue in solution-minor order
+// and its warps take them one at a time without a block barrier (BlockQueue)
 // (consecutive items = same tet, next solution, so the warps of an SM share
 // their texel and record footprints in L1; large tets first).  Inside an item
 // the 32 lanes compute the exact x-intervals of 32 bbox rows, prefix-sum their
