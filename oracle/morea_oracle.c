@@ -1360,6 +1360,13 @@ int orc_distance_map(orc_problem *P, int s, int i, float *out) {
     return 0;
 }
 
+/* D_i^s at n given voxel centres q (n x 3, voxel indices): the same exact value
+ * the maps above hold (test access for large configs, no new arithmetic). */
+int orc_distance_at(orc_problem *P, int s, int i, int64_t n, const int64_t *q, float *out) {
+    for (int64_t k = 0; k < n; k++) out[k] = dmap_exact(P, s, i, q + 3 * k);
+    return 0;
+}
+
 /* debug: one sample of tet t on side s at lattice point q.
  * out = {owned, x, y, z (fp64 transformed position), a, b, fg, h,
  *        floor/integer code per axis (3 values: 2*set_size + (first index sign))} */

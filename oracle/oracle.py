@@ -64,6 +64,7 @@ def lib():
         L.orc_check_folds.argtypes = [vp, vp, vp, vp, vp]
         L.orc_owner_map.argtypes = [vp, vp, ctypes.c_int, vp]
         L.orc_distance_map.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp]
+        L.orc_distance_at.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp, vp]
         L.orc_sample_debug.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.orc_h.restype = ctypes.c_double
         L.orc_h.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_int]
@@ -203,6 +204,13 @@ class Oracle:
     def distance_map(self, side, pair):
         out = np.empty(self.V, dtype=np.float32)
         lib().orc_distance_map(self.h, int(side), int(pair), _p(out))
+        return out
+
+    def distance_at(self, side, pair, q):
+        """D_pair^side at voxel centres q (n x 3 integer voxel indices)."""
+        qq = np.ascontiguousarray(q, dtype=np.int64)
+        out = np.empty(len(qq), dtype=np.float32)
+        lib().orc_distance_at(self.h, int(side), int(pair), len(qq), _p(qq), _p(out))
         return out
 
     def sample_debug(self, offsets_one, tet, side, q):

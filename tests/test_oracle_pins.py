@@ -423,6 +423,114 @@ def test_f_guid_identity_closed_form(wl):
     assert obj[2] == pytest.approx(tot / (2 * w.V), rel=1e-6)
 
 
+def _brute_dmap(q_vox, pts, spacing):
+    """D(q) = min_c ||(q - c) * spacing|| by brute force over ALL points (SURVEY §8(c) 'Form'):
+    per point dx, dy, dz in fp64, ((dx^2 + dy^2) + dz^2), min, sqrt, rounded once to fp32.
+    A different algorithm from the oracle's bucket search, the same arithmetic definition."""
+    best = np.full(len(q_vox), np.inf)
+    c = pts.astype(np.float64)
+    for j in range(len(c)):
+        dx = (q_vox[:, 0] - c[j, 0]) * spacing[0]
+        dy = (q_vox[:, 1] - c[j, 1]) * spacing[1]
+        dz = (q_vox[:, 2] - c[j, 2]) * spacing[2]
+        best = np.minimum(best, (dx * dx + dy * dy) + dz * dz)
+    return np.sqrt(best).astype(np.float32)
+
+
+def test_f_guid_global_affine_closed_form():
+    """f_guidance under an exact global affine target mesh (x = A q + b at NON-lattice positions)
+    == a mesh-free evaluation of eq. L338-342 / App. A.3 L793-796 (reading O8): brute-force
+    distance maps at the voxel centres, D'_i interpolated with scipy map_coordinates(order=1,
+    mode='nearest') at A q + b (side s) and A^-1 (q - b) (side t).  Pins the oracle's
+    trilinear_map at fractional positions (a wrong fractional weight fails it)."""
+    from scipy.ndimage import map_coordinates
+    dims, base, tets, off, A, b = _affine_problem()
+    n = dims[0]
+    sp = np.array([1.5, 1.5, 1.5])
+    rng = np.random.default_rng(41)
+    cs = [rng.uniform(1, n - 2, size=(60, 3)).astype(np.float32),
+          rng.uniform(2, n - 3, size=(25, 3)).astype(np.float32)]
+    ct = [(cs[0].astype(np.float64) @ A.T + b + rng.normal(0, 0.4, size=(60, 3))).astype(np.float32),
+          rng.uniform(2, n - 3, size=(31, 3)).astype(np.float32)]
+    r_mm = 4.0
+    I = blob_volume(dims, 7)
+    orc = make_oracle(dims, I, I, base, tets, cs=cs, ct=ct, r_mm=r_mm, spacing=tuple(sp))
+    obj, acc = orc.eval(off)
+    z, y, x = np.meshgrid(range(n), range(n), range(n), indexing="ij")
+    q = np.stack([x.ravel(), y.ravel(), z.ravel()], 1).astype(np.float64)
+    D = {(s, i): _brute_dmap(q, (cs, ct)[s][i], sp).astype(np.float64) for s in (0, 1) for i in range(2)}
+    for (s, i), d in D.items():  # the oracle's stored maps are these exact values
+        assert np.array_equal(orc.distance_map(s, i), d.astype(np.float32))
+    y_src = (q - b) @ np.linalg.inv(A).T
+    margin = np.minimum(y_src + 0.5, (n - 0.5) - y_src).min(axis=1)
+    assert np.abs(margin).min() > 1e-6
+    inside_t = margin > 0
+    pos = {0: (np.ones(len(q), bool), q @ A.T + b), 1: (inside_t, y_src)}
+    tot = 0.0
+    for s in (0, 1):
+        owned, xs = pos[s]
+        sizes = [len((cs, ct)[s][i]) for i in range(2)]
+        for i in range(2):
+            w_i = sizes[i] / sum(sizes)  # |C_i^s| / |G_s| (L340)
+            d = D[(s, i)][owned]
+            grid = D[(1 - s, i)].reshape(n, n, n)
+            Dp = map_coordinates(grid, xs[owned][:, ::-1].T, order=1, mode="nearest")
+            bnd = d < r_mm  # strict (eq. L341)
+            assert bnd.sum() > 20  # the band is populated on both sides
+            tot += w_i * (((r_mm - d[bnd]) / r_mm) * (d[bnd] - Dp[bnd]) ** 2).sum()
+    n_tot = n ** 3 + inside_t.sum()
+    assert acc.n_samples == n_tot
+    assert obj[2] == pytest.approx(tot / n_tot, rel=1e-12)
+
+
+def test_f_guid_truncation_closed_forms():
+    """SPEC S:L426-427 and the strict d < r of eq. L341: a source voxel at distance d = 0 whose
+    mapped distance is delta contributes w delta^2; a voxel at exactly d = r contributes 0.
+    Identity mesh, one source contour point on voxel centre c, one target point at c + (1/2, 0, 0)
+    (distance 0.75 mm from its two nearest voxel centres, 1.5 mm spacing)."""
+    dims = (8, 8, 8)
+    base, tets = kuhn_lattice_mesh([-0.5, 3.5, 7.5], [-0.5, 3.5, 7.5], [-0.5, 3.5, 7.5])
+    base = base.astype(np.float32)
+    I = blob_volume(dims, 3)
+    c = np.array([[3.0, 4.0, 2.0]], np.float32)
+    ct = [c + np.array([0.5, 0.0, 0.0], np.float32)]
+    off = np.zeros((len(base), 6), np.float32)
+    V = 8 ** 3
+    # r = 0.6 mm: source band = {c} (d = 0), target band empty (nearest centre at 0.75 mm)
+    orc = make_oracle(dims, I, I, base, tets, cs=[c], ct=ct, r_mm=0.6)
+    obj, acc = orc.eval(off)
+    assert acc.n_samples == 2 * V
+    assert acc.g_sum == 0.75 ** 2  # w = 1, (r - 0)/r = 1, (0 - 0.75)^2 exactly
+    assert obj[2] == 0.75 ** 2 / (2 * V)
+    # r = 0.75 exactly: the two target-side centres at d = 0.75 = r are NOT in the band
+    orc = make_oracle(dims, I, I, base, tets, cs=[c], ct=ct, r_mm=0.75)
+    assert orc.eval(off)[1].g_sum == 0.75 ** 2
+    # r just above 0.75: they enter with weight (r - 0.75)/r and D_s there = 1.5 mm (one voxel from c)
+    r = 0.76
+    orc = make_oracle(dims, I, I, base, tets, cs=[c], ct=ct, r_mm=r)
+    g = orc.eval(off)[1].g_sum
+    ref = 0.75 ** 2 + 2 * ((r - 0.75) / r) * (0.75 - 1.5) ** 2
+    assert g == pytest.approx(ref, rel=1e-12)
+
+
+def test_distance_map_bruteforce_c3_sampled(wl):
+    """C3 distance maps of the oracle (bucket search) == SURVEY §8(c)'s brute force, bit-exact,
+    on 3000 sampled voxels of every pair and side (the bucket search at full config size)."""
+    w = wl(3, 4)
+    orc = O.Oracle.from_workload(w)
+    nx, ny, nz = w.dims
+    rng = np.random.default_rng(5)
+    v = rng.integers(0, w.V, size=3000)
+    q = np.stack([v % nx, (v // nx) % ny, v // (nx * ny)], 1).astype(np.float64)
+    sides = [(w.cs_off, w.cs_xyz), (w.ct_off, w.ct_xyz)]
+    for s in (0, 1):
+        off_s, xyz_s = sides[s]
+        for i in range(len(w.pairs)):
+            got = orc.distance_at(s, i, q.astype(np.int64))
+            ref = _brute_dmap(q, xyz_s[off_s[i]:off_s[i + 1]], w.spacing)
+            assert np.array_equal(got, ref), (s, i)
+
+
 # --------------------------------------------------------------------------- f_magnitude (O9)
 def test_f_mag_closed_forms():
     """Identity/translation -> 0; uniform scale alpha -> (1-alpha)^2 sum c sum |e|^2 / (10T);
