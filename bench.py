@@ -6,15 +6,19 @@ C4 = 256x256x96 CT-shaped phantom at 1.5 mm, 600-point Delaunay dual-dynamic
 mesh (3607 tets), 7 contour pairs, P = 512 solutions per GPU (weak scaling:
 N GPUs evaluate N*512 solutions, the C5 configuration at N = 8).
 
-One step = one MO-RV-GOMEA generation batch over every §8(a) row:
+One step = one MO-RV-GOMEA generation's evaluation work (§4.2.1
+L401-410: partial evaluations run one colour class after another):
   full evaluation of the P solutions (writes the per-tet cache),
-  partial evaluation of one FOS colour class (each edge = one group, delta on
-  its dependent tets, old contributions from the cache) for all P solutions,
-  fold check of the P solutions, and (N > 1) the NCCL all-gather of the
+  a partial evaluation of EVERY FOS colour class in turn (each edge = one
+  group, delta on its dependent tets, old contributions from the cache), for
+  all P solutions,
+  the fold check of the P solutions, and (N > 1) the all-gather of the
   per-solution outputs.
-Units per step = P full + P * G partial solution evaluations.
+Units per step = P full + P * (sum of the classes' groups) partial evaluations;
+the full and partial rates are reported separately next to the blend.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--dist-backend nccl|gloo] [--dump-records PATH]
 """
 from __future__ import annotations
 
@@ -36,15 +40,17 @@ P_PER_GPU = 512
 CONFIG_INDEX = 4  # synth config C4 == BASELINE.json configs[3]
 
 
-def workload_config(P_total, G, world, class_index, T):
+def workload_config(P_total, n_groups, n_classes, world, T, backend):
     return {
         "workload": f"C4 paper-scale: 256x256x96 CT-shaped phantom (1.5 mm), 600-point Delaunay dual mesh "
-                    f"({T} tets), 7 contour pairs, P={P_PER_GPU}/GPU (P_total={P_total}); step = full eval + "
-                    f"partial eval of FOS colour class {class_index} ({G} edge groups, tet cache) + fold check"
-                    + (" + NCCL all-gather" if world > 1 else ""),
-        "population_per_gpu": P_PER_GPU,
+                    f"({T} tets), 7 contour pairs, P={P_total // world}/GPU (P_total={P_total}); step = one generation: "
+                    f"full eval + partial eval of every FOS colour class ({n_classes} classes, {n_groups} "
+                    f"edge groups, tet cache) + fold check"
+                    + (f" + {backend} all-gather" if world > 1 else ""),
+        "population_per_gpu": P_total // world,
         "population_total": P_total,
-        "partial_groups": G,
+        "colour_classes": n_classes,
+        "partial_groups_per_step": n_groups,
         "l2": "flushed between timed steps (256 MiB device write, untimed)",
         "inputs": "seeded synthetic (synth/, SURVEY.md §8(d)); resident in HBM before timing",
     }
@@ -148,20 +154,50 @@ def host_cpu():
     return {"host_cpu": model, "host_threads": os.cpu_count()}
 
 
-def oracle_sample(w, plan_req, sols, n_partial):
-    """Time the oracle as it stands on a bounded sample: per solution of `sols`,
-    1 full + n_partial partial evaluations."""
+def _oracle_solution(w, classes, sol, core, conn):
+    """Child process: pinned to one core, 1 full + every class's partial evaluations of one
+    solution (the GPU step's full:partial mix); sends (units, seconds)."""
+    try:
+        os.sched_setaffinity(0, {core})
+    except Exception:
+        pass
     from oracle.oracle import Oracle
-    go, ch, nv = plan_req
     orc = Oracle.from_workload(w)
-    orc.eval(w.offsets[0])  # untimed: builds the oracle's lazy distance-map memo (load-time work)
+    orc.eval(w.offsets[0])  # untimed: the oracle's lazy distance-map memo (load-time work)
     t0 = time.perf_counter()
-    for sol in sols:
-        _, base = orc.eval(w.offsets[sol])
-        for g in range(n_partial):
+    _, base = orc.eval(w.offsets[sol])
+    units = 1
+    for go, ch, nv in classes:
+        for g in range(len(go) - 1):
             orc.eval_partial(w.offsets[sol], base, ch[go[g]:go[g + 1]], nv[sol, go[g]:go[g + 1]])
-    dt = time.perf_counter() - t0
-    return len(sols) * (1 + n_partial) / dt, dt
+            units += 1
+    conn.send((units, time.perf_counter() - t0))
+    conn.close()
+
+
+def oracle_baseline(w, classes, n_proc):
+    """The oracle as it stands, per process one solution (1 full + all class partials),
+    each process pinned to its own core; n_proc processes on disjoint solutions."""
+    import multiprocessing as mproc
+    ctx = mproc.get_context("fork")
+    cores = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else list(range(os.cpu_count()))
+    n_proc = max(1, min(n_proc, len(cores)))
+    pipes, procs = [], []
+    t0 = time.perf_counter()
+    for i in range(n_proc):
+        r, s_ = ctx.Pipe(duplex=False)
+        pr = ctx.Process(target=_oracle_solution, args=(w, classes, 1 + i, cores[i], s_))
+        pr.start()
+        pipes.append(r)
+        procs.append(pr)
+    res = [r.recv() for r in pipes]
+    for pr in procs:
+        pr.join()
+    wall = time.perf_counter() - t0
+    units = sum(u for u, _ in res)
+    # throughput over the processes' own timed regions (the memo warm-up excluded)
+    busy = max(t for _, t in res)
+    return units / busy, units, busy, n_proc, wall
 
 
 def run_reference(args, rank, world):
@@ -171,32 +207,33 @@ def run_reference(args, rank, world):
     from synth import fos_plan, make_workload, partial_request
     w = make_workload(CONFIG_INDEX, P=P_PER_GPU)
     plan = fos_plan(w.tets, w.N)
-    req = partial_request(w, plan, "class", args.class_index)
+    classes = [partial_request(w, plan, "class", c) for c in range(len(plan["classes"]))]
     from oracle.oracle import Oracle
-    go, ch, nv = req
     orc = Oracle.from_workload(w)
     orc.eval(w.offsets[0])
-    n_part = 4
-    times = []
+    # each step: a bounded sample of the generation workload: 1 full evaluation and
+    # one class's partial evaluations (classes in turn), of one solution
+    times, units = [], 0
     for it in range(args.warmup + args.steps):
         sol = 1 + it % (w.P - 1)
+        go, ch, nv = classes[it % len(classes)]
         t0 = time.perf_counter()
         _, base = orc.eval(w.offsets[sol])
-        for g in range(n_part):
+        for g in range(len(go) - 1):
             orc.eval_partial(w.offsets[sol], base, ch[go[g]:go[g + 1]], nv[sol, go[g]:go[g + 1]])
         if it >= args.warmup:
             times.append(time.perf_counter() - t0)
+            units += len(go)
     total = sum(times)
-    units = (1 + n_part) * len(times)
     value = units / total
-    G = len(go) - 1
-    sample = (f"per step: 1 full + {n_part} partial (1-edge groups of FOS class {args.class_index}) "
-              f"evaluations of one C4 solution, oracle single-threaded")
+    G = sum(len(c[0]) - 1 for c in classes)
+    sample = ("per step: 1 full + the partial evaluations of one FOS colour class (classes in turn) "
+              "of one C4 solution, oracle single-threaded")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(P_PER_GPU * world, G, world, args.class_index, w.T),
+        "config": workload_config(P_PER_GPU * world, G, len(classes), world, w.T, "none"),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
                          **host_cpu()},
@@ -218,10 +255,17 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--class-index", type=int, default=0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: records staged through host memory (several ranks may share one GPU)")
+    ap.add_argument("--dump-records", default=None, help="rank 0 writes the gathered records (.npy)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-procs", type=int, default=32, help="processes of the oracle x nproc leg (cap)")
     ap.add_argument("--no-extras", action="store_true",
-                    help="skip the Sobol / repair / mixing breakdown timings (for ncu launch lists)")
+                    help="skip the Sobol / repair / mixing / plain-load breakdown timings")
+    ap.add_argument("--quick", action="store_true",
+                    help="timed region only (no breakdown, sweep, e2e or CPU legs): multi-rank checks")
+    ap.add_argument("--pop-per-rank", type=int, default=P_PER_GPU,
+                    help="solutions per rank (default 512: the C4 / C5 workload)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: at least 3 untimed warm-up steps
@@ -236,46 +280,66 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dev_index = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    backend = args.dist_backend
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     from paper_2303_04873_b200 import morea
     from paper_2303_04873_b200.distributed import all_gather_records, pack, shard_bounds
     from synth import fos_plan, make_workload, partial_request
 
-    P_total = P_PER_GPU * world
+    P_total = args.pop_per_rank * world
     w = make_workload(CONFIG_INDEX, P=P_total)
     plan = fos_plan(w.tets, w.N)
-    go, ch, nv = partial_request(w, plan, "class", args.class_index)
-    G = len(go) - 1
+    classes = [partial_request(w, plan, "class", c) for c in range(len(plan["classes"]))]
+    n_cls = len(classes)
+    Gs = [len(c[0]) - 1 for c in classes]
+    G_tot = sum(Gs)
     s0, s1 = shard_bounds(P_total, world, rank)
     P = s1 - s0
 
-    ctx = morea.Context.from_workload(w, device=local_rank)
+    ctx = morea.Context.from_workload(w, device=dev_index)
     stream = torch.cuda.ExternalStream(ctx.stream_handle, device=dev)
     T = w.T
+    for go, ch, _ in classes:  # build every class's dependent-tet plan up front (cached)
+        ctx.prepare_partial(go, ch)
     off_d = torch.from_numpy(w.offsets[s0:s1].copy()).to(dev)
-    nv_d = torch.from_numpy(nv[s0:s1].copy()).to(dev)
+    nv_d = [torch.from_numpy(c[2][s0:s1].copy()).to(dev) for c in classes]
     obj_d = torch.empty((P, 3), dtype=torch.float64, device=dev)
     acc_d = torch.empty((P, 6), dtype=torch.int64, device=dev)
     cache_d = torch.empty((P, T, 4), dtype=torch.float64, device=dev)
-    pobj_d = torch.empty((P * G, 3), dtype=torch.float64, device=dev)
-    pacc_d = torch.empty((P * G, 6), dtype=torch.int64, device=dev)
+    pobj_d = [torch.empty((P * G, 3), dtype=torch.float64, device=dev) for G in Gs]
+    pacc_d = [torch.empty((P * G, 6), dtype=torch.int64, device=dev) for G in Gs]
     cnt_d = torch.empty(P, dtype=torch.int32, device=dev)
     sev_d = torch.empty(P, dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
+    def gather():
+        outs = []
+        with torch.cuda.stream(stream):
+            outs.append(all_gather_records(pack(obj_d, acc_d), P_total))
+            for c in range(n_cls):
+                outs.append(all_gather_records(pack(pobj_d[c], pacc_d[c]), P_total, rows_per_solution=Gs[c]))
+        return outs
+
+    def partials():
+        for c, (go, ch, _) in enumerate(classes):
+            ctx.eval_partial(off_d, acc_d, go, ch, nv_d[c], cache_d, pobj_d[c], pacc_d[c])
+
     def step():
         ctx.eval_full(off_d, obj_d, acc_d, cache_d)
-        ctx.eval_partial(off_d, acc_d, go, ch, nv_d, cache_d, pobj_d, pacc_d)
+        partials()
         ctx.check_folds(off_d, cnt_d, sev_d, None)
         if world > 1:
-            with torch.cuda.stream(stream):
-                all_gather_records(pack(obj_d, acc_d), P_total)
-                all_gather_records(pack(pobj_d, pacc_d), P_total, rows_per_solution=G)
+            return gather()
+        return None
 
     def barrier():
         if world > 1:
@@ -290,7 +354,7 @@ def main():
     ctx.prof_read()
     k0 = ctx.kernel_launches()
     times = []
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_index) as clk:
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
@@ -306,15 +370,36 @@ def main():
     launches = ctx.kernel_launches() - k0
     prof = ctx.prof_read()
     ctx.prof_enable(False)
-    t_local = sum(times)
-    t_max = torch.tensor([t_local], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    t_max = float(t_max.item())
-    units = (P_total + P_total * G) * args.steps
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    t_max = max_over_ranks(sum(times))
+    units = (P_total + P_total * G_tot) * args.steps
     value = units / (t_max / 1e3)
 
-    # separate full / partial throughputs (same inputs, device time, not in the contract value)
+    if args.dump_records:
+        recs = gather() if world > 1 else [pack(obj_d, acc_d)] + [pack(pobj_d[c], pacc_d[c]) for c in range(n_cls)]
+        if rank == 0:
+            import numpy as _np
+            _np.save(args.dump_records, torch.cat([r.cpu() for r in recs]).numpy())
+
+    if args.quick:
+        if rank == 0:
+            print(json.dumps({
+                "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": workload_config(P_total, G_tot, n_cls, world, T, backend),
+                "gpu_launches": int(launches), "clocks": clk.summary(), "quick": True}), flush=True)
+        ctx.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
     def timed(fn, reps=3):
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
@@ -326,37 +411,50 @@ def main():
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps
 
-    t_full = timed(lambda: ctx.eval_full(off_d, obj_d, acc_d, cache_d))
-    t_part = timed(lambda: ctx.eval_partial(off_d, acc_d, go, ch, nv_d, cache_d, pobj_d, pacc_d))
-    t_part_nc = timed(lambda: ctx.eval_partial(off_d, acc_d, go, ch, nv_d, None, pobj_d, pacc_d))
-    # partial-evaluation sweep over FOS sizes (BASELINE.json configs[3]):
-    # 1 edge, 4 and 16 edges of colour class `class_index`, the whole class as one
-    # group, all points as one group; cached old contributions; k_raster algorithmic
-    # GB/s of the call from the kernel's own counters and CUDA events
-    sweep = {}
     peak, peak_src = measured_hbm_peak()
+
+    def prof_run(fn, reps=3):
+        """k_sweep algorithmic GB/s of fn from the kernel's own counters and CUDA events."""
+        fn()
+        torch.cuda.synchronize()
+        ctx.prof_enable(True)
+        ctx.prof_read()
+        t = timed(fn, reps)
+        sp = ctx.prof_read()
+        ctx.prof_enable(False)
+        sb = 8 * sp["samples"] + 12 * sp["band_entries"] + 32 * sp["items"]
+        gbs = sb / (sp["ms"] / 1e3) / 1e9 if sp["ms"] > 0 else None
+        return t, sp, gbs
+
+    # separate full / partial throughputs (same inputs, device time)
+    t_full, sp_full, gbs_full = prof_run(lambda: ctx.eval_full(off_d, obj_d, acc_d, cache_d))
+    t_parts, sp_parts, gbs_parts = prof_run(partials)
+    per_class = []
+    for c, (go, ch, _) in enumerate(classes):
+        run = (lambda c=c, go=go, ch=ch: ctx.eval_partial(off_d, acc_d, go, ch, nv_d[c], cache_d, pobj_d[c],
+                                                          pacc_d[c]))
+        t_c, sp_c, gbs_c = prof_run(run)
+        per_class.append({"class": c, "groups": Gs[c], "evals_per_s": P * Gs[c] * 1e3 / t_c, "ms": t_c,
+                          "k_sweep_frac": (gbs_c / peak) if gbs_c else None})
+    t_part_nc = timed(lambda: ctx.eval_partial(off_d, acc_d, classes[0][0], classes[0][1], nv_d[0], None,
+                                               pobj_d[0], pacc_d[0]))
+    # partial-evaluation sweep over FOS sizes (SURVEY.md §8(d)): 1 edge, 4 and 16 edges of
+    # colour class 0, the whole class as one group, all points as one group; cached
+    sweep = {}
     for kind in ("class", "edges4", "edges16", "wholeclass", "all"):
-        sgo, sch, snv = partial_request(w, plan, kind, args.class_index)
+        sgo, sch, snv = partial_request(w, plan, kind, 0)
         sG = len(sgo) - 1
         snv_d = torch.from_numpy(snv[s0:s1].copy()).to(dev)
         spo = torch.empty((P * sG, 3), dtype=torch.float64, device=dev)
         spa = torch.empty((P * sG, 6), dtype=torch.int64, device=dev)
         run = (lambda sgo=sgo, sch=sch, snv_d=snv_d, spo=spo, spa=spa:
                ctx.eval_partial(off_d, acc_d, sgo, sch, snv_d, cache_d, spo, spa))
-        run()
-        torch.cuda.synchronize()
-        ctx.prof_enable(True)
-        ctx.prof_read()
-        t_k = timed(run)
-        sp = ctx.prof_read()
-        ctx.prof_enable(False)
-        sb = 8 * sp["samples"] + 12 * sp["band_entries"] + 32 * sp["items"]
-        gbs = sb / (sp["ms"] / 1e3) / 1e9 if sp["ms"] > 0 else None
+        t_k, sp, gbs = prof_run(run)
         sweep[kind] = {"groups": sG, "points_per_group": round(len(sch) / sG, 2),
                        "evals_per_s": P * sG * 1e3 / t_k, "ms": t_k,
-                       "k_raster_gbs": gbs, "k_raster_frac": (gbs / peak) if gbs else None,
+                       "k_sweep_gbs": gbs, "k_sweep_frac": (gbs / peak) if gbs else None,
                        "samples_per_eval": sp["samples"] / max(sp["launches"], 1) / (P * sG)}
-    t_sobol = t_repair = t_mix = float("nan")
+    t_sobol = t_repair = t_mix = t_plain = float("nan")
     mix_accept_frac = float("nan")
     if not args.no_extras:
         # NEXT-1: the paper's Sobol-in-tetrahedron sample set (App. A.2), rate 1 sample / voxel
@@ -370,10 +468,11 @@ def main():
         # NEXT-3: optimal mixing of colour class 0 on the device (model: this shard's
         # population mean and covariance per FOS element, one cluster), on copies of the state
         import numpy as _np
+        go0, ch0, _ = classes[0]
         offs_h = w.offsets[s0:s1]
         mus, Ls = [], []
-        for g in range(G):
-            X = offs_h[:, ch[go[g]:go[g + 1]], :].reshape(offs_h.shape[0], -1).astype(_np.float64)
+        for g in range(Gs[0]):
+            X = offs_h[:, ch0[go0[g]:go0[g + 1]], :].reshape(offs_h.shape[0], -1).astype(_np.float64)
             C = _np.cov(X.T, bias=True) + 1e-4 * _np.eye(X.shape[1])
             mus.append(X.mean(0))
             Ls.append(_np.linalg.cholesky(C).ravel())
@@ -382,22 +481,18 @@ def main():
         cl_d = torch.zeros(P, dtype=torch.int32, device=dev)
         ctx.eval_full(off_d, obj_d, acc_d, cache_d)  # voxel-mode state of off_d (the Sobol run overwrote it)
         mx_off, mx_acc, mx_obj, mx_tc = off_d.clone(), acc_d.clone(), obj_d.clone(), cache_d.clone()
-        mx_flags = torch.zeros((P, G), dtype=torch.uint8, device=dev)
+        mx_flags = torch.zeros((P, Gs[0]), dtype=torch.uint8, device=dev)
 
         def mix_once():
             mx_off.copy_(off_d); mx_acc.copy_(acc_d); mx_obj.copy_(obj_d); mx_tc.copy_(cache_d)
-            ctx.mix_class(mx_off, mx_acc, mx_obj, mx_tc, go, ch, cl_d, mu_d, L_d, fixed_d, None, 0.0, 2024, 0, s0,
-                          mx_flags)
+            ctx.mix_class(mx_off, mx_acc, mx_obj, mx_tc, go0, ch0, cl_d, mu_d, L_d, fixed_d, None, 0.0, 2024, 0,
+                          s0, mx_flags)
         mix_once()  # first call allocates the mixing scratch
         t_mix = timed(mix_once, reps=2)
         mix_accept_frac = float(mx_flags.float().mean().item())
-
-    # plain-load path (volumes beyond the 2D gather-texture limits, e.g. 512 x 512 x 128):
-    # the same full evaluation with MOREA_NO_TEX on a second context
-    t_plain = float("nan")
-    if not args.no_extras:
+        # plain-load path (volumes beyond the 2D gather-texture limits): MOREA_NO_TEX context
         os.environ["MOREA_NO_TEX"] = "1"
-        ctx_plain = morea.Context.from_workload(w, device=local_rank)
+        ctx_plain = morea.Context.from_workload(w, device=dev_index)
         del os.environ["MOREA_NO_TEX"]
         stream_plain = torch.cuda.ExternalStream(ctx_plain.stream_handle, device=dev)
         ctx_plain.eval_full(off_d, obj_d, acc_d, None)
@@ -411,33 +506,41 @@ def main():
         torch.cuda.synchronize()
         t_plain = a0.elapsed_time(a1) / 3
         ctx_plain.close()
+        ctx.eval_full(off_d, obj_d, acc_d, cache_d)
 
-    # ---- roofline of the dominant kernel (k_raster), SURVEY.md §8(d) algorithmic bytes
+    # ---- roofline of the dominant kernel (k_sweep), SURVEY.md §8(d) algorithmic bytes
     alg_bytes = 8 * prof["samples"] + 12 * prof["band_entries"] + 32 * prof["items"]
     achieved = alg_bytes / (prof["ms"] / 1e3) / 1e9 if prof["ms"] > 0 else None
     per_launch_bytes = alg_bytes / max(prof["launches"], 1)
     ncu = ncu_summary()
-    traffic = ncu.get("k_raster_dram_bytes_per_launch")
+    traffic = ncu.get("k_sweep_dram_bytes_per_launch")
 
-    # ---- e2e: the same step through the C-ABI with HOST buffers (pinned), copies inside
+    # ---- e2e: the same step through the public API, inputs copied from pinned host memory
+    # and the results read back to pinned host memory inside the timed region
     off_h = torch.from_numpy(w.offsets[s0:s1].copy()).pin_memory()
-    nv_h = torch.from_numpy(nv[s0:s1].copy()).pin_memory()
+    nv_h = [torch.from_numpy(c[2][s0:s1].copy()).pin_memory() for c in classes]
     obj_h = torch.empty((P, 3), dtype=torch.float64).pin_memory()
     acc_h = torch.empty((P, 6), dtype=torch.int64).pin_memory()
-    pobj_h = torch.empty((P * G, 3), dtype=torch.float64).pin_memory()
-    pacc_h = torch.empty((P * G, 6), dtype=torch.int64).pin_memory()
+    pobj_h = [torch.empty((P * G, 3), dtype=torch.float64).pin_memory() for G in Gs]
+    pacc_h = [torch.empty((P * G, 6), dtype=torch.int64).pin_memory() for G in Gs]
     cnt_h = torch.empty(P, dtype=torch.int32).pin_memory()
     sev_h = torch.empty(P, dtype=torch.float64).pin_memory()
 
     def step_e2e():
-        ctx.eval_full(off_h, obj_h, acc_h, cache_d)
-        ctx.eval_partial(off_h, acc_h, go, ch, nv_h, cache_d, pobj_h, pacc_h)
-        ctx.check_folds(off_h, cnt_h, sev_h, None)
-        if world > 1:
-            with torch.cuda.stream(stream):
-                all_gather_records(pack(obj_d, acc_d), P_total)
-                all_gather_records(pack(pobj_d, pacc_d), P_total, rows_per_solution=G)
-            torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            off_d.copy_(off_h, non_blocking=True)
+            for c in range(n_cls):
+                nv_d[c].copy_(nv_h[c], non_blocking=True)
+        step()
+        with torch.cuda.stream(stream):
+            obj_h.copy_(obj_d, non_blocking=True)
+            acc_h.copy_(acc_d, non_blocking=True)
+            for c in range(n_cls):
+                pobj_h[c].copy_(pobj_d[c], non_blocking=True)
+                pacc_h[c].copy_(pacc_d[c], non_blocking=True)
+            cnt_h.copy_(cnt_d, non_blocking=True)
+            sev_h.copy_(sev_d, non_blocking=True)
+        torch.cuda.synchronize()
 
     for _ in range(2):
         step_e2e()
@@ -449,53 +552,63 @@ def main():
         t0 = time.perf_counter()
         step_e2e()
         e2e_times.append(time.perf_counter() - t0)
-    t_e2e = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_value = units / float(t_e2e.item())
-    h2d = (2 * off_h.numel() * 4 + nv_h.numel() * 4 + acc_h.numel() * 8)
-    d2h = (obj_h.numel() + acc_h.numel() + pobj_h.numel() + pacc_h.numel()) * 8 + cnt_h.numel() * 4 + sev_h.numel() * 8
+    e2e_value = units / max_over_ranks(sum(e2e_times))
+    h2d = off_h.numel() * 4 + sum(x.numel() * 4 for x in nv_h)
+    d2h = (obj_h.numel() + acc_h.numel() + sum(x.numel() for x in pobj_h) + sum(x.numel() for x in pacc_h)) * 8 \
+        + cnt_h.numel() * 4 + sev_h.numel() * 8
 
-    # ---- CPU baseline: the oracle as it stands on a bounded sample (rank 0, N = 1 only)
+    # ---- CPU baseline: the oracle as it stands (rank 0, N = 1 only): one solution's
+    # generation work (1 full + every class's partials) on one pinned core, and the same
+    # per process on min(nproc, --cpu-procs) cores (disjoint solutions)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_part, sols = 8, (1, 2, 3, 4)
-        v, dt = oracle_sample(w, (go, ch, nv), sols, n_part)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"solutions 1-4 of this C4 workload, each 1 full + {n_part} partial "
-                         f"(1-edge groups, FOS class {args.class_index}) evaluations, single thread, "
-                         f"{dt:.1f} s", **host_cpu()}
+        v1, u1, t1, _, _ = oracle_baseline(w, classes, 1)
+        vn, un, tn, npr, wall = oracle_baseline(w, classes, args.cpu_procs)
+        cpu = {"value": v1, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"one C4 solution's generation work: 1 full + {u1 - 1} partial evaluations (every "
+                         f"1-edge group of all {n_cls} FOS colour classes, the GPU step's mix), one process "
+                         f"pinned to one core (sched_setaffinity), {t1:.1f} s",
+               "oracle_x_nproc": {"value": vn, "processes": npr, "units": un, "seconds": tn,
+                                  "note": "one solution per process, each pinned to its own core; "
+                                          "throughput over the slowest process's timed region"},
+               **host_cpu()}
 
     if rank == 0:
+        full_rate = P_total * 1e3 / t_full
+        part_rate = P_total * G_tot * 1e3 / t_parts
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": workload_config(P_total, G, world, args.class_index, T),
+            "value_full_evals_per_s": full_rate,
+            "value_partial_evals_per_s": part_rate,
+            "config": workload_config(P_total, G_tot, n_cls, world, T, backend),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
-                         "traffic": traffic, "kernel": "k_raster",
+                         "traffic": traffic, "kernel": "k_sweep",
+                         "frac_full_launch": (gbs_full / peak) if gbs_full else None,
+                         "frac_partial_launches": (gbs_parts / peak) if gbs_parts else None,
                          "algorithmic_bytes_per_launch": per_launch_bytes, "peak_source": peak_src,
                          "launches": prof["launches"], "kernel_ms": prof["ms"],
-                         "ncu": {"source": ncu.get("source"), "l2_hit_pct": ncu.get("k_raster_l2_hit_pct"),
-                                 "l1tex_hit_pct": ncu.get("k_raster_l1tex_hit_pct"),
-                                 "issue_active_pct": ncu.get("k_raster_issue_active_pct"),
-                                 "note": "per captured launch (full, cached partial); the kernel is "
-                                         "gather-latency bound, DESIGN.md §4.4"}},
+                         "ncu": {"source": ncu.get("source"), "l2_hit_pct": ncu.get("k_sweep_l2_hit_pct"),
+                                 "l1tex_hit_pct": ncu.get("k_sweep_l1tex_hit_pct"),
+                                 "issue_active_pct": ncu.get("k_sweep_issue_active_pct")}},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "breakdown": {
-                "full_evals_per_s": P * 1e3 / t_full, "full_ms": t_full,
-                "partial_evals_per_s": P * G * 1e3 / t_part, "partial_ms": t_part,
-                "partial_nocache_evals_per_s": P * G * 1e3 / t_part_nc,
+                "full_evals_per_s": full_rate / world, "full_ms": t_full,
+                "partial_evals_per_s_all_classes": part_rate / world, "partial_ms_all_classes": t_parts,
+                "partial_per_class": per_class,
+                "partial_class0_nocache_evals_per_s": P * Gs[0] * 1e3 / t_part_nc,
+                "k_sweep_lane_steps_per_sample": (32.0 * prof["steps"] / prof["samples"]) if prof["samples"] else None,
                 "sobol_full_evals_per_s": _fin(P * 1e3 / t_sobol),
                 "sobol_full_ms": _fin(t_sobol),
                 "repair_population_ms": _fin(t_repair),
                 "mix_class_ms": _fin(t_mix),
-                "mix_class_evals_per_s": _fin(P * G * 1e3 / t_mix),
+                "mix_class_evals_per_s": _fin(P * Gs[0] * 1e3 / t_mix),
                 "mix_class_accept_frac": _fin(mix_accept_frac),
                 "samples_per_launch": prof["samples"] / max(prof["launches"], 1),
                 "band_entries_per_launch": prof["band_entries"] / max(prof["launches"], 1),

@@ -16,10 +16,12 @@
  *  - Every buffer is caller-owned.  Unless a call says otherwise, an array
  *    argument may be HOST memory (pageable or pinned) or DEVICE memory of the
  *    context's device; the library detects which (cudaPointerGetAttributes).
- *    Host inputs are staged to device scratch inside the call; when any
- *    output is host memory the call synchronises the context stream before
- *    returning.  When every pointer is device memory the call is asynchronous
- *    and stream-ordered on the context stream.
+ *    Host inputs are staged to device scratch inside the call and consumed
+ *    before it returns (a call with a host input or a host output synchronises
+ *    the context stream before returning), so the caller may reuse host
+ *    buffers at once.  When every pointer is device memory the call is
+ *    asynchronous and stream-ordered on the context stream (device offsets
+ *    that are not 8-byte aligned are staged by a device copy).
  *  - A context is bound to one device and is not thread-safe.  Multi-GPU use
  *    is one context per process/rank; the library itself makes no NCCL calls.
  *  - Return value: MOREA_OK (0) or a negative MOREA_E* code; the message is
@@ -183,8 +185,10 @@ int morea_eval_partial(morea_ctx *ctx, int pop, const float *base_offsets,
  *    the guidance term uses d = trilinear D_i^side(p).  Readings S1..S9 in
  *    DESIGN.md §3.  f_int / f_guid normalise by the total sample count.  The
  *    coverage flag is not computed in this mode.
- * rate must be in (0, 8]: per-tet sample counts are 32-bit (a tet inside the
- * Q.10 window spans at most 1.8e8 voxels).  Takes effect for the following morea_eval_*
+ * rate must be in (0, 8].  Per-side point counts are 32-bit: a (solution, tet)
+ * whose count exceeds 2^31 - 1 (a tet of more than 2^31 / rate voxels, only
+ * possible for degenerate meshes spanning most of the Q.10 window) gets
+ * MOREA_F_DOMAIN and NaN objectives instead of a wrong count.  Takes effect for the following morea_eval_*
  * calls (morea_owner_map always uses the voxel-centre rasterizer).
  * Errors: EINVAL (bad mode / rate), ESTATE (before morea_create finished). */
 int morea_set_sampler(morea_ctx *ctx, int mode, double rate);
@@ -218,7 +222,8 @@ int morea_repair(morea_ctx *ctx, int pop, float *offsets, const uint8_t *fixed, 
  * into the parent solution results in a solution that dominates the parent
  * solution or that is non-dominated in the current elitist archive").
  * The groups (grp_off / changed_pts, HOST arrays as for morea_eval_partial) must
- * be one colour class: pairwise disjoint dependent tets.  Per solution k and
+ * be one colour class: pairwise disjoint changed points and dependent tets
+ * (checked: MOREA_EINVAL otherwise).  Per solution k and
  * group g: z ~ N(0, I_d) (d = 6 |S_g|, SplitMix64 keys of (seed, gen,
  * sol_base + k, g), Marsaglia's polar method); x = mu + L z with the model of
  * cluster[k] (mu: n_clusters blocks of sum_g d_g doubles, group after group; L:
@@ -267,10 +272,23 @@ int morea_elasticity(morea_ctx *ctx, const uint8_t *masks, int M, const float *f
  * voxel); coverage: NULL or V bytes, 1 where owned. */
 int morea_dvf(morea_ctx *ctx, const float *offsets_one, int side, float *dvf, uint8_t *coverage);
 
-/* The dependent tets of the plan of the last morea_eval_partial call: writes
- * up to `cap` tet ids (group order, ascending within a group) into `tets` (host)
- * and the n_groups+1 offsets into `dep_off` (host).  Returns ND (>= 0). */
-int morea_partial_deps(morea_ctx *ctx, int cap, int32_t *tets, int32_t *dep_off);
+/* The dependent tets of the plan of the last morea_eval_partial,
+ * morea_mix_class or morea_prepare_partial call: writes up to `cap` tet ids
+ * (group order, ascending within a group) into `tets` (host, or NULL) and up to
+ * `off_cap` of the n_groups+1 offsets into `dep_off` (host, or NULL).
+ * Returns ND (>= 0), or ESTATE if no plan exists yet. */
+int morea_partial_deps(morea_ctx *ctx, int cap, int32_t *tets, int off_cap, int32_t *dep_off);
+/* n_groups of that plan (>= 0), or ESTATE. */
+int morea_partial_groups(const morea_ctx *ctx);
+
+/* Build (or find) the dependent-tet plan of a partial request ahead of time
+ * (same arguments as morea_eval_partial).  Plans are cached per distinct
+ * (grp_off, changed_pts) request, least recently used first out of 64, so a
+ * generation that evaluates every colour class in turn rebuilds nothing; a
+ * miss builds the plan on the host and uploads it asynchronously (pinned
+ * staging, no stream synchronisation).  Optional: morea_eval_partial builds
+ * missing plans itself. */
+int morea_prepare_partial(morea_ctx *ctx, int n_groups, const int32_t *grp_off, const int32_t *changed_pts);
 
 /* Fold check only (row a9): per solution the number of folded (tet, side) pairs
  * and their summed severity (mm^3); tet_flags (NULL or pop*2*T uint8, index
@@ -284,6 +302,14 @@ int morea_check_folds(morea_ctx *ctx, int pop, const float *offsets, int32_t *fo
  * tet id, -1 = no owner, -2 = more than one owner.  offsets_one: N*6. */
 int morea_owner_map(morea_ctx *ctx, const float *offsets_one, int side, int32_t *owner);
 
+/* Test hook (not on the hot path): the per-sample values of one side of one
+ * solution from the evaluation kernel itself (k_sweep in a dump instantiation):
+ * for every voxel centre q owned on `side`, h[q] = h(I_side(q), I_other(T(q)))
+ * as summed into f_intensity (fp32) and fg[q] = the exact O6 case decision
+ * (1: some contributing corner of the trilinear footprint is > 0); h = NaN,
+ * fg = 255 where no tet owns q.  h: V float32, fg: V bytes.  Voxel sampler only. */
+int morea_sample_map(morea_ctx *ctx, const float *offsets_one, int side, float *h, uint8_t *fg);
+
 /* Test hook: the fp32 distance map D_pair^side (V floats) built by
  * morea_load_images. */
 int morea_distance_map(morea_ctx *ctx, int side, int pair, float *out);
@@ -292,12 +318,14 @@ int morea_distance_map(morea_ctx *ctx, int side, int pair, float *out);
  * the rasterize/evaluate kernel is bracketed by CUDA events on the context
  * stream and its algorithmic work is counted.  morea_prof_read synchronises
  * and returns: launches, summed kernel milliseconds, sampled voxels, band
- * entries, tet-side items.  Reading resets the counters. */
+ * entries, (slab, solution) items and the warp-steps of the voxel sweep (32
+ * lane-steps each: the lane utilisation is samples / (32 warp_steps)).
+ * Reading resets the counters. */
 int morea_prof_enable(morea_ctx *ctx, int on);
 /* Number of kernels this context has launched since it was created. */
 int64_t morea_kernel_launches(const morea_ctx *ctx);
 int morea_prof_read(morea_ctx *ctx, int64_t *launches, double *ms, int64_t *samples,
-                    int64_t *band_entries, int64_t *items);
+                    int64_t *band_entries, int64_t *items, int64_t *warp_steps);
 
 #ifdef __cplusplus
 }

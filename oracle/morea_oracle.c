@@ -91,6 +91,9 @@ typedef struct {
     /* sample set: 0 = exactly-once voxel centres (O3), 1 = Sobol points per tet (NEXT-1) */
     int sampler;
     double rate; /* Sobol samples per voxel of tet volume */
+    /* test accessor (orc_sample_map): per-voxel h and fg of the side being sampled */
+    double *dump_h;
+    uint8_t *dump_fg;
 } orc_problem;
 
 /* ------------------------------------------------------------------ */
@@ -475,6 +478,10 @@ static void tet_side_samples(orc_problem *P, int s, const int64_t Q[2][4][3], do
                 double b_val = trilinear(P, Ioth, xp);
                 int fg = fg_exact(P, Ioth, Pnum, M);
                 *h_sum += h_of(a_val, b_val, fg);
+                if (P->dump_h) {
+                    P->dump_h[vidx(P, x, y, z)] = h_of(a_val, b_val, fg);
+                    P->dump_fg[vidx(P, x, y, z)] = (uint8_t)fg;
+                }
                 /* O8: guidance over the pairs whose source-side distance is < r */
                 for (int i = 0; i < P->K; i++) {
                     float d;
@@ -1231,6 +1238,28 @@ int orc_check_folds(orc_problem *P, const float *offsets_one, int32_t *count, do
             }
         }
     }
+    return 0;
+}
+
+/* test accessor: h and fg (the exact O6 case decision) of every voxel centre
+ * sampled on `side` for one solution (fg 255 / h NaN where no tet owns it);
+ * the same per-sample arithmetic as orc_eval, written out per voxel. */
+int orc_sample_map(orc_problem *P, const float *offsets_one, int side, double *h, uint8_t *fg) {
+    for (int64_t v = 0; v < P->V; v++) {
+        h[v] = NAN;
+        fg[v] = 255;
+    }
+    P->dump_h = h;
+    P->dump_fg = fg;
+    for (int t = 0; t < P->T; t++) {
+        int64_t Q[2][4][3];
+        if (!tet_coords(P, offsets_one, t, Q)) continue;
+        double hs = 0.0, gs = 0.0;
+        int64_t n = 0;
+        tet_side_samples(P, side, Q, &hs, &gs, &n, NULL, t);
+    }
+    P->dump_h = NULL;
+    P->dump_fg = NULL;
     return 0;
 }
 

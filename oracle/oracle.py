@@ -64,6 +64,7 @@ def lib():
         L.orc_check_folds.argtypes = [vp, vp, vp, vp, vp]
         L.orc_owner_map.argtypes = [vp, vp, ctypes.c_int, vp]
         L.orc_distance_map.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp]
+        L.orc_sample_map.argtypes = [vp, vp, ctypes.c_int, vp, vp]
         L.orc_distance_at.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp, vp]
         L.orc_sample_debug.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.orc_h.restype = ctypes.c_double
@@ -205,6 +206,14 @@ class Oracle:
         out = np.empty(self.V, dtype=np.float32)
         lib().orc_distance_map(self.h, int(side), int(pair), _p(out))
         return out
+
+    def sample_map(self, offsets_one, side):
+        """Per-voxel h (NaN = not sampled) and fg (255 = not sampled) of one side."""
+        o = self._off(offsets_one)
+        h = np.empty(self.V, dtype=np.float64)
+        fg = np.empty(self.V, dtype=np.uint8)
+        lib().orc_sample_map(self.h, _p(o), int(side), _p(h), _p(fg))
+        return h, fg
 
     def distance_at(self, side, pair, q):
         """D_pair^side at voxel centres q (n x 3 integer voxel indices)."""

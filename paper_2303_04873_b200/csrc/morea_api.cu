@@ -6,6 +6,7 @@
 // and kernel launches.  No arithmetic of the objectives happens here: every
 // step of an evaluation runs in morea_kernels.cu.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -13,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <string>
 #include <utility>
@@ -47,13 +49,53 @@ struct DevBuf {
   T* as() const { return static_cast<T*>(p); }
 };
 
-struct Plan {
-  bool valid = false;
-  std::vector<int32_t> key_off, key_pts;
-  int G = 0, S = 0, n_entries = 0;
-  std::vector<int32_t> dep_tets, dep_off;  // canonical order
-  DevBuf canon_tet, canon_slots, sched, group_off, grp_off, changed;
+// Page-locked host staging (uploads without a stream synchronisation).
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    release();
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+  ~PinnedBuf() { release(); }
 };
+
+// The static structure of one evaluation request (O10): canonical entries
+// (dependent tets of each group, tets ascending within a group), their changed
+// vertex slots, the (solution-independent) queue order, and the z-slabs of
+// k_sweep.  Built on the host once per distinct FOS request, uploaded through
+// pinned memory (no synchronisation), and kept in a small LRU cache.
+struct Plan {
+  std::vector<int32_t> key_off, key_pts;
+  unsigned long long hash = 0, last_use = 0;
+  int G = 0, S = 0, n_entries = 0, n_slabs = 0;
+  bool disjoint = true;  // dependent-tet sets pairwise disjoint (a colour class)
+  std::vector<int32_t> dep_tets, dep_off;
+  DevBuf dev;      // all device arrays below, one allocation
+  PinnedBuf host;  // their staged copy (kept alive with the plan: the upload is async)
+  const int* canon_tet = nullptr;  // nullptr: identity (the full plan)
+  const int4* canon_slots = nullptr;
+  const int* sched = nullptr;       // entries, largest tets first (k_setup, k_sobol)
+  const int* group_off = nullptr;   // G + 1 offsets into the entries
+  const int* grp_off = nullptr;     // G + 1 offsets into changed
+  const int* changed = nullptr;     // S changed point ids
+  const int* slab_off = nullptr;    // entry -> first slab (n_entries + 1)
+  const int* slab_entry = nullptr;  // slab -> entry
+  const int2* slab_z = nullptr;     // slab -> [z_begin, z_end)
+  const int* slab_sched = nullptr;  // slabs, largest first
+  const int* id_off = nullptr;      // identity offsets (Sobol mode: one slab per entry)
+};
+constexpr int kPlanCache = 64;        // distinct FOS requests kept (one per colour class and size)
+constexpr double kSlabVoxels = 4096;  // k_sweep: base-mesh voxels per z-slab (and side) at most
 
 }  // namespace
 
@@ -70,7 +112,7 @@ struct morea_ctx {
   double sp[3] = {1, 1, 1};
   double r = 0;
   double w[2][kMaxPairs] = {};
-  DevBuf I[2], band[2], dmap[2], wts, own;
+  DevBuf I[2], band[2], dmap[2], wts, own, band_runs;
   // Sobol sampler (NEXT-1): mode, rate, dilated band masks (2 V bytes), direction numbers
   int sampler = MOREA_SAMPLER_VOXEL;
   double rate = 1.0;
@@ -94,21 +136,32 @@ struct morea_ctx {
   std::vector<float> h_base;
   std::vector<int32_t> h_tets, inc_off, inc;
   std::vector<double> tet_size;
-  DevBuf full_sched, full_group_off;
   long long expect[2] = {-1, -1};  // base-mesh sample counts per side (coverage check)
   // scratch
-  DevBuf geom, scal, hgn, counter, stats;
+  DevBuf sgeom, scal, hgn, counter, stats, scratch;
   DevBuf st_off, st_nv, st_cache_in, st_base_acc, st_obj, st_acc, st_cache_out, st_i32, st_f64,
       st_u8;
-  Plan plan;
+  std::unique_ptr<Plan> full;                 // all tets, one group (set_mesh)
+  std::vector<std::unique_ptr<Plan>> plans;  // partial requests, LRU
+  Plan* plan = nullptr;                      // the plan of the last partial / mixing call
+  unsigned long long plan_clock = 0;
+  std::vector<long long> baseQ;              // base points in Q.10 (slab bounds)
   // profiling
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
   long long prof_launches = 0;
   long long kernels = 0;  // every kernel launch of this context
+  long long run_off_len = 0;  // band runs: ints of the row offsets (padded to 2) before the int2 runs
+  bool host_in = false;   // the current call staged a host input
 };
 
 namespace {
+
+// NVTX range around an ABI call or a kernel launch (closed on every return path).
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
 
 int fail(morea_ctx* c, int code, const char* fmt, ...) {
   char buf[512];
@@ -144,18 +197,24 @@ bool is_device_ptr(const void* p) {
 // Device view of an input: the pointer itself if it is device memory,
 // otherwise an async copy into `st` (pageable sources are consumed before the
 // call returns, so the caller may reuse them immediately).
+// Host sources (pageable or pinned) are consumed before the call returns: a call
+// that staged a pinned host input synchronises its stream before returning
+// (finish_outputs), so the caller may refill the buffer at once.  Device inputs
+// not 8-byte aligned are staged too (the kernels load offsets as float2).
 cudaError_t in_dev(morea_ctx* ctx, const void* p, size_t bytes, DevBuf& st, const void** out) {
   if (!p || bytes == 0) {
     *out = p;
     return cudaSuccess;
   }
-  if (is_device_ptr(p)) {
+  const bool dev = is_device_ptr(p);
+  if (dev && ((uintptr_t)p & 7u) == 0) {
     *out = p;
     return cudaSuccess;
   }
   cudaError_t e = st.ensure(bytes);
   if (e != cudaSuccess) return e;
-  e = cudaMemcpyAsync(st.p, p, bytes, cudaMemcpyHostToDevice, ctx->stream);
+  e = cudaMemcpyAsync(st.p, p, bytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream);
+  if (!dev) ctx->host_in = true;
   *out = st.p;
   return e;
 }
@@ -183,7 +242,8 @@ cudaError_t out_dev(void* p, size_t bytes, DevBuf& st, OutView& v) {
 
 // Copy staged outputs back and synchronise if any output was host memory.
 cudaError_t finish_outputs(morea_ctx* ctx, OutView* v, int n) {
-  bool any = false;
+  bool any = ctx->host_in;
+  ctx->host_in = false;
   for (int i = 0; i < n; i++) {
     if (!v[i].copy) continue;
     cudaError_t e = cudaMemcpyAsync(v[i].user, v[i].dev, v[i].bytes, cudaMemcpyDeviceToHost,
@@ -242,10 +302,13 @@ Volumes volumes_of(const morea_ctx* c) {
   v.fny2 = (float)(c->ny - 2);
   v.fnz2 = (float)(c->nz - 2);
   v.w = c->wts.as<double>();
+  v.wfd = c->wts.p ? reinterpret_cast<const float*>(c->wts.as<double>() + 2 * kMaxPairs) : nullptr;
   for (int s = 0; s < 2; s++)
     for (int i = 0; i < kMaxPairs; i++) v.wf[s][i] = c->r > 0 ? (float)(c->w[s][i] / c->r) : 0.f;
   v.rf = (float)c->r;
   v.rlo = (float)(c->r - (double)v.rf);
+  v.run_off = c->band_runs.p ? c->band_runs.as<int>() : nullptr;
+  v.runs = c->band_runs.p ? reinterpret_cast<const int2*>(c->band_runs.as<int>() + c->run_off_len) : nullptr;
   v.own[0] = c->own.as<uint2>();
   v.own[1] = v.own[0] ? v.own[0] + c->V : nullptr;
   v.use_tex = c->use_tex ? 1 : 0;
@@ -256,6 +319,7 @@ Volumes volumes_of(const morea_ctx* c) {
   v.fnyp = (float)(c->ny + 2 * pad);
   v.uoff0 = (float)(1 + pad);
   v.voff = (float)((c->ny + 2 * pad) * pad + pad + 1);
+  for (int j = 0; j < 2; j++) v.uoffI[j] = v.uoff0 + (float)j * v.fnxp;
   return v;
 }
 
@@ -272,26 +336,29 @@ MeshDev mesh_of(const morea_ctx* c) {
 
 constexpr long long kMixMaxDimHost = 192;  // = kMixMaxDim (morea_mix.cuh)
 
-int raster_grid(morea_ctx* ctx, long long n_items) {
-  long long g = (long long)ctx->n_sm * (ctx->use_tex ? ctx->blocks_per_sm_tex : ctx->blocks_per_sm);
-  const int bw = raster_block_warps();
-  long long need = (n_items + bw - 1) / bw;
-  return (int)std::max<long long>(1, std::min(g, need));
+int sweep_grid(morea_ctx* ctx) {
+  return std::max(1, ctx->n_sm * (ctx->use_tex ? ctx->blocks_per_sm_tex : ctx->blocks_per_sm));
 }
 
-// Scratch for one evaluation: SideRec per rastered (version, entry, sol, side),
-// Scal per (version, entry, sol), HGN per rastered (version, entry, sol).
+// Scratch for one evaluation: Scal per (version, entry, sol), HGN per (version,
+// slab, sol), SobolRec per (version, entry, sol, side) in Sobol mode, and one
+// WarpScratch per resident k_sweep warp.
 cudaError_t eval_scratch(morea_ctx* ctx, EvalArgs& a) {
   const size_t items = (size_t)a.n_entries * a.P;
-  cudaError_t e = ctx->geom.ensure(std::max<size_t>(1, items * a.n_raster_versions * 2) * sizeof(SideRec));
+  cudaError_t e = ctx->scal.ensure(std::max<size_t>(1, items * a.n_setup_versions) * sizeof(Scal));
   if (e != cudaSuccess) return e;
-  e = ctx->scal.ensure(std::max<size_t>(1, items * a.n_setup_versions) * sizeof(Scal));
+  e = ctx->hgn.ensure(std::max<size_t>(1, (size_t)a.n_slabs * a.P * a.n_raster_versions) * sizeof(HGN));
   if (e != cudaSuccess) return e;
-  e = ctx->hgn.ensure(std::max<size_t>(1, items * a.n_raster_versions) * sizeof(HGN));
-  if (e != cudaSuccess) return e;
-  a.geom = ctx->geom.as<SideRec>();
   a.scal = ctx->scal.as<Scal>();
   a.hgn = ctx->hgn.as<HGN>();
+  if (a.sampler == MOREA_SAMPLER_SOBOL) {
+    e = ctx->sgeom.ensure(std::max<size_t>(1, items * a.n_raster_versions * 2) * sizeof(SobolRec));
+    if (e != cudaSuccess) return e;
+    a.sgeom = ctx->sgeom.as<SobolRec>();
+  }
+  e = ctx->scratch.ensure((size_t)sweep_grid(ctx) * sweep_block_warps() * sizeof(WarpScratch));
+  if (e != cudaSuccess) return e;
+  a.scratch = ctx->scratch.as<WarpScratch>();
   e = ctx->counter.ensure(sizeof(unsigned long long));
   if (e != cudaSuccess) return e;
   a.counter = ctx->counter.as<unsigned long long>();
@@ -307,11 +374,33 @@ void set_sampler_args(const morea_ctx* ctx, EvalArgs& a) {
   a.sobol_force_exact = (fe && fe[0] && fe[0] != '0') ? 1 : 0;
 }
 
-// k_setup -> k_raster / k_sobol (the dominant kernel; bracketed by events when profiling).
+// The plan's entries, queue order and slabs into the launch arguments.
+void plan_args(const morea_ctx* ctx, const Plan& P, EvalArgs& a) {
+  a.n_entries = P.n_entries;
+  a.canon_tet = P.canon_tet;
+  a.canon_slots = P.canon_slots;
+  a.sched = P.sched;
+  set_sampler_args(ctx, a);
+  if (a.sampler == MOREA_SAMPLER_SOBOL) {
+    a.n_slabs = P.n_entries;
+    a.slab_off = P.id_off;
+  } else {
+    a.n_slabs = P.n_slabs;
+    a.slab_off = P.slab_off;
+    a.slab_entry = P.slab_entry;
+    a.slab_z = P.slab_z;
+    a.slab_sched = P.slab_sched;
+  }
+}
+
+// k_setup -> k_sweep / k_sobol (the dominant kernel; bracketed by events when profiling).
 cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
   cudaError_t e = eval_scratch(ctx, a);
   if (e != cudaSuccess) return e;
-  e = launch_setup(a, ctx->stream);
+  {
+    NvtxScope r("k_setup");
+    e = launch_setup(a, ctx->stream);
+  }
   ctx->kernels++;
   if (e != cudaSuccess) return e;
   const long long n_items = (long long)a.n_entries * a.P * a.n_raster_versions;
@@ -325,12 +414,14 @@ cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
     cudaEventRecord(e0, ctx->stream);
   }
   if (a.sampler == MOREA_SAMPLER_SOBOL) {
+    NvtxScope r("k_sobol");
     const long long g = (long long)ctx->n_sm *
                         (ctx->use_tex ? ctx->blocks_per_sm_sobol_tex : ctx->blocks_per_sm_sobol);
     const long long need = (n_items + sobol_block_warps() - 1) / sobol_block_warps();
     e = launch_sobol(a, (int)std::max<long long>(1, std::min(g, need)), ctx->stream);
   } else {
-    e = launch_raster(a, raster_grid(ctx, n_items), ctx->stream);
+    NvtxScope r("k_sweep");
+    e = launch_sweep(a, sweep_grid(ctx), ctx->stream);
   }
   ctx->kernels++;
   if (ctx->prof) {
@@ -341,28 +432,134 @@ cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
   return e;
 }
 
-// Build (or reuse) the dependent-tet plan of a partial request (host, O10).
-int build_plan(morea_ctx* ctx, int G, const int32_t* grp_off_in, const int32_t* changed_in) {
+// Slabs of the entries (k_sweep items): the lattice z range of the base tet split
+// into ceil(volume / kSlabVoxels) parts; the outer slabs are open-ended, since a
+// solution's tet may reach past the base tet's range.
+void build_slabs(const morea_ctx* ctx, const std::vector<int>& ent_tet, std::vector<int>& slab_off,
+                 std::vector<int>& slab_entry, std::vector<int2>& slab_z, std::vector<int>& slab_sched) {
+  std::vector<double> est;
+  slab_off.assign(1, 0);
+  slab_entry.clear();
+  slab_z.clear();
+  for (size_t e = 0; e < ent_tet.size(); e++) {
+    const int t = ent_tet[e];
+    long long mn = 1LL << 40, mx = -(1LL << 40);
+    for (int k = 0; k < 4; k++) {
+      const long long q = ctx->baseQ[3 * ctx->h_tets[4 * t + k] + 2];
+      mn = std::min(mn, q);
+      mx = std::max(mx, q);
+    }
+    const long long zlo = std::max<long long>(-((-mn) >> 10), 0), zhi = std::min<long long>(mx >> 10, ctx->nz - 1);
+    const long long nsl = std::max<long long>(1, zhi - zlo + 1);
+    const double vol = ctx->tet_size[t] / (6.0 * 1073741824.0);
+    const long long k = std::max<long long>(1, std::min<long long>(nsl, (long long)std::ceil(vol / kSlabVoxels)));
+    for (long long j = 0; j < k; j++) {
+      const long long b0 = zlo + j * nsl / k, b1 = zlo + (j + 1) * nsl / k;
+      slab_z.push_back(make_int2(j == 0 ? INT32_MIN : (int)b0, j == k - 1 ? INT32_MAX : (int)b1));
+      slab_entry.push_back((int)e);
+      est.push_back(vol * (double)(b1 - b0) / (double)nsl);
+    }
+    slab_off.push_back((int)slab_z.size());
+  }
+  slab_sched.resize(est.size());
+  std::iota(slab_sched.begin(), slab_sched.end(), 0);
+  std::stable_sort(slab_sched.begin(), slab_sched.end(), [&](int a, int b) { return est[a] > est[b]; });
+}
+
+// Upload the plan's arrays in one allocation through pinned staging (no sync).
+cudaError_t upload_plan(morea_ctx* ctx, Plan& P, const std::vector<int>& ct, const std::vector<int4>& cs,
+                        const std::vector<int>& sched, const std::vector<int>& group_off,
+                        const std::vector<int>& off, const std::vector<int>& pts, bool identity) {
+  std::vector<int> slab_off, slab_entry, slab_sched, id_off(P.n_entries + 1);
+  std::vector<int2> slab_z;
+  build_slabs(ctx, ct, slab_off, slab_entry, slab_z, slab_sched);
+  std::iota(id_off.begin(), id_off.end(), 0);
+  P.n_slabs = (int)slab_z.size();
+  struct Seg { const void* src; size_t bytes; size_t at; };
+  std::vector<Seg> segs;
+  size_t tot = 0;
+  auto add = [&](const void* src, size_t bytes) {
+    tot = (tot + 15) & ~(size_t)15;
+    segs.push_back({src, bytes, tot});
+    tot += std::max<size_t>(bytes, 16);
+    return segs.size() - 1;
+  };
+  const size_t i_ct = add(ct.data(), identity ? 0 : ct.size() * sizeof(int));
+  const size_t i_cs = add(cs.data(), cs.size() * sizeof(int4));
+  const size_t i_sc = add(sched.data(), sched.size() * sizeof(int));
+  const size_t i_go = add(group_off.data(), group_off.size() * sizeof(int));
+  const size_t i_of = add(off.data(), off.size() * sizeof(int));
+  const size_t i_pt = add(pts.data(), pts.size() * sizeof(int));
+  const size_t i_so = add(slab_off.data(), slab_off.size() * sizeof(int));
+  const size_t i_se = add(slab_entry.data(), slab_entry.size() * sizeof(int));
+  const size_t i_sz = add(slab_z.data(), slab_z.size() * sizeof(int2));
+  const size_t i_ss = add(slab_sched.data(), slab_sched.size() * sizeof(int));
+  const size_t i_id = add(id_off.data(), id_off.size() * sizeof(int));
+  cudaError_t e = P.dev.ensure(tot);
+  if (e != cudaSuccess) return e;
+  e = P.host.ensure(tot);
+  if (e != cudaSuccess) return e;
+  for (const Seg& g : segs)
+    if (g.bytes) std::memcpy((char*)P.host.p + g.at, g.src, g.bytes);
+  e = cudaMemcpyAsync(P.dev.p, P.host.p, tot, cudaMemcpyHostToDevice, ctx->stream);
+  if (e != cudaSuccess) return e;
+  char* d = (char*)P.dev.p;
+  P.canon_tet = identity ? nullptr : (const int*)(d + segs[i_ct].at);
+  P.canon_slots = cs.empty() ? nullptr : (const int4*)(d + segs[i_cs].at);
+  P.sched = (const int*)(d + segs[i_sc].at);
+  P.group_off = (const int*)(d + segs[i_go].at);
+  P.grp_off = (const int*)(d + segs[i_of].at);
+  P.changed = (const int*)(d + segs[i_pt].at);
+  P.slab_off = (const int*)(d + segs[i_so].at);
+  P.slab_entry = (const int*)(d + segs[i_se].at);
+  P.slab_z = (const int2*)(d + segs[i_sz].at);
+  P.slab_sched = (const int*)(d + segs[i_ss].at);
+  P.id_off = (const int*)(d + segs[i_id].at);
+  return cudaSuccess;
+}
+
+unsigned long long plan_hash(const std::vector<int32_t>& off, const std::vector<int32_t>& pts) {
+  unsigned long long h = 1469598103934665603ULL;
+  auto mix = [&](int32_t v) {
+    h ^= (unsigned)v;
+    h *= 1099511628211ULL;
+  };
+  mix((int32_t)off.size());
+  for (int32_t v : off) mix(v);
+  for (int32_t v : pts) mix(v);
+  return h;
+}
+
+// The dependent-tet plan of a partial request (host, O10), from the LRU cache
+// or built and uploaded (asynchronously) on a miss.
+int get_plan(morea_ctx* ctx, int G, const int32_t* grp_off_in, const int32_t* changed_in, Plan** out) {
   std::vector<int32_t> off, pts;
   CK(to_host(ctx, grp_off_in, (size_t)G + 1, off));
   if (off[0] != 0) return fail(ctx, MOREA_EINVAL, "grp_off[0] must be 0");
   for (int g = 0; g < G; g++)
     if (off[g + 1] < off[g]) return fail(ctx, MOREA_EINVAL, "grp_off must be non-decreasing");
   const int S = off[G];
+  if (S > 0 && !changed_in) return fail(ctx, MOREA_EINVAL, "null changed_pts");
   CK(to_host(ctx, changed_in, (size_t)S, pts));
-  Plan& P = ctx->plan;
-  if (P.valid && P.key_off == off && P.key_pts == pts) return MOREA_OK;
-  P.valid = false;
-  std::vector<int> stamp(ctx->N, -1), slot_of(ctx->N, -1), tstamp(ctx->T, -1);
+  const unsigned long long h = plan_hash(off, pts);
+  for (auto& p : ctx->plans)
+    if (p->hash == h && p->key_off == off && p->key_pts == pts) {
+      p->last_use = ++ctx->plan_clock;
+      *out = p.get();
+      return MOREA_OK;
+    }
+  std::vector<int> stamp(ctx->N, -1), slot_of(ctx->N, -1), tstamp(ctx->T, -1), towner(ctx->T, -1);
   std::vector<int32_t> dep_tets, dep_off(1, 0);
-  struct Ent { int tet; int4 slots; };
-  std::vector<Ent> ents;
+  std::vector<int> ct;
+  std::vector<int4> cs;
+  bool disjoint = true;
   for (int g = 0; g < G; g++) {
     std::vector<int32_t> D;
     for (int i = off[g]; i < off[g + 1]; i++) {
       const int j = pts[i];
       if (j < 0 || j >= ctx->N) return fail(ctx, MOREA_EINVAL, "changed point %d out of range", j);
       if (stamp[j] == g) return fail(ctx, MOREA_EINVAL, "point %d twice in group %d", j, g);
+      if (stamp[j] >= 0) disjoint = false;  // the point is in an earlier group too
       stamp[j] = g;
       slot_of[j] = i;
       for (int u = ctx->inc_off[j]; u < ctx->inc_off[j + 1]; u++) {
@@ -375,52 +572,46 @@ int build_plan(morea_ctx* ctx, int G, const int32_t* grp_off_in, const int32_t* 
     }
     std::sort(D.begin(), D.end());
     for (int t : D) {
+      if (towner[t] >= 0) disjoint = false;  // the tet depends on an earlier group too
+      towner[t] = g;
       int s4[4];
       for (int k = 0; k < 4; k++) {
         const int j = ctx->h_tets[4 * t + k];
         s4[k] = stamp[j] == g ? slot_of[j] : -1;
       }
-      ents.push_back({t, make_int4(s4[0], s4[1], s4[2], s4[3])});
+      ct.push_back(t);
+      cs.push_back(make_int4(s4[0], s4[1], s4[2], s4[3]));
       dep_tets.push_back(t);
     }
     dep_off.push_back((int32_t)dep_tets.size());
   }
-  // canonical arrays + schedule (largest tets first, stable) so the queue drains evenly
-  const size_t ne = ents.size();
-  std::vector<int> ct(ne), sched(ne);
-  std::vector<int4> cs(ne);
-  for (size_t i = 0; i < ne; i++) {
-    ct[i] = ents[i].tet;
-    cs[i] = ents[i].slots;
-  }
+  const size_t ne = ct.size();
+  std::vector<int> sched(ne);
   std::iota(sched.begin(), sched.end(), 0);
-  std::stable_sort(sched.begin(), sched.end(), [&](int a, int b) {
-    return ctx->tet_size[ents[a].tet] > ctx->tet_size[ents[b].tet];
-  });
-  CK(P.canon_tet.ensure(std::max<size_t>(ne, 1) * sizeof(int)));
-  CK(P.canon_slots.ensure(std::max<size_t>(ne, 1) * sizeof(int4)));
-  CK(P.sched.ensure(std::max<size_t>(ne, 1) * sizeof(int)));
-  CK(P.group_off.ensure((G + 1) * sizeof(int)));
-  CK(P.grp_off.ensure((G + 1) * sizeof(int)));
-  CK(P.changed.ensure(std::max(S, 1) * sizeof(int)));
-  if (ne) {
-    CK(cudaMemcpyAsync(P.canon_tet.p, ct.data(), ne * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(P.canon_slots.p, cs.data(), ne * sizeof(int4), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(P.sched.p, sched.data(), ne * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  std::stable_sort(sched.begin(), sched.end(),
+                   [&](int a, int b) { return ctx->tet_size[ct[a]] > ctx->tet_size[ct[b]]; });
+  std::unique_ptr<Plan> P(new Plan());
+  P->key_off = off;
+  P->key_pts = pts;
+  P->hash = h;
+  P->G = G;
+  P->S = S;
+  P->n_entries = (int)ne;
+  P->disjoint = disjoint;
+  P->dep_tets = dep_tets;
+  P->dep_off = dep_off;
+  CK(upload_plan(ctx, *P, ct, cs, sched, dep_off, off, pts, false));
+  P->last_use = ++ctx->plan_clock;
+  if ((int)ctx->plans.size() >= kPlanCache) {  // evict the least recently used
+    size_t v = 0;
+    for (size_t i = 1; i < ctx->plans.size(); i++)
+      if (ctx->plans[i]->last_use < ctx->plans[v]->last_use) v = i;
+    if (ctx->plan == ctx->plans[v].get()) ctx->plan = nullptr;
+    CK(cudaStreamSynchronize(ctx->stream));  // its arrays may be in use by queued work
+    ctx->plans.erase(ctx->plans.begin() + v);
   }
-  CK(cudaMemcpyAsync(P.group_off.p, dep_off.data(), (G + 1) * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(P.grp_off.p, off.data(), (G + 1) * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-  if (S) CK(cudaMemcpyAsync(P.changed.p, pts.data(), S * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-  // the host vectors above are pageable: the copies have consumed them on return
-  CK(cudaStreamSynchronize(ctx->stream));
-  P.key_off = off;
-  P.key_pts = pts;
-  P.G = G;
-  P.S = S;
-  P.n_entries = (int)ne;
-  P.dep_tets = dep_tets;
-  P.dep_off = dep_off;
-  P.valid = true;
+  *out = P.get();
+  ctx->plans.push_back(std::move(P));
   return MOREA_OK;
 }
 
@@ -567,8 +758,8 @@ int morea_create(int cuda_device, void* cuda_stream, morea_ctx** out) {
     ctx->own_stream = true;
   }
   cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, cuda_device);
-  ctx->blocks_per_sm = raster_blocks_per_sm(false);
-  ctx->blocks_per_sm_tex = raster_blocks_per_sm(true);
+  ctx->blocks_per_sm = sweep_blocks_per_sm(false);
+  ctx->blocks_per_sm_tex = sweep_blocks_per_sm(true);
   ctx->blocks_per_sm_sobol = sobol_blocks_per_sm(false);
   ctx->blocks_per_sm_sobol_tex = sobol_blocks_per_sm(true);
   {
@@ -599,18 +790,20 @@ void morea_destroy(morea_ctx* ctx) {
     cudaEventDestroy(p.second);
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
-                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->st_masks, &ctx->st_counts, &ctx->st_dvf, &ctx->st_cov,
+                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->band_runs, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->st_masks, &ctx->st_counts, &ctx->st_dvf, &ctx->st_cov,
                     &ctx->scratch_owner, &ctx->zero_off, &ctx->mx_off, &ctx->mx_acc,
                     &ctx->mx_obj, &ctx->mx_cache, &ctx->mx_nv, &ctx->mx_pobj, &ctx->mx_pacc, &ctx->mx_dep,
                     &ctx->mx_base, &ctx->mx_accepted, &ctx->mx_cluster, &ctx->mx_mu, &ctx->mx_L, &ctx->mx_arch,
                     &ctx->mx_moff, &ctx->mx_fixed, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
-                    &ctx->full_sched, &ctx->full_group_off, &ctx->geom, &ctx->scal, &ctx->hgn,
+                    &ctx->sgeom, &ctx->scal, &ctx->hgn, &ctx->scratch,
                     &ctx->counter, &ctx->stats, &ctx->st_off, &ctx->st_nv, &ctx->st_cache_in,
                     &ctx->st_base_acc, &ctx->st_obj, &ctx->st_acc, &ctx->st_cache_out,
-                    &ctx->st_i32, &ctx->st_f64, &ctx->st_u8, &ctx->plan.canon_tet,
-                    &ctx->plan.canon_slots, &ctx->plan.sched, &ctx->plan.group_off,
-                    &ctx->plan.grp_off, &ctx->plan.changed};
+                    &ctx->st_i32, &ctx->st_f64, &ctx->st_u8};
   for (DevBuf* b : bufs) b->release();
+  for (auto& p : ctx->plans) p->dev.release();
+  ctx->plans.clear();
+  if (ctx->full) ctx->full->dev.release();
+  ctx->full.reset();
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -623,6 +816,7 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
                       const float* I_s, const float* I_t, int n_pairs, const int64_t* cs_off,
                       const float* cs_xyz, const int64_t* ct_off, const float* ct_xyz,
                       double r_mm) {
+  NvtxScope nvtx_("morea_load_images");
   if (!ctx) return MOREA_EINVAL;
   CK(cudaSetDevice(ctx->device));
   if (nx < 2 || ny < 2 || nz < 2 || nx > 768 || ny > 768 || nz > 768)
@@ -636,7 +830,8 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
     return fail(ctx, MOREA_EINVAL, "n_pairs must be in [0, %d]", kMaxPairs);
   ctx->have_images = false;
   ctx->have_mesh = false;
-  ctx->plan.valid = false;
+  ctx->plans.clear();
+  ctx->plan = nullptr;
   const long long V = (long long)nx * ny * nz;
   ctx->nx = nx; ctx->ny = ny; ctx->nz = nz; ctx->V = V;
   for (int a = 0; a < 3; a++) ctx->sp[a] = sp[a];
@@ -684,8 +879,49 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
     pts.release();
     doff.release();
   }
-  CK(ctx->wts.ensure(sizeof(ctx->w)));
+  // device weights: w (fp64, 2 x kMaxPairs) then w / r (fp32, 2 x kMaxPairs)
+  CK(ctx->wts.ensure(sizeof(ctx->w) + 2 * kMaxPairs * sizeof(float)));
   CK(cudaMemcpyAsync(ctx->wts.p, ctx->w, sizeof(ctx->w), cudaMemcpyHostToDevice, ctx->stream));
+  {
+    std::vector<float> wf(2 * kMaxPairs);
+    for (int s = 0; s < 2; s++)
+      for (int i = 0; i < kMaxPairs; i++) wf[s * kMaxPairs + i] = ctx->r > 0 ? (float)(ctx->w[s][i] / ctx->r) : 0.f;
+    CK(cudaMemcpy((char*)ctx->wts.p + sizeof(ctx->w), wf.data(), wf.size() * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  // band runs (a6): per side and image row (y, z), the maximal x-runs of voxels with
+  // band bits, so the guidance pass of a row visits only band voxels
+  {
+    const long long rows = (long long)ny * nz;
+    std::vector<int> off(2 * rows + 2, 0);
+    std::vector<int> runs;
+    std::vector<unsigned char> hb((size_t)V);
+    for (int s = 0; s < 2; s++) {
+      if (K > 0) {
+        CK(cudaMemcpy(hb.data(), ctx->band[s].p, (size_t)V, cudaMemcpyDeviceToHost));
+      } else {
+        std::fill(hb.begin(), hb.end(), 0);
+      }
+      for (long long rho = 0; rho < rows; rho++) {
+        off[s * rows + rho] = (int)(runs.size() / 2);
+        const unsigned char* b = hb.data() + rho * nx;
+        for (int x = 0; x < nx;) {
+          if (!b[x]) { x++; continue; }
+          int e = x;
+          while (e + 1 < nx && b[e + 1]) e++;
+          runs.push_back(x);
+          runs.push_back(e);
+          x = e + 1;
+        }
+      }
+    }
+    off[2 * rows] = (int)(runs.size() / 2);
+    ctx->run_off_len = (2 * rows + 2);
+    CK(ctx->band_runs.ensure((off.size() + std::max<size_t>(runs.size(), 2)) * sizeof(int)));
+    CK(cudaMemcpy(ctx->band_runs.p, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!runs.empty())
+      CK(cudaMemcpy(ctx->band_runs.as<int>() + off.size(), runs.data(), runs.size() * sizeof(int),
+                    cudaMemcpyHostToDevice));
+  }
   CK(ctx->own.ensure(2 * V * sizeof(uint2)));
   for (int s = 0; s < 2; s++)
     CK(launch_own_records(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr, V,
@@ -700,6 +936,7 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
 
 int morea_set_mesh(morea_ctx* ctx, int n_points, const float* base_xyz, int n_tets,
                    const int32_t* tets, const float* c_delta, int spoke_mode) {
+  NvtxScope nvtx_("morea_set_mesh");
   if (!ctx) return MOREA_EINVAL;
   CK(cudaSetDevice(ctx->device));
   if (!ctx->have_images) return fail(ctx, MOREA_ESTATE, "morea_load_images must come first");
@@ -708,7 +945,9 @@ int morea_set_mesh(morea_ctx* ctx, int n_points, const float* base_xyz, int n_te
   if (spoke_mode != MOREA_SPOKE_FACE_CENTROID && spoke_mode != MOREA_SPOKE_TET_CENTROID)
     return fail(ctx, MOREA_EINVAL, "bad spoke_mode");
   ctx->have_mesh = false;
-  ctx->plan.valid = false;
+  CK(cudaStreamSynchronize(ctx->stream));  // cached plans may be in use by queued work
+  ctx->plans.clear();
+  ctx->plan = nullptr;
   std::vector<float> b, cd;
   std::vector<int32_t> t;
   CK(to_host(ctx, base_xyz, (size_t)n_points * 3, b));
@@ -777,22 +1016,26 @@ int morea_set_mesh(morea_ctx* ctx, int n_points, const float* base_xyz, int n_te
     CK(cudaMemcpyAsync(ctx->d_inc.p, inc.data(), inc.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
                        ctx->stream));
   ctx->tet_size = size;
-  std::vector<int> order(n_tets);
+  ctx->baseQ = Q;
+  std::vector<int> order(n_tets), all(n_tets);
   std::iota(order.begin(), order.end(), 0);
+  std::iota(all.begin(), all.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int a, int c) { return size[a] > size[c]; });
-  const int goff[2] = {0, n_tets};
+  const std::vector<int> goff = {0, n_tets};
   CK(ctx->base.ensure(b.size() * sizeof(float)));
   CK(ctx->tets.ensure(t.size() * sizeof(int32_t)));
   CK(ctx->cdelta.ensure(cd.size() * sizeof(float)));
   CK(ctx->ref.ensure(ref.size()));
-  CK(ctx->full_sched.ensure(n_tets * sizeof(int)));
-  CK(ctx->full_group_off.ensure(2 * sizeof(int)));
   CK(cudaMemcpyAsync(ctx->base.p, b.data(), b.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->tets.p, t.data(), t.size() * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->cdelta.p, cd.data(), cd.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->ref.p, ref.data(), ref.size(), cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->full_sched.p, order.data(), n_tets * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->full_group_off.p, goff, 2 * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  // the full-evaluation plan: every tet, one group, identity entries
+  ctx->full.reset(new Plan());
+  ctx->full->G = 1;
+  ctx->full->n_entries = n_tets;
+  CK(upload_plan(ctx, *ctx->full, all, std::vector<int4>(), order, goff, std::vector<int>{0}, std::vector<int>(),
+                 true));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->have_mesh = true;
   // coverage reference: per-side owned-sample counts of the base mesh (zero offsets)
@@ -807,19 +1050,24 @@ int morea_set_mesh(morea_ctx* ctx, int n_points, const float* base_xyz, int n_te
     a.mesh = mesh_of(ctx);
     a.P = 1;
     a.offsets = zoff.as<float>();
-    a.n_entries = n_tets;
-    a.sched = ctx->full_sched.as<int>();
+    plan_args(ctx, *ctx->full, a);
+    a.sampler = MOREA_SAMPLER_VOXEL;  // the coverage reference is always voxel centres
+    a.n_slabs = ctx->full->n_slabs;
+    a.slab_off = ctx->full->slab_off;
+    a.slab_entry = ctx->full->slab_entry;
+    a.slab_z = ctx->full->slab_z;
+    a.slab_sched = ctx->full->slab_sched;
     a.n_setup_versions = 1;
     a.n_raster_versions = 1;
     a.expect[0] = a.expect[1] = -1;
     CK(run_eval(ctx, a));
-    std::vector<HGN> hg(n_tets);
-    CK(cudaMemcpyAsync(hg.data(), ctx->hgn.p, n_tets * sizeof(HGN), cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<HGN> hg(a.n_slabs);
+    CK(cudaMemcpyAsync(hg.data(), ctx->hgn.p, hg.size() * sizeof(HGN), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     long long c0 = 0, c1 = 0;
-    for (int t = 0; t < n_tets; t++) {
-      c0 += hg[t].n0;
-      c1 += hg[t].n - hg[t].n0;
+    for (const HGN& x : hg) {
+      c0 += x.n0;
+      c1 += x.n - x.n0;
     }
     ctx->expect[0] = c0;
     ctx->expect[1] = c1;
@@ -847,8 +1095,10 @@ int morea_eval_full(morea_ctx* ctx, int pop, const float* offsets, double* obj, 
   CK(cudaSetDevice(ctx->device));
   if (pop < 0 || (pop > 0 && !offsets)) return fail(ctx, MOREA_EINVAL, "bad pop / offsets");
   if (pop == 0) return MOREA_OK;
+  NvtxScope nvtx_("morea_eval_full");
   const int N = ctx->N, T = ctx->T;
   const float* off = nullptr;
+  ctx->host_in = false;
   CK(in_dev(ctx, offsets, (size_t)pop * N * 6 * sizeof(float), ctx->st_off, (const void**)&off));
   OutView ov[3];
   CK(out_dev(obj, (size_t)pop * 3 * sizeof(double), ctx->st_obj, ov[0]));
@@ -860,53 +1110,56 @@ int morea_eval_full(morea_ctx* ctx, int pop, const float* offsets, double* obj, 
   a.mesh = mesh_of(ctx);
   a.P = pop;
   a.offsets = off;
-  a.n_entries = T;
-  a.canon_tet = nullptr;
-  a.canon_slots = nullptr;
-  a.sched = ctx->full_sched.as<int>();
+  plan_args(ctx, *ctx->full, a);
   a.partial = 0;
   a.n_setup_versions = 1;
   a.n_raster_versions = 1;
   a.expect[0] = ctx->sampler == MOREA_SAMPLER_VOXEL ? ctx->expect[0] : -1;
   a.expect[1] = ctx->sampler == MOREA_SAMPLER_VOXEL ? ctx->expect[1] : -1;
-  set_sampler_args(ctx, a);
   CK(run_eval(ctx, a));
-  CK(launch_reduce(a, 1, ctx->full_group_off.as<int>(), nullptr, nullptr, (double*)ov[2].dev,
-                   nullptr, nullptr, (double*)ov[0].dev, ov[1].dev, ctx->stream));
+  CK(launch_reduce(a, 1, ctx->full->group_off, nullptr, nullptr, (double*)ov[2].dev, nullptr, nullptr,
+                   (double*)ov[0].dev, ov[1].dev, ctx->stream));
   ctx->kernels++;
   CK(finish_outputs(ctx, ov, 3));
   return MOREA_OK;
 }
 
-// a8 on device buffers: the plan of ctx->plan, base offsets/acc, new values,
-// optional cache; outputs per (solution, group) and the dependent-tet cache rows
-static cudaError_t partial_core(morea_ctx* ctx, int pop, int G, const float* off, const morea_acc* bacc,
-                                const float* nv, const double* cin, double* obj, morea_acc* acc,
-                                double* dep_out) {
-  const Plan& P = ctx->plan;
+// a8 on device buffers: the plan P, base offsets/acc, new values, optional
+// cache; outputs per (solution, group) and the dependent-tet cache rows
+static cudaError_t partial_core(morea_ctx* ctx, const Plan& P, int pop, int G, const float* off,
+                                const morea_acc* bacc, const float* nv, const double* cin, double* obj,
+                                morea_acc* acc, double* dep_out) {
   EvalArgs a;
   std::memset(&a, 0, sizeof(a));
   a.vol = volumes_of(ctx);
   a.mesh = mesh_of(ctx);
   a.P = pop;
   a.offsets = off;
-  a.n_entries = P.n_entries;
-  a.canon_tet = P.canon_tet.as<int>();
-  a.canon_slots = P.canon_slots.as<int4>();
-  a.sched = P.sched.as<int>();
+  plan_args(ctx, P, a);
   a.new_vals = nv;
   a.S_total = P.S;
   a.partial = 1;
   a.n_setup_versions = 2;
   a.n_raster_versions = cin ? 1 : 2;
   a.expect[0] = a.expect[1] = -1;
-  set_sampler_args(ctx, a);
   cudaError_t e = run_eval(ctx, a);
   if (e != cudaSuccess) return e;
-  e = launch_reduce(a, G, P.group_off.as<int>(), bacc, cin, dep_out, P.changed.as<int>(), P.grp_off.as<int>(),
-                    obj, acc, ctx->stream);
+  e = launch_reduce(a, G, P.group_off, bacc, cin, dep_out, P.changed, P.grp_off, obj, acc, ctx->stream);
   ctx->kernels++;
   return e;
+}
+
+int morea_prepare_partial(morea_ctx* ctx, int n_groups, const int32_t* grp_off, const int32_t* changed_pts) {
+  NvtxScope nvtx_("morea_prepare_partial");
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  if (n_groups < 0 || !grp_off) return fail(ctx, MOREA_EINVAL, "bad groups");
+  Plan* P = nullptr;
+  rc = get_plan(ctx, n_groups, grp_off, changed_pts, &P);
+  if (rc) return rc;
+  ctx->plan = P;
+  return MOREA_OK;
 }
 
 int morea_eval_partial(morea_ctx* ctx, int pop, const float* base_offsets,
@@ -918,15 +1171,19 @@ int morea_eval_partial(morea_ctx* ctx, int pop, const float* base_offsets,
   CK(cudaSetDevice(ctx->device));
   if (pop < 0 || n_groups < 0 || !grp_off) return fail(ctx, MOREA_EINVAL, "bad pop / groups");
   if (pop > 0 && (!base_offsets || !base_acc)) return fail(ctx, MOREA_EINVAL, "null base inputs");
-  rc = build_plan(ctx, n_groups, grp_off, changed_pts);
+  NvtxScope nvtx_("morea_eval_partial");
+  Plan* Pp = nullptr;
+  rc = get_plan(ctx, n_groups, grp_off, changed_pts, &Pp);
   if (rc) return rc;
+  ctx->plan = Pp;
+  const Plan& P = *Pp;
   if (pop == 0 || n_groups == 0) return MOREA_OK;
-  const Plan& P = ctx->plan;
   if (P.S > 0 && !new_vals) return fail(ctx, MOREA_EINVAL, "null new_vals");
   const int N = ctx->N, T = ctx->T, G = n_groups;
   const float *off = nullptr, *nv = nullptr;
   const double* cin = nullptr;
   const morea_acc* bacc = nullptr;
+  ctx->host_in = false;
   CK(in_dev(ctx, base_offsets, (size_t)pop * N * 6 * sizeof(float), ctx->st_off, (const void**)&off));
   CK(in_dev(ctx, new_vals, (size_t)pop * P.S * 6 * sizeof(float), ctx->st_nv, (const void**)&nv));
   CK(in_dev(ctx, tet_cache, (size_t)pop * T * 4 * sizeof(double), ctx->st_cache_in, (const void**)&cin));
@@ -935,13 +1192,14 @@ int morea_eval_partial(morea_ctx* ctx, int pop, const float* base_offsets,
   CK(out_dev(obj, (size_t)pop * G * 3 * sizeof(double), ctx->st_obj, ov[0]));
   CK(out_dev(acc, (size_t)pop * G * sizeof(morea_acc), ctx->st_acc, ov[1]));
   CK(out_dev(dep_cache_out, (size_t)pop * P.n_entries * 4 * sizeof(double), ctx->st_cache_out, ov[2]));
-  CK(partial_core(ctx, pop, G, off, bacc, nv, cin, (double*)ov[0].dev, (morea_acc*)ov[1].dev,
+  CK(partial_core(ctx, P, pop, G, off, bacc, nv, cin, (double*)ov[0].dev, (morea_acc*)ov[1].dev,
                   (double*)ov[2].dev));
   CK(finish_outputs(ctx, ov, 3));
   return MOREA_OK;
 }
 
 int morea_set_sampler(morea_ctx* ctx, int mode, double rate) {
+  NvtxScope nvtx_("morea_set_sampler");
   if (!ctx) return MOREA_EINVAL;
   if (mode != MOREA_SAMPLER_VOXEL && mode != MOREA_SAMPLER_SOBOL)
     return fail(ctx, MOREA_EINVAL, "unknown sampler mode %d", mode);
@@ -955,6 +1213,7 @@ int morea_set_sampler(morea_ctx* ctx, int mode, double rate) {
 
 int morea_repair(morea_ctx* ctx, int pop, float* offsets, const uint8_t* fixed, uint64_t seed,
                  int64_t sol_base, int32_t* moved, int32_t* aborted) {
+  NvtxScope nvtx_("morea_repair");
   int rc = check_ready(ctx);
   if (rc) return rc;
   CK(cudaSetDevice(ctx->device));
@@ -991,8 +1250,13 @@ static int export_args(morea_ctx* ctx, const float* offsets_one, EvalArgs& a) {
   a.mesh = mesh_of(ctx);
   a.P = 1;
   a.offsets = off;
-  a.n_entries = ctx->T;
-  a.sched = ctx->full_sched.as<int>();
+  plan_args(ctx, *ctx->full, a);
+  a.sampler = MOREA_SAMPLER_VOXEL;  // the exports always use the voxel-centre sample set
+  a.n_slabs = ctx->full->n_slabs;
+  a.slab_off = ctx->full->slab_off;
+  a.slab_entry = ctx->full->slab_entry;
+  a.slab_z = ctx->full->slab_z;
+  a.slab_sched = ctx->full->slab_sched;
   a.n_setup_versions = 1;
   a.n_raster_versions = 1;
   a.expect[0] = a.expect[1] = -1;
@@ -1002,6 +1266,7 @@ static int export_args(morea_ctx* ctx, const float* offsets_one, EvalArgs& a) {
 
 int morea_label_counts(morea_ctx* ctx, const float* offsets_one, int side, const uint8_t* masks, int M,
                        int64_t* counts) {
+  NvtxScope nvtx_("morea_label_counts");
   int rc = check_ready(ctx);
   if (rc) return rc;
   CK(cudaSetDevice(ctx->device));
@@ -1014,7 +1279,7 @@ int morea_label_counts(morea_ctx* ctx, const float* offsets_one, int side, const
   CK(in_dev(ctx, masks, (size_t)ctx->V, ctx->st_masks, (const void**)&m));
   OutView ov[1];
   CK(out_dev(counts, (size_t)ctx->T * (M + 1) * sizeof(int64_t), ctx->st_counts, ov[0]));
-  CK(launch_label_counts(a, side, m, M, (long long*)ov[0].dev, ctx->stream));
+  CK(launch_label_counts(a, sweep_grid(ctx), side, m, M, (long long*)ov[0].dev, ctx->stream));
   ctx->kernels += 2;
   CK(finish_outputs(ctx, ov, 1));
   return MOREA_OK;
@@ -1049,6 +1314,7 @@ int morea_elasticity(morea_ctx* ctx, const uint8_t* masks, int M, const float* f
 }
 
 int morea_dvf(morea_ctx* ctx, const float* offsets_one, int side, float* dvf, uint8_t* coverage) {
+  NvtxScope nvtx_("morea_dvf");
   int rc = check_ready(ctx);
   if (rc) return rc;
   CK(cudaSetDevice(ctx->device));
@@ -1062,7 +1328,7 @@ int morea_dvf(morea_ctx* ctx, const float* offsets_one, int side, float* dvf, ui
   CK(out_dev(coverage, (size_t)ctx->V, ctx->st_cov, ov[1]));
   unsigned char* cov = ov[1].dev ? (unsigned char*)ov[1].dev : ctx->st_cov.as<unsigned char>();
   CK(ctx->scratch_owner.ensure((size_t)ctx->V * sizeof(int)));
-  CK(launch_dvf(a, side, ctx->scratch_owner.as<int>(), (float*)ov[0].dev, cov, ctx->stream));
+  CK(launch_dvf(a, sweep_grid(ctx), side, ctx->scratch_owner.as<int>(), (float*)ov[0].dev, cov, ctx->stream));
   ctx->kernels += 4;
   CK(finish_outputs(ctx, ov, 2));
   return MOREA_OK;
@@ -1080,6 +1346,7 @@ int morea_mix_class(morea_ctx* ctx, int pop, float* offsets, morea_acc* acc, dou
                     int n_clusters, const double* mu, const double* L, const uint8_t* fixed, int n_archive,
                     const double* archive, double steer_max, uint64_t seed, int64_t gen, int64_t sol_base,
                     uint8_t* accepted) {
+  NvtxScope nvtx_("morea_mix_class");
   int rc = check_ready(ctx);
   if (rc) return rc;
   CK(cudaSetDevice(ctx->device));
@@ -1088,10 +1355,15 @@ int morea_mix_class(morea_ctx* ctx, int pop, float* offsets, morea_acc* acc, dou
   if (pop > 0 && (!offsets || !acc || !obj || !tet_cache || !cluster || !mu || !L))
     return fail(ctx, MOREA_EINVAL, "null state or model");
   if (n_archive > 0 && !archive) return fail(ctx, MOREA_EINVAL, "null archive");
-  rc = build_plan(ctx, n_groups, grp_off, changed_pts);
+  Plan* Pp = nullptr;
+  rc = get_plan(ctx, n_groups, grp_off, changed_pts, &Pp);
   if (rc) return rc;
+  ctx->plan = Pp;
+  const Plan& P = *Pp;
+  if (!P.disjoint)
+    return fail(ctx, MOREA_EINVAL, "the groups of morea_mix_class must be one colour class (pairwise disjoint "
+                                   "changed points and dependent tets)");
   if (pop == 0 || n_groups == 0) return MOREA_OK;
-  const Plan& P = ctx->plan;
   const int N = ctx->N, T = ctx->T, G = n_groups;
   // model layout: per cluster, mu_g (d_g) then the next group's; L_g (d_g^2) likewise
   std::vector<long long> moff(2 * G);
@@ -1138,8 +1410,8 @@ int morea_mix_class(morea_ctx* ctx, int pop, float* offsets, morea_acc* acc, dou
   m.sol_base = sol_base;
   m.offsets = (const float*)ov[0].dev;
   m.new_vals = ctx->mx_nv.as<float>();
-  m.grp_off = P.grp_off.as<int>();
-  m.changed = P.changed.as<int>();
+  m.grp_off = P.grp_off;
+  m.changed = P.changed;
   m.model_off = ctx->mx_moff.as<long long>();
   m.mu_stride = mu_stride;
   m.L_stride = L_stride;
@@ -1154,34 +1426,40 @@ int morea_mix_class(morea_ctx* ctx, int pop, float* offsets, morea_acc* acc, dou
   // a8: every candidate against the class-start state, with the per-tet cache
   CK(cudaMemcpyAsync(ctx->mx_base.p, ov[1].dev, (size_t)pop * sizeof(morea_acc), cudaMemcpyDeviceToDevice,
                      ctx->stream));
-  CK(partial_core(ctx, pop, G, (const float*)ov[0].dev, ctx->mx_base.as<morea_acc>(), ctx->mx_nv.as<float>(),
+  CK(partial_core(ctx, P, pop, G, (const float*)ov[0].dev, ctx->mx_base.as<morea_acc>(), ctx->mx_nv.as<float>(),
                   (const double*)ov[3].dev, ctx->mx_pobj.as<double>(), ctx->mx_pacc.as<morea_acc>(),
                   ctx->mx_dep.as<double>()));
   // M4-M6: acceptance in group order, then commit
   CK(launch_mix_accept(pop, G, T, ctx->mx_base.as<morea_acc>(), ctx->mx_pacc.as<morea_acc>(),
                        (morea_acc*)ov[1].dev, (double*)ov[2].dev, ar_d, n_archive, steer_max, acc_flags,
                        ctx->stream));
-  CK(launch_mix_commit(pop, G, N, T, P.S, P.n_entries, acc_flags, P.grp_off.as<int>(), P.changed.as<int>(),
-                       P.group_off.as<int>(), P.canon_tet.as<int>(), ctx->mx_nv.as<float>(),
+  CK(launch_mix_commit(pop, G, N, T, P.S, P.n_entries, acc_flags, P.grp_off, P.changed,
+                       P.group_off, P.canon_tet, ctx->mx_nv.as<float>(),
                        ctx->mx_dep.as<double>(), (float*)ov[0].dev, (double*)ov[3].dev, ctx->stream));
   ctx->kernels += 2;
   CK(finish_outputs(ctx, ov, 5));
   return MOREA_OK;
 }
 
-int morea_partial_deps(morea_ctx* ctx, int cap, int32_t* tets, int32_t* dep_off) {
+int morea_partial_deps(morea_ctx* ctx, int cap, int32_t* tets, int off_cap, int32_t* dep_off) {
   if (!ctx) return MOREA_EINVAL;
-  if (!ctx->plan.valid) return fail(ctx, MOREA_ESTATE, "no partial plan yet");
-  const Plan& P = ctx->plan;
+  if (!ctx->plan) return fail(ctx, MOREA_ESTATE, "no partial plan yet");
+  const Plan& P = *ctx->plan;
   if (tets)
     for (int i = 0; i < std::min<int>(cap, (int)P.dep_tets.size()); i++) tets[i] = P.dep_tets[i];
   if (dep_off)
-    for (int g = 0; g <= P.G; g++) dep_off[g] = P.dep_off[g];
+    for (int g = 0; g <= std::min(P.G, off_cap - 1); g++) dep_off[g] = P.dep_off[g];
   return (int)P.dep_tets.size();
+}
+
+int morea_partial_groups(const morea_ctx* ctx) {
+  if (!ctx) return MOREA_EINVAL;
+  return ctx->plan ? ctx->plan->G : MOREA_ESTATE;
 }
 
 int morea_check_folds(morea_ctx* ctx, int pop, const float* offsets, int32_t* fold_count,
                       double* severity, uint8_t* tet_flags) {
+  NvtxScope nvtx_("morea_check_folds");
   int rc = check_ready(ctx);
   if (rc) return rc;
   CK(cudaSetDevice(ctx->device));
@@ -1201,6 +1479,7 @@ int morea_check_folds(morea_ctx* ctx, int pop, const float* offsets, int32_t* fo
 }
 
 int morea_owner_map(morea_ctx* ctx, const float* offsets_one, int side, int32_t* owner) {
+  NvtxScope nvtx_("morea_owner_map");
   int rc = check_ready(ctx);
   if (rc) return rc;
   CK(cudaSetDevice(ctx->device));
@@ -1215,15 +1494,53 @@ int morea_owner_map(morea_ctx* ctx, const float* offsets_one, int side, int32_t*
   a.mesh = mesh_of(ctx);
   a.P = 1;
   a.offsets = off;
-  a.n_entries = ctx->T;
-  a.sched = ctx->full_sched.as<int>();
+  plan_args(ctx, *ctx->full, a);
+  a.sampler = MOREA_SAMPLER_VOXEL;
+  a.n_slabs = ctx->full->n_slabs;
+  a.slab_off = ctx->full->slab_off;
+  a.slab_entry = ctx->full->slab_entry;
+  a.slab_z = ctx->full->slab_z;
+  a.slab_sched = ctx->full->slab_sched;
   a.n_setup_versions = 1;
   a.n_raster_versions = 1;
   a.expect[0] = a.expect[1] = -1;
   CK(eval_scratch(ctx, a));
-  CK(launch_owner_map(a, side, (int*)ov[0].dev, ctx->stream));
-  ctx->kernels += 3;
+  CK(launch_owner_map(a, sweep_grid(ctx), side, (int*)ov[0].dev, ctx->stream));
+  ctx->kernels += 2;
   CK(finish_outputs(ctx, ov, 1));
+  return MOREA_OK;
+}
+
+int morea_sample_map(morea_ctx* ctx, const float* offsets_one, int side, float* h, uint8_t* fg) {
+  NvtxScope nvtx_("morea_sample_map");
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  if (!offsets_one || !h || !fg || (side != 0 && side != 1)) return fail(ctx, MOREA_EINVAL, "bad args");
+  if (ctx->sampler != MOREA_SAMPLER_VOXEL) return fail(ctx, MOREA_ESTATE, "morea_sample_map needs the voxel sampler");
+  const float* off = nullptr;
+  ctx->host_in = false;
+  CK(in_dev(ctx, offsets_one, (size_t)ctx->N * 6 * sizeof(float), ctx->st_off, (const void**)&off));
+  OutView ov[2];
+  CK(out_dev(h, (size_t)ctx->V * sizeof(float), ctx->st_f64, ov[0]));
+  CK(out_dev(fg, (size_t)ctx->V, ctx->st_u8, ov[1]));
+  CK(launch_fill((float*)ov[0].dev, (unsigned char*)ov[1].dev, ctx->V, ctx->stream));
+  EvalArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.vol = volumes_of(ctx);
+  a.mesh = mesh_of(ctx);
+  a.P = 1;
+  a.offsets = off;
+  plan_args(ctx, *ctx->full, a);
+  a.n_setup_versions = 1;
+  a.n_raster_versions = 1;
+  a.expect[0] = a.expect[1] = -1;
+  a.dump_h = (float*)ov[0].dev;
+  a.dump_fg = (unsigned char*)ov[1].dev;
+  a.dump_side = side;
+  CK(run_eval(ctx, a));
+  ctx->kernels++;
+  CK(finish_outputs(ctx, ov, 2));
   return MOREA_OK;
 }
 
@@ -1247,7 +1564,7 @@ int morea_prof_enable(morea_ctx* ctx, int on) {
 }
 
 int morea_prof_read(morea_ctx* ctx, int64_t* launches, double* ms, int64_t* samples,
-                    int64_t* band_entries, int64_t* items) {
+                    int64_t* band_entries, int64_t* items, int64_t* warp_steps) {
   if (!ctx) return MOREA_EINVAL;
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1268,6 +1585,7 @@ int morea_prof_read(morea_ctx* ctx, int64_t* launches, double* ms, int64_t* samp
   if (samples) *samples = (int64_t)st[0];
   if (band_entries) *band_entries = (int64_t)st[1];
   if (items) *items = (int64_t)st[2];
+  if (warp_steps) *warp_steps = (int64_t)st[3];
   ctx->prof_launches = 0;
   return MOREA_OK;
 }

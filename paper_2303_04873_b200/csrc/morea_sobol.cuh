@@ -200,12 +200,8 @@ constexpr int kSobolThreads = 32 * kSobolWarps;
 template <bool TEX>
 __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
   __shared__ SobolWarp smem[kSobolWarps];
-#if MOREA_SOBOL_CLAIM_LOCAL
   __shared__ BlockQueue bq;
   bq.init();
-#else
-  __shared__ unsigned long long chunk;
-#endif
   __shared__ unsigned sV[4][32];
   int warp, lane;
   asm volatile("shr.u32 %0, %1, 5;" : "=r"(warp) : "r"(threadIdx.x));
@@ -231,17 +227,8 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
   const long long n_items = per_v * A.n_raster_versions;
   if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0ull;
   while (true) {
-#if MOREA_SOBOL_CLAIM_LOCAL
     const unsigned long long item = bq.claim(A.counter, lane, n_items, MOREA_CLAIM_CHUNK, MOREA_CLAIM_SPREAD);
     if ((long long)item >= n_items) break;
-#else
-    __syncthreads();
-    if (threadIdx.x == 0) chunk = atomicAdd(A.counter, (unsigned long long)kSobolWarps);
-    __syncthreads();
-    if ((long long)chunk >= n_items) break;  // block-uniform
-    const unsigned long long item = chunk + warp;
-    if ((long long)item >= n_items) continue;
-#endif
     const int ver = (int)(item / (unsigned long long)per_v);
     const long long rem = (long long)item - (long long)ver * per_v;
     const int es = (int)(rem / A.P);
@@ -258,7 +245,7 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
       __syncwarp();
       if (lane < kVec)
         reinterpret_cast<int4*>(&S.R)[lane] =
-            __ldg(reinterpret_cast<const int4*>(&A.geom[2 * i + side]) + lane);
+            __ldg(reinterpret_cast<const int4*>(&A.sgeom[2 * i + side]) + lane);
       __syncwarp();
       const SobolRec& R = S.R;
       if (!(R.flags & 1)) continue;
@@ -284,7 +271,7 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
       // g(s0 + 32) ^ g(s0) = 2^4 ^ 2^(5 + ctz(m + 1)), so two direction numbers
       // per dimension change (warp-uniform)
       unsigned x0 = m0, x1 = m1, x2 = m2, x3 = m3;
-      const int Ni = (int)N;  // < 2^31: rate <= 8 (morea_set_sampler)
+      const int Ni = (int)N;  // < 2^31: k_setup flags larger counts (DOMAIN) and clears the side
 #pragma unroll 1
       for (int s0 = 0; s0 < Ni; s0 += 32) {
         if (s0 > 0) {
@@ -357,7 +344,7 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
             }
             if (d < V.rf) {
               const float dd = d - Dp;
-              gf += V.wf[side][pi] * ((V.rf - d) + V.rlo) * (dd * dd);
+              gf += __ldg(&V.wfd[side * kMaxPairs + pi]) * ((V.rf - d) + V.rlo) * (dd * dd);
             }
           }
         }
@@ -373,14 +360,13 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
     HGN out;
     out.h = warp_sum_d(hsum);
     out.g = warp_sum_d(gsum);
-    out.n = (int)n_tot;
-    out.nb = warp_sum_i(nb);
-    out.n0 = (int)n_side0;
-    out.pad = 0;
+    out.n = n_tot;
+    out.n0 = n_side0;
+    const int nb_w = warp_sum_i(nb);
     if (lane == 0) {
       A.hgn[i] = out;
       S.stat[0] += n_tot;
-      S.stat[1] += out.nb;
+      S.stat[1] += nb_w;
       S.stat[2] += 1;
     }
   }

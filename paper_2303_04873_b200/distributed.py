@@ -42,10 +42,13 @@ def all_gather_records(local: torch.Tensor, P_total: int, rows_per_solution: int
     """
     world = dist.get_world_size(group)
     rows_max = (P_total + world - 1) // world * rows_per_solution
-    buf = torch.zeros((rows_max, RECORD_WORDS), dtype=torch.int64, device=local.device)
-    buf[: local.shape[0]] = local
-    out = torch.empty((world * rows_max, RECORD_WORDS), dtype=torch.int64, device=local.device)
-    if dist.get_backend(group) == "nccl":
+    nccl = dist.get_backend(group) == "nccl"
+    # gloo moves host tensors: device records are staged through host memory
+    dev = local.device if nccl else torch.device("cpu")
+    buf = torch.zeros((rows_max, RECORD_WORDS), dtype=torch.int64, device=dev)
+    buf[: local.shape[0]] = local.to(dev)
+    out = torch.empty((world * rows_max, RECORD_WORDS), dtype=torch.int64, device=dev)
+    if nccl:
         dist.all_gather_into_tensor(out, buf, group=group)
     else:
         parts = list(out.chunk(world))
@@ -55,4 +58,4 @@ def all_gather_records(local: torch.Tensor, P_total: int, rows_per_solution: int
     for r in range(world):
         s, e = shard_bounds(P_total, world, r)
         keep.append(out[r * rows_max: r * rows_max + (e - s) * rows_per_solution])
-    return torch.cat(keep)
+    return torch.cat(keep).to(local.device)

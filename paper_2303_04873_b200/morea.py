@@ -32,7 +32,7 @@ EXPORTS = ["morea_create", "morea_destroy", "morea_last_error", "morea_stream", 
            "morea_set_mesh", "morea_eval_full", "morea_eval_partial", "morea_partial_deps",
            "morea_check_folds", "morea_owner_map", "morea_distance_map", "morea_prof_enable",
            "morea_prof_read", "morea_kernel_launches", "morea_set_sampler", "morea_repair", "morea_label_counts", "morea_elasticity", "morea_dvf",
-           "morea_mix_class"]
+           "morea_mix_class", "morea_prepare_partial", "morea_partial_groups", "morea_sample_map"]
 SAMPLER_VOXEL = 0
 SAMPLER_SOBOL = 1
 
@@ -60,9 +60,12 @@ def _load():
     L.morea_set_mesh.argtypes = [vp, i32, vp, i32, vp, vp, i32]
     L.morea_eval_full.argtypes = [vp, i32, vp, vp, vp, vp]
     L.morea_eval_partial.argtypes = [vp, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp]
-    L.morea_partial_deps.argtypes = [vp, i32, vp, vp]
+    L.morea_partial_deps.argtypes = [vp, i32, vp, i32, vp]
+    L.morea_partial_groups.argtypes = [vp]
+    L.morea_prepare_partial.argtypes = [vp, i32, vp, vp]
     L.morea_check_folds.argtypes = [vp, i32, vp, vp, vp, vp]
     L.morea_owner_map.argtypes = [vp, vp, i32, vp]
+    L.morea_sample_map.argtypes = [vp, vp, i32, vp, vp]
     L.morea_distance_map.argtypes = [vp, i32, i32, vp]
     L.morea_prof_enable.argtypes = [vp, i32]
     L.morea_set_sampler.argtypes = [vp, i32, f64]
@@ -75,7 +78,7 @@ def _load():
     L.morea_kernel_launches.argtypes = [vp]
     L.morea_kernel_launches.restype = i64
     L.morea_prof_read.argtypes = [vp] + [ctypes.POINTER(i64), ctypes.POINTER(f64)] + \
-        [ctypes.POINTER(i64)] * 3
+        [ctypes.POINTER(i64)] * 4
     return L
 
 
@@ -109,6 +112,31 @@ def _is_torch(a):
     return hasattr(a, "data_ptr") and not isinstance(a, np.ndarray)
 
 
+_DT = {"f4": ("float32",), "f8": ("float64",), "i8": ("int64",), "i4": ("int32",), "u1": ("uint8",)}
+
+
+def _check(a, name, kind, shape):
+    """Marshalling guard: dtype and shape of an array handed to the C-ABI (the library
+    reads raw pointers, so a wrong dtype would be silently misread)."""
+    if a is None:
+        return
+    if not _is_torch(a) and kind == "i8" and a.dtype == ACC_DTYPE:
+        dt = "int64"  # structured accumulator records: 48 bytes = 6 x int64
+        a = a.view(np.uint8)
+        if a.size < 48 * (shape[0] if shape else 1):
+            raise ValueError(f"{name}: {a.size} bytes, at least {48 * shape[0]} needed")
+        return
+    dt = str(a.dtype).replace("torch.", "")
+    if dt not in _DT[kind]:
+        raise TypeError(f"{name}: dtype {dt}, expected {_DT[kind][0]}")
+    n = 1
+    for d in shape:
+        n *= d
+    got = int(a.numel()) if _is_torch(a) else int(a.size)
+    if got < n:
+        raise ValueError(f"{name}: {got} elements, at least {n} {tuple(shape)} needed")
+
+
 class Context:
     """One evaluator instance bound to one CUDA device (include/morea.h)."""
 
@@ -122,7 +150,6 @@ class Context:
         self.device = device
         self.N = self.T = self.V = self.K = 0
         self.dims = None
-        self._last_G = 0
 
     def close(self):
         if getattr(self, "h", None):
@@ -180,6 +207,10 @@ class Context:
         """offsets: (P, N, 6) float32 (device or host).  Outputs are written into
         the given arrays (device or host); returns (obj, acc, tet_cache)."""
         P = int(offsets.shape[0])
+        _check(offsets, "offsets", "f4", (P, self.N, 6))
+        _check(obj, "obj", "f8", (P, 3))
+        _check(acc, "acc", "i8", (P, 6))
+        _check(tet_cache, "tet_cache", "f8", (P, self.T, 4))
         self._check(_lib.morea_eval_full(self.h, P, _ptr(offsets), _ptr(obj), _ptr(acc),
                                          _ptr(tet_cache)))
         return obj, acc, tet_cache
@@ -190,19 +221,35 @@ class Context:
         go = _np(grp_off, np.int32)
         ch = _np(changed, np.int32)
         G = len(go) - 1
-        self._last_G = G
+        S = int(go[-1]) if G >= 0 else 0
+        _check(base_offsets, "base_offsets", "f4", (P, self.N, 6))
+        _check(base_acc, "base_acc", "i8", (P, 6))
+        _check(new_vals, "new_vals", "f4", (P, S, 6))
+        _check(tet_cache, "tet_cache", "f8", (P, self.T, 4))
+        _check(obj, "obj", "f8", (P * G, 3))
+        _check(acc, "acc", "i8", (P * G, 6))
         self._check(_lib.morea_eval_partial(self.h, P, _ptr(base_offsets), _ptr(base_acc), G,
                                             _ptr(go), _ptr(ch), _ptr(new_vals), _ptr(tet_cache),
                                             _ptr(obj), _ptr(acc), _ptr(dep_cache_out)))
         return obj, acc, dep_cache_out
 
+    def prepare_partial(self, grp_off, changed):
+        """Build (or find) the cached dependent-tet plan of a partial request ahead of time."""
+        go = _np(grp_off, np.int32)
+        ch = _np(changed, np.int32)
+        self._check(_lib.morea_prepare_partial(self.h, len(go) - 1, _ptr(go), _ptr(ch)))
+
     def partial_deps(self):
-        n = _lib.morea_partial_deps(self.h, 0, None, None)
+        """Dependent tets (group order) and their group offsets of the last plan used."""
+        n = _lib.morea_partial_deps(self.h, 0, None, 0, None)
         if n < 0:
             self._check(n)
+        G = _lib.morea_partial_groups(self.h)
+        if G < 0:
+            self._check(G)
         tets = np.zeros(max(n, 1), np.int32)
-        off = np.zeros(self._last_G + 1, np.int32)
-        _lib.morea_partial_deps(self.h, n, _ptr(tets), _ptr(off))
+        off = np.zeros(G + 1, np.int32)
+        _lib.morea_partial_deps(self.h, n, _ptr(tets), G + 1, _ptr(off))
         return tets[:n], off
 
     def check_folds(self, offsets, fold_count=None, severity=None, tet_flags=None):
@@ -217,6 +264,14 @@ class Context:
         o = offsets_one if _is_torch(offsets_one) else _np(offsets_one, np.float32)
         self._check(_lib.morea_owner_map(self.h, _ptr(o), int(side), _ptr(owner)))
         return owner
+
+    def sample_map(self, offsets_one, side):
+        """Test hook: per-voxel h (fp32, NaN = not sampled) and exact fg (255 = not sampled)."""
+        h = np.empty(self.V, np.float32)
+        fg = np.empty(self.V, np.uint8)
+        o = offsets_one if _is_torch(offsets_one) else _np(offsets_one, np.float32)
+        self._check(_lib.morea_sample_map(self.h, _ptr(o), int(side), _ptr(h), _ptr(fg)))
+        return h, fg
 
     def distance_map(self, side, pair, out=None):
         if out is None:
@@ -295,12 +350,13 @@ class Context:
         self._check(_lib.morea_prof_enable(self.h, 1 if on else 0))
 
     def prof_read(self):
-        la, sa, ba, it = (ctypes.c_int64() for _ in range(4))
+        la, sa, ba, it, stp = (ctypes.c_int64() for _ in range(5))
         ms = ctypes.c_double()
         self._check(_lib.morea_prof_read(self.h, ctypes.byref(la), ctypes.byref(ms),
-                                         ctypes.byref(sa), ctypes.byref(ba), ctypes.byref(it)))
+                                         ctypes.byref(sa), ctypes.byref(ba), ctypes.byref(it),
+                                         ctypes.byref(stp)))
         return dict(launches=la.value, ms=ms.value, samples=sa.value, band_entries=ba.value,
-                    items=it.value)
+                    items=it.value, steps=stp.value)
 
 
 # ---------------------------------------------------------------------------- helpers

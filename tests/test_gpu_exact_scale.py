@@ -1,0 +1,143 @@
+"""Bit-exact ownership and the exact h case split at paper scale (run with -m gpu).
+
+north_star: "bit-exact ownership/fold results ... on all five configs".  The
+owner map of the evaluation's own rasterizer (morea_owner_map: k_sweep's
+per-lane rows, one solution) is compared voxel by voxel with the oracle's
+per-voxel bbox loop (O3, App. A.2) at C3, C4 and one C5
+shard, on the identity, a solution with alpha ~ 1 (k = P - 1) and a forced fold
+(k = 7 mod 16).  The per-sample h-case decision fg (O6, eq. L316-323) of one
+full C4 solution comes from the evaluation kernel itself (morea_sample_map, a
+dump instantiation of k_sweep) and must agree with the oracle's exact int128
+decision on every voxel of both sides.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+if not torch.cuda.is_available():  # collected on CPU boxes, skipped there
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from oracle.oracle import Oracle  # noqa: E402
+from paper_2303_04873_b200 import morea  # noqa: E402
+from paper_2303_04873_b200.distributed import shard_bounds  # noqa: E402
+from synth import fos_plan, partial_request  # noqa: E402
+from tests.test_gpu_parity import _ctx  # noqa: E402
+
+
+def _sols(P, base=0):
+    fold = base + 7 + 16 * ((P // 2) // 16)  # k = 7 mod 16: a vertex pushed across a face
+    return [base, base + P - 1, fold]
+
+
+@pytest.mark.parametrize("idx", [3, 4])
+def test_owner_maps_bitexact_paper_scale(wl, idx):
+    w = wl(idx)
+    ctx = _ctx(w)
+    orc = Oracle.from_workload(w)
+    folded = 0
+    for k in _sols(w.P):
+        folded += orc.check_folds(w.offsets[k])[0] > 0
+        for side in (0, 1):
+            g = ctx.owner_map(w.offsets[k], side)
+            o = orc.owner_map(w.offsets[k], side)
+            bad = int((g != o).sum())
+            assert bad == 0, (w.name, k, side, bad)
+    assert folded >= 1  # the fold case is really folded (-2 / -1 entries compared too)
+    ctx.close()
+
+
+def test_owner_maps_bitexact_c5_shard(wl):
+    w = wl(5)
+    s0, s1 = shard_bounds(w.P, 8, 7)
+    ctx = _ctx(w)
+    orc = Oracle.from_workload(w)
+    for k in _sols(s1 - s0, s0):
+        for side in (0, 1):
+            g = ctx.owner_map(w.offsets[k], side)
+            o = orc.owner_map(w.offsets[k], side)
+            assert int((g != o).sum()) == 0, (k, side)
+    ctx.close()
+
+
+def test_sample_map_fg_exact_full_c4_solution(wl):
+    """Zero h-case disagreements over one full C4 solution (both sides, ~12.6 M samples)."""
+    w = wl(4)
+    ctx = _ctx(w)
+    orc = Oracle.from_workload(w)
+    k = 300
+    assert orc.check_folds(w.offsets[k])[0] == 0
+    for side in (0, 1):
+        gh, gfg = ctx.sample_map(w.offsets[k], side)
+        oh, ofg = orc.sample_map(w.offsets[k], side)
+        assert np.array_equal(gfg == 255, ofg == 255)  # the same sample set
+        s = ofg != 255
+        assert s.sum() == w.V
+        disagree = int((gfg[s] != ofg[s]).sum())
+        assert disagree == 0, (side, disagree)
+        # both cases of h (0/1 mismatch values, (a-b)^2) per sample: fp32 vs fp64 values
+        np.testing.assert_allclose(gh[s].astype(np.float64), oh[s], rtol=0, atol=2e-6)
+        mixed = ((oh[s] == 1.0) | (oh[s] == 0.0)).sum()
+        assert mixed > 0  # the mismatch branch is exercised
+    ctx.close()
+
+
+def test_mix_class_rejects_non_disjoint_groups(wl):
+    """morea_mix_class needs one colour class (disjoint dependent tets)."""
+    w = wl(2)
+    ctx = _ctx(w)
+    plan = fos_plan(w.tets, w.N)
+    go, ch, nv = partial_request(w, plan, "class", 0)
+    # second group = the first group again: overlapping points and dependent tets
+    ch2 = np.concatenate([ch[go[0]:go[1]], ch[go[0]:go[1]]]).astype(np.int32)
+    go2 = np.array([0, go[1] - go[0], 2 * (go[1] - go[0])], np.int32)
+    dev = torch.device("cuda:0")
+    P = w.P
+    off = torch.from_numpy(w.offsets).to(dev)
+    obj = torch.empty((P, 3), dtype=torch.float64, device=dev)
+    acc = torch.empty((P, 6), dtype=torch.int64, device=dev)
+    tc = torch.empty((P, w.T, 4), dtype=torch.float64, device=dev)
+    ctx.eval_full(off, obj, acc, tc)
+    d = 6 * (go[1] - go[0])
+    mu = torch.zeros(2 * d, dtype=torch.float64, device=dev)
+    L = torch.zeros(2 * d * d, dtype=torch.float64, device=dev)
+    cl = torch.zeros(P, dtype=torch.int32, device=dev)
+    with pytest.raises(morea.MoreaError) as e:
+        ctx.mix_class(off, acc, obj, tc, go2, ch2, cl, mu, L)
+    assert e.value.code == -1
+    ctx.close()
+
+
+def test_plan_cache_every_colour_class(wl):
+    """A generation-shaped sequence (every colour class in turn, twice): cached plans give
+    bitwise-equal results, partial_deps follows the last call, prepare_partial pre-builds."""
+    w = wl(2)
+    ctx = _ctx(w)
+    plan = fos_plan(w.tets, w.N)
+    dev = torch.device("cuda:0")
+    P = w.P
+    off = torch.from_numpy(w.offsets).to(dev)
+    obj = torch.empty((P, 3), dtype=torch.float64, device=dev)
+    acc = torch.empty((P, 6), dtype=torch.int64, device=dev)
+    tc = torch.empty((P, w.T, 4), dtype=torch.float64, device=dev)
+    ctx.eval_full(off, obj, acc, tc)
+    reqs = [partial_request(w, plan, "class", c) for c in range(len(plan["classes"]))]
+    assert len(reqs) >= 2
+    for go, ch, _ in reqs:
+        ctx.prepare_partial(go, ch)
+    first = []
+    for rep in range(2):
+        for i, (go, ch, nv) in enumerate(reqs):
+            G = len(go) - 1
+            po = torch.empty((P * G, 3), dtype=torch.float64, device=dev)
+            pa = torch.empty((P * G, 6), dtype=torch.int64, device=dev)
+            ctx.eval_partial(off, acc, go, ch, torch.from_numpy(nv).to(dev), tc, po, pa)
+            r = (po.cpu().numpy().copy(), pa.cpu().numpy().copy())
+            deps, dep_off = ctx.partial_deps()
+            assert len(dep_off) == G + 1 and dep_off[-1] == len(deps)
+            if rep == 0:
+                first.append(r)
+            else:
+                assert np.array_equal(r[0], first[i][0]) and np.array_equal(r[1], first[i][1])
+    ctx.close()

@@ -740,3 +740,24 @@ def test_coverage_flag_detects_gaps_and_overlaps():
     fold[j, :3] = (2 * c - base[j]) - base[j]
     _, acc = orc.eval(fold)
     assert acc.folds > 0 and acc.flags & O.F_COVERAGE
+
+
+def test_sample_map_accessor_sums_to_h_sum(wl):
+    """The test accessor orc_sample_map (per-voxel h, fg) re-states orc_eval's samples: on C2
+    the per-voxel h of both sides sum to acc.h_sum, every voxel is sampled once per side
+    (unfolded, hull at the image extent), and h follows the case rules of L318-322."""
+    w = wl(2)
+    orc = O.Oracle.from_workload(w)
+    k = 5
+    _, acc = orc.eval(w.offsets[k])
+    tot = 0.0
+    for side in (0, 1):
+        h, fg = orc.sample_map(w.offsets[k], side)
+        assert (fg != 255).all() and not np.isnan(h).any()
+        tot += h.sum()
+        a = (w.I_s if side == 0 else w.I_t).ravel()
+        # the case rules of L318-322: both background -> 0, exactly one background -> 1
+        assert (h[(a == 0) & (fg == 0)] == 0.0).all()
+        assert (h[(a == 0) != (fg == 0)] == 1.0).all()
+        assert ((a == 0) != (fg == 0)).sum() > 0
+    assert tot == pytest.approx(acc.h_sum, rel=1e-12)
