@@ -414,7 +414,7 @@ def main():
     peak, peak_src = measured_hbm_peak()
 
     def prof_run(fn, reps=3):
-        """k_sweep algorithmic GB/s of fn from the kernel's own counters and CUDA events."""
+        """k_raster algorithmic GB/s of fn from the kernel's own counters and CUDA events."""
         fn()
         torch.cuda.synchronize()
         ctx.prof_enable(True)
@@ -435,7 +435,7 @@ def main():
                                                           pacc_d[c]))
         t_c, sp_c, gbs_c = prof_run(run)
         per_class.append({"class": c, "groups": Gs[c], "evals_per_s": P * Gs[c] * 1e3 / t_c, "ms": t_c,
-                          "k_sweep_frac": (gbs_c / peak) if gbs_c else None})
+                          "k_raster_frac": (gbs_c / peak) if gbs_c else None})
     t_part_nc = timed(lambda: ctx.eval_partial(off_d, acc_d, classes[0][0], classes[0][1], nv_d[0], None,
                                                pobj_d[0], pacc_d[0]))
     # partial-evaluation sweep over FOS sizes: 1 edge, 4 and 16 edges of
@@ -452,7 +452,7 @@ def main():
         t_k, sp, gbs = prof_run(run)
         sweep[kind] = {"groups": sG, "points_per_group": round(len(sch) / sG, 2),
                        "evals_per_s": P * sG * 1e3 / t_k, "ms": t_k,
-                       "k_sweep_gbs": gbs, "k_sweep_frac": (gbs / peak) if gbs else None,
+                       "k_raster_gbs": gbs, "k_raster_frac": (gbs / peak) if gbs else None,
                        "samples_per_eval": sp["samples"] / max(sp["launches"], 1) / (P * sG)}
     t_sobol = t_repair = t_mix = t_plain = float("nan")
     mix_accept_frac = float("nan")
@@ -508,12 +508,12 @@ def main():
         ctx_plain.close()
         ctx.eval_full(off_d, obj_d, acc_d, cache_d)
 
-    # ---- roofline of the dominant kernel (k_sweep), SURVEY.md §8(d) algorithmic bytes
+    # ---- roofline of the dominant kernel (k_raster), SURVEY.md §8(d) algorithmic bytes
     alg_bytes = 8 * prof["samples"] + 12 * prof["band_entries"] + 32 * prof["items"]
     achieved = alg_bytes / (prof["ms"] / 1e3) / 1e9 if prof["ms"] > 0 else None
     per_launch_bytes = alg_bytes / max(prof["launches"], 1)
     ncu = ncu_summary()
-    traffic = ncu.get("k_sweep_dram_bytes_per_launch")
+    traffic = ncu.get("k_raster_dram_bytes_per_launch")
 
     # ---- e2e: the same step through the public API, inputs copied from pinned host memory
     # and the results read back to pinned host memory inside the timed region
@@ -526,20 +526,20 @@ def main():
     cnt_h = torch.empty(P, dtype=torch.int32).pin_memory()
     sev_h = torch.empty(P, dtype=torch.float64).pin_memory()
 
+    # (copies on torch's default stream: the legacy default stream orders them
+    # against the context stream, which is a blocking stream, both ways)
     def step_e2e():
-        with torch.cuda.stream(stream):
-            off_d.copy_(off_h, non_blocking=True)
-            for c in range(n_cls):
-                nv_d[c].copy_(nv_h[c], non_blocking=True)
+        off_d.copy_(off_h, non_blocking=True)
+        for c in range(n_cls):
+            nv_d[c].copy_(nv_h[c], non_blocking=True)
         step()
-        with torch.cuda.stream(stream):
-            obj_h.copy_(obj_d, non_blocking=True)
-            acc_h.copy_(acc_d, non_blocking=True)
-            for c in range(n_cls):
-                pobj_h[c].copy_(pobj_d[c], non_blocking=True)
-                pacc_h[c].copy_(pacc_d[c], non_blocking=True)
-            cnt_h.copy_(cnt_d, non_blocking=True)
-            sev_h.copy_(sev_d, non_blocking=True)
+        obj_h.copy_(obj_d, non_blocking=True)
+        acc_h.copy_(acc_d, non_blocking=True)
+        for c in range(n_cls):
+            pobj_h[c].copy_(pobj_d[c], non_blocking=True)
+            pacc_h[c].copy_(pacc_d[c], non_blocking=True)
+        cnt_h.copy_(cnt_d, non_blocking=True)
+        sev_h.copy_(sev_d, non_blocking=True)
         torch.cuda.synchronize()
 
     for _ in range(2):
@@ -585,14 +585,14 @@ def main():
             "config": workload_config(P_total, G_tot, n_cls, world, T, backend),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
-                         "traffic": traffic, "kernel": "k_sweep",
+                         "traffic": traffic, "kernel": "k_raster",
                          "frac_full_launch": (gbs_full / peak) if gbs_full else None,
                          "frac_partial_launches": (gbs_parts / peak) if gbs_parts else None,
                          "algorithmic_bytes_per_launch": per_launch_bytes, "peak_source": peak_src,
                          "launches": prof["launches"], "kernel_ms": prof["ms"],
-                         "ncu": {"source": ncu.get("source"), "l2_hit_pct": ncu.get("k_sweep_l2_hit_pct"),
-                                 "l1tex_hit_pct": ncu.get("k_sweep_l1tex_hit_pct"),
-                                 "issue_active_pct": ncu.get("k_sweep_issue_active_pct")}},
+                         "ncu": {"source": ncu.get("source"), "l2_hit_pct": ncu.get("k_raster_l2_hit_pct"),
+                                 "l1tex_hit_pct": ncu.get("k_raster_l1tex_hit_pct"),
+                                 "issue_active_pct": ncu.get("k_raster_issue_active_pct")}},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
@@ -603,7 +603,6 @@ def main():
                 "partial_evals_per_s_all_classes": part_rate / world, "partial_ms_all_classes": t_parts,
                 "partial_per_class": per_class,
                 "partial_class0_nocache_evals_per_s": P * Gs[0] * 1e3 / t_part_nc,
-                "k_sweep_lane_steps_per_sample": (32.0 * prof["steps"] / prof["samples"]) if prof["samples"] else None,
                 "sobol_full_evals_per_s": _fin(P * 1e3 / t_sobol),
                 "sobol_full_ms": _fin(t_sobol),
                 "repair_population_ms": _fin(t_repair),
@@ -626,4 +625,9 @@ def main():
 
 
 if __name__ == "__main__":
-    sys.exit(main())
+    rc = main()
+    # leave without the interpreter's teardown of CUDA-owning objects (torch tensors
+    # freed after the context stream is gone); everything is flushed and finished here
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os._exit(rc)

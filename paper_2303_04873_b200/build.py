@@ -10,6 +10,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libmorea.so")
+# the same sources with device-side index and invariant checks (MOREA_CHECK -> assert);
+# used by tests/test_gpu_debug_checks.py only
+LIB_DEBUG = os.path.join(PKG, "libmorea_debug.so")
 SOURCES = ["morea_kernels.cu", "morea_api.cu"]
 HEADERS = [os.path.join(CSRC, h) for h in ("morea_internal.h", "morea_sobol_setup.cuh", "morea_sobol.cuh", "morea_repair.cuh", "morea_export.cuh", "morea_mix.cuh")] + \
     [os.path.join(INCLUDE, "morea.h")]
@@ -41,20 +44,24 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     lib = out or LIB
     if not force and out is None and not _stale():
         return LIB
-    objs = []
-    for s in SOURCES:
+    tag = "" if out is None else ".alt"
+    objs, procs = [], []
+    for s in SOURCES:  # the translation units compile in parallel
         src = os.path.join(CSRC, s)
-        obj = os.path.join(CSRC, s.replace(".cu", ".o") if out is None else s.replace(".cu", ".alt.o"))
+        obj = os.path.join(CSRC, s.replace(".cu", tag + ".o"))
         cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
+        procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+        objs.append(obj)
+    for s, p in procs:
+        so, se = p.communicate()
+        if p.returncode != 0:
+            sys.stderr.write(so + se)
             raise RuntimeError(f"nvcc failed on {s}")
         if verbose:
-            sys.stderr.write(r.stderr)
-        with open(os.path.join(CSRC, s + ".ptxas.txt"), "w") as f:
-            f.write(r.stderr)
-        objs.append(obj)
+            sys.stderr.write(se)
+        if out is None:
+            with open(os.path.join(CSRC, s + ".ptxas.txt"), "w") as f:
+                f.write(se)
     tmp = lib + ".tmp"
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
            "-Xcompiler", "-fPIC"]
@@ -64,6 +71,14 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         raise RuntimeError("nvcc link failed")
     os.replace(tmp, lib)
     return lib
+
+
+def build_debug(force: bool = False) -> str:
+    """libmorea_debug.so: the product sources with -DMOREA_DEBUG_CHECKS."""
+    if not force and os.path.exists(LIB_DEBUG) and os.path.getmtime(LIB_DEBUG) >= max(
+            os.path.getmtime(d) for d in [os.path.join(CSRC, x) for x in SOURCES] + HEADERS):
+        return LIB_DEBUG
+    return build(force=True, out=LIB_DEBUG, defines=("MOREA_DEBUG_CHECKS",))
 
 
 if __name__ == "__main__":

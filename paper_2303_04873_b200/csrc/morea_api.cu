@@ -71,13 +71,13 @@ struct PinnedBuf {
 
 // The static structure of one evaluation request (O10): canonical entries
 // (dependent tets of each group, tets ascending within a group), their changed
-// vertex slots, the (solution-independent) queue order, and the z-slabs of
-// k_sweep.  Built on the host once per distinct FOS request, uploaded through
+// vertex slots and the (solution-independent) queue order.  Built on the host
+// once per distinct FOS request, uploaded through
 // pinned memory (no synchronisation), and kept in a small LRU cache.
 struct Plan {
   std::vector<int32_t> key_off, key_pts;
   unsigned long long hash = 0, last_use = 0;
-  int G = 0, S = 0, n_entries = 0, n_slabs = 0;
+  int G = 0, S = 0, n_entries = 0;
   bool disjoint = true;  // dependent-tet sets pairwise disjoint (a colour class)
   std::vector<int32_t> dep_tets, dep_off;
   DevBuf dev;      // all device arrays below, one allocation
@@ -88,14 +88,8 @@ struct Plan {
   const int* group_off = nullptr;   // G + 1 offsets into the entries
   const int* grp_off = nullptr;     // G + 1 offsets into changed
   const int* changed = nullptr;     // S changed point ids
-  const int* slab_off = nullptr;    // entry -> first slab (n_entries + 1)
-  const int* slab_entry = nullptr;  // slab -> entry
-  const int2* slab_z = nullptr;     // slab -> [z_begin, z_end)
-  const int* slab_sched = nullptr;  // slabs, largest first
-  const int* id_off = nullptr;      // identity offsets (Sobol mode: one slab per entry)
 };
-constexpr int kPlanCache = 64;        // distinct FOS requests kept (one per colour class and size)
-constexpr double kSlabVoxels = 4096;  // k_sweep: base-mesh voxels per z-slab (and side) at most
+constexpr int kPlanCache = 64;  // distinct FOS requests kept (one per colour class and size)
 
 }  // namespace
 
@@ -112,7 +106,7 @@ struct morea_ctx {
   double sp[3] = {1, 1, 1};
   double r = 0;
   double w[2][kMaxPairs] = {};
-  DevBuf I[2], band[2], dmap[2], wts, own, band_runs;
+  DevBuf I[2], band[2], dmap[2], wts, own;
   // Sobol sampler (NEXT-1): mode, rate, dilated band masks (2 V bytes), direction numbers
   int sampler = MOREA_SAMPLER_VOXEL;
   double rate = 1.0;
@@ -138,20 +132,18 @@ struct morea_ctx {
   std::vector<double> tet_size;
   long long expect[2] = {-1, -1};  // base-mesh sample counts per side (coverage check)
   // scratch
-  DevBuf sgeom, scal, hgn, counter, stats, scratch;
+  DevBuf geom, sgeom, scal, hgn, counter, stats;
   DevBuf st_off, st_nv, st_cache_in, st_base_acc, st_obj, st_acc, st_cache_out, st_i32, st_f64,
       st_u8;
   std::unique_ptr<Plan> full;                 // all tets, one group (set_mesh)
   std::vector<std::unique_ptr<Plan>> plans;  // partial requests, LRU
   Plan* plan = nullptr;                      // the plan of the last partial / mixing call
   unsigned long long plan_clock = 0;
-  std::vector<long long> baseQ;              // base points in Q.10 (slab bounds)
   // profiling
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
   long long prof_launches = 0;
   long long kernels = 0;  // every kernel launch of this context
-  long long run_off_len = 0;  // band runs: ints of the row offsets (padded to 2) before the int2 runs
   bool host_in = false;   // the current call staged a host input
 };
 
@@ -307,8 +299,6 @@ Volumes volumes_of(const morea_ctx* c) {
     for (int i = 0; i < kMaxPairs; i++) v.wf[s][i] = c->r > 0 ? (float)(c->w[s][i] / c->r) : 0.f;
   v.rf = (float)c->r;
   v.rlo = (float)(c->r - (double)v.rf);
-  v.run_off = c->band_runs.p ? c->band_runs.as<int>() : nullptr;
-  v.runs = c->band_runs.p ? reinterpret_cast<const int2*>(c->band_runs.as<int>() + c->run_off_len) : nullptr;
   v.own[0] = c->own.as<uint2>();
   v.own[1] = v.own[0] ? v.own[0] + c->V : nullptr;
   v.use_tex = c->use_tex ? 1 : 0;
@@ -336,34 +326,11 @@ MeshDev mesh_of(const morea_ctx* c) {
 
 constexpr long long kMixMaxDimHost = 192;  // = kMixMaxDim (morea_mix.cuh)
 
-int sweep_grid(morea_ctx* ctx) {
-  return std::max(1, ctx->n_sm * (ctx->use_tex ? ctx->blocks_per_sm_tex : ctx->blocks_per_sm));
-}
-
-// Scratch for one evaluation: Scal per (version, entry, sol), HGN per (version,
-// slab, sol), SobolRec per (version, entry, sol, side) in Sobol mode, and one
-// WarpScratch per resident k_sweep warp.
-cudaError_t eval_scratch(morea_ctx* ctx, EvalArgs& a) {
-  const size_t items = (size_t)a.n_entries * a.P;
-  cudaError_t e = ctx->scal.ensure(std::max<size_t>(1, items * a.n_setup_versions) * sizeof(Scal));
-  if (e != cudaSuccess) return e;
-  e = ctx->hgn.ensure(std::max<size_t>(1, (size_t)a.n_slabs * a.P * a.n_raster_versions) * sizeof(HGN));
-  if (e != cudaSuccess) return e;
-  a.scal = ctx->scal.as<Scal>();
-  a.hgn = ctx->hgn.as<HGN>();
-  if (a.sampler == MOREA_SAMPLER_SOBOL) {
-    e = ctx->sgeom.ensure(std::max<size_t>(1, items * a.n_raster_versions * 2) * sizeof(SobolRec));
-    if (e != cudaSuccess) return e;
-    a.sgeom = ctx->sgeom.as<SobolRec>();
-  }
-  e = ctx->scratch.ensure((size_t)sweep_grid(ctx) * sweep_block_warps() * sizeof(WarpScratch));
-  if (e != cudaSuccess) return e;
-  a.scratch = ctx->scratch.as<WarpScratch>();
-  e = ctx->counter.ensure(sizeof(unsigned long long));
-  if (e != cudaSuccess) return e;
-  a.counter = ctx->counter.as<unsigned long long>();
-  a.stats = ctx->prof ? ctx->stats.as<unsigned long long>() : nullptr;
-  return cudaSuccess;
+int raster_grid(morea_ctx* ctx, long long n_items) {
+  long long g = (long long)ctx->n_sm * (ctx->use_tex ? ctx->blocks_per_sm_tex : ctx->blocks_per_sm);
+  const int bw = raster_block_warps();
+  long long need = (n_items + bw - 1) / bw;
+  return (int)std::max<long long>(1, std::min(g, need));
 }
 
 void set_sampler_args(const morea_ctx* ctx, EvalArgs& a) {
@@ -374,26 +341,43 @@ void set_sampler_args(const morea_ctx* ctx, EvalArgs& a) {
   a.sobol_force_exact = (fe && fe[0] && fe[0] != '0') ? 1 : 0;
 }
 
-// The plan's entries, queue order and slabs into the launch arguments.
+// Scratch for one evaluation: Scal per (version, entry, sol); SideRec (voxel
+// centres) or SobolRec per rastered (version, entry, sol, side); HGN per
+// rastered (version, entry, sol).
+cudaError_t eval_scratch(morea_ctx* ctx, EvalArgs& a) {
+  const size_t items = (size_t)a.n_entries * a.P;
+  cudaError_t e = ctx->scal.ensure(std::max<size_t>(1, items * a.n_setup_versions) * sizeof(Scal));
+  if (e != cudaSuccess) return e;
+  e = ctx->hgn.ensure(std::max<size_t>(1, items * a.n_raster_versions) * sizeof(HGN));
+  if (e != cudaSuccess) return e;
+  a.scal = ctx->scal.as<Scal>();
+  a.hgn = ctx->hgn.as<HGN>();
+  if (a.sampler == MOREA_SAMPLER_SOBOL) {
+    e = ctx->sgeom.ensure(std::max<size_t>(1, items * a.n_raster_versions * 2) * sizeof(SobolRec));
+    if (e != cudaSuccess) return e;
+    a.sgeom = ctx->sgeom.as<SobolRec>();
+  } else {
+    e = ctx->geom.ensure(std::max<size_t>(1, items * a.n_raster_versions * 2) * sizeof(SideRec));
+    if (e != cudaSuccess) return e;
+    a.geom = ctx->geom.as<SideRec>();
+  }
+  e = ctx->counter.ensure(sizeof(unsigned long long));
+  if (e != cudaSuccess) return e;
+  a.counter = ctx->counter.as<unsigned long long>();
+  a.stats = ctx->prof ? ctx->stats.as<unsigned long long>() : nullptr;
+  return cudaSuccess;
+}
+
+// The plan's entries and queue order into the launch arguments.
 void plan_args(const morea_ctx* ctx, const Plan& P, EvalArgs& a) {
   a.n_entries = P.n_entries;
   a.canon_tet = P.canon_tet;
   a.canon_slots = P.canon_slots;
   a.sched = P.sched;
   set_sampler_args(ctx, a);
-  if (a.sampler == MOREA_SAMPLER_SOBOL) {
-    a.n_slabs = P.n_entries;
-    a.slab_off = P.id_off;
-  } else {
-    a.n_slabs = P.n_slabs;
-    a.slab_off = P.slab_off;
-    a.slab_entry = P.slab_entry;
-    a.slab_z = P.slab_z;
-    a.slab_sched = P.slab_sched;
-  }
 }
 
-// k_setup -> k_sweep / k_sobol (the dominant kernel; bracketed by events when profiling).
+// k_setup -> k_raster / k_sobol (the dominant kernel; bracketed by events when profiling).
 cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
   cudaError_t e = eval_scratch(ctx, a);
   if (e != cudaSuccess) return e;
@@ -420,8 +404,8 @@ cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
     const long long need = (n_items + sobol_block_warps() - 1) / sobol_block_warps();
     e = launch_sobol(a, (int)std::max<long long>(1, std::min(g, need)), ctx->stream);
   } else {
-    NvtxScope r("k_sweep");
-    e = launch_sweep(a, sweep_grid(ctx), ctx->stream);
+    NvtxScope r("k_raster");
+    e = launch_raster(a, raster_grid(ctx, n_items), ctx->stream);
   }
   ctx->kernels++;
   if (ctx->prof) {
@@ -432,49 +416,10 @@ cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
   return e;
 }
 
-// Slabs of the entries (k_sweep items): the lattice z range of the base tet split
-// into ceil(volume / kSlabVoxels) parts; the outer slabs are open-ended, since a
-// solution's tet may reach past the base tet's range.
-void build_slabs(const morea_ctx* ctx, const std::vector<int>& ent_tet, std::vector<int>& slab_off,
-                 std::vector<int>& slab_entry, std::vector<int2>& slab_z, std::vector<int>& slab_sched) {
-  std::vector<double> est;
-  slab_off.assign(1, 0);
-  slab_entry.clear();
-  slab_z.clear();
-  for (size_t e = 0; e < ent_tet.size(); e++) {
-    const int t = ent_tet[e];
-    long long mn = 1LL << 40, mx = -(1LL << 40);
-    for (int k = 0; k < 4; k++) {
-      const long long q = ctx->baseQ[3 * ctx->h_tets[4 * t + k] + 2];
-      mn = std::min(mn, q);
-      mx = std::max(mx, q);
-    }
-    const long long zlo = std::max<long long>(-((-mn) >> 10), 0), zhi = std::min<long long>(mx >> 10, ctx->nz - 1);
-    const long long nsl = std::max<long long>(1, zhi - zlo + 1);
-    const double vol = ctx->tet_size[t] / (6.0 * 1073741824.0);
-    const long long k = std::max<long long>(1, std::min<long long>(nsl, (long long)std::ceil(vol / kSlabVoxels)));
-    for (long long j = 0; j < k; j++) {
-      const long long b0 = zlo + j * nsl / k, b1 = zlo + (j + 1) * nsl / k;
-      slab_z.push_back(make_int2(j == 0 ? INT32_MIN : (int)b0, j == k - 1 ? INT32_MAX : (int)b1));
-      slab_entry.push_back((int)e);
-      est.push_back(vol * (double)(b1 - b0) / (double)nsl);
-    }
-    slab_off.push_back((int)slab_z.size());
-  }
-  slab_sched.resize(est.size());
-  std::iota(slab_sched.begin(), slab_sched.end(), 0);
-  std::stable_sort(slab_sched.begin(), slab_sched.end(), [&](int a, int b) { return est[a] > est[b]; });
-}
-
 // Upload the plan's arrays in one allocation through pinned staging (no sync).
 cudaError_t upload_plan(morea_ctx* ctx, Plan& P, const std::vector<int>& ct, const std::vector<int4>& cs,
                         const std::vector<int>& sched, const std::vector<int>& group_off,
                         const std::vector<int>& off, const std::vector<int>& pts, bool identity) {
-  std::vector<int> slab_off, slab_entry, slab_sched, id_off(P.n_entries + 1);
-  std::vector<int2> slab_z;
-  build_slabs(ctx, ct, slab_off, slab_entry, slab_z, slab_sched);
-  std::iota(id_off.begin(), id_off.end(), 0);
-  P.n_slabs = (int)slab_z.size();
   struct Seg { const void* src; size_t bytes; size_t at; };
   std::vector<Seg> segs;
   size_t tot = 0;
@@ -490,11 +435,6 @@ cudaError_t upload_plan(morea_ctx* ctx, Plan& P, const std::vector<int>& ct, con
   const size_t i_go = add(group_off.data(), group_off.size() * sizeof(int));
   const size_t i_of = add(off.data(), off.size() * sizeof(int));
   const size_t i_pt = add(pts.data(), pts.size() * sizeof(int));
-  const size_t i_so = add(slab_off.data(), slab_off.size() * sizeof(int));
-  const size_t i_se = add(slab_entry.data(), slab_entry.size() * sizeof(int));
-  const size_t i_sz = add(slab_z.data(), slab_z.size() * sizeof(int2));
-  const size_t i_ss = add(slab_sched.data(), slab_sched.size() * sizeof(int));
-  const size_t i_id = add(id_off.data(), id_off.size() * sizeof(int));
   cudaError_t e = P.dev.ensure(tot);
   if (e != cudaSuccess) return e;
   e = P.host.ensure(tot);
@@ -510,11 +450,6 @@ cudaError_t upload_plan(morea_ctx* ctx, Plan& P, const std::vector<int>& ct, con
   P.group_off = (const int*)(d + segs[i_go].at);
   P.grp_off = (const int*)(d + segs[i_of].at);
   P.changed = (const int*)(d + segs[i_pt].at);
-  P.slab_off = (const int*)(d + segs[i_so].at);
-  P.slab_entry = (const int*)(d + segs[i_se].at);
-  P.slab_z = (const int2*)(d + segs[i_sz].at);
-  P.slab_sched = (const int*)(d + segs[i_ss].at);
-  P.id_off = (const int*)(d + segs[i_id].at);
   return cudaSuccess;
 }
 
@@ -758,8 +693,8 @@ int morea_create(int cuda_device, void* cuda_stream, morea_ctx** out) {
     ctx->own_stream = true;
   }
   cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, cuda_device);
-  ctx->blocks_per_sm = sweep_blocks_per_sm(false);
-  ctx->blocks_per_sm_tex = sweep_blocks_per_sm(true);
+  ctx->blocks_per_sm = raster_blocks_per_sm(false);
+  ctx->blocks_per_sm_tex = raster_blocks_per_sm(true);
   ctx->blocks_per_sm_sobol = sobol_blocks_per_sm(false);
   ctx->blocks_per_sm_sobol_tex = sobol_blocks_per_sm(true);
   {
@@ -790,12 +725,12 @@ void morea_destroy(morea_ctx* ctx) {
     cudaEventDestroy(p.second);
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
-                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->band_runs, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->st_masks, &ctx->st_counts, &ctx->st_dvf, &ctx->st_cov,
+                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->st_masks, &ctx->st_counts, &ctx->st_dvf, &ctx->st_cov,
                     &ctx->scratch_owner, &ctx->zero_off, &ctx->mx_off, &ctx->mx_acc,
                     &ctx->mx_obj, &ctx->mx_cache, &ctx->mx_nv, &ctx->mx_pobj, &ctx->mx_pacc, &ctx->mx_dep,
                     &ctx->mx_base, &ctx->mx_accepted, &ctx->mx_cluster, &ctx->mx_mu, &ctx->mx_L, &ctx->mx_arch,
                     &ctx->mx_moff, &ctx->mx_fixed, &ctx->base, &ctx->tets, &ctx->cdelta, &ctx->ref,
-                    &ctx->sgeom, &ctx->scal, &ctx->hgn, &ctx->scratch,
+                    &ctx->geom, &ctx->sgeom, &ctx->scal, &ctx->hgn,
                     &ctx->counter, &ctx->stats, &ctx->st_off, &ctx->st_nv, &ctx->st_cache_in,
                     &ctx->st_base_acc, &ctx->st_obj, &ctx->st_acc, &ctx->st_cache_out,
                     &ctx->st_i32, &ctx->st_f64, &ctx->st_u8};
@@ -887,40 +822,6 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
     for (int s = 0; s < 2; s++)
       for (int i = 0; i < kMaxPairs; i++) wf[s * kMaxPairs + i] = ctx->r > 0 ? (float)(ctx->w[s][i] / ctx->r) : 0.f;
     CK(cudaMemcpy((char*)ctx->wts.p + sizeof(ctx->w), wf.data(), wf.size() * sizeof(float), cudaMemcpyHostToDevice));
-  }
-  // band runs (a6): per side and image row (y, z), the maximal x-runs of voxels with
-  // band bits, so the guidance pass of a row visits only band voxels
-  {
-    const long long rows = (long long)ny * nz;
-    std::vector<int> off(2 * rows + 2, 0);
-    std::vector<int> runs;
-    std::vector<unsigned char> hb((size_t)V);
-    for (int s = 0; s < 2; s++) {
-      if (K > 0) {
-        CK(cudaMemcpy(hb.data(), ctx->band[s].p, (size_t)V, cudaMemcpyDeviceToHost));
-      } else {
-        std::fill(hb.begin(), hb.end(), 0);
-      }
-      for (long long rho = 0; rho < rows; rho++) {
-        off[s * rows + rho] = (int)(runs.size() / 2);
-        const unsigned char* b = hb.data() + rho * nx;
-        for (int x = 0; x < nx;) {
-          if (!b[x]) { x++; continue; }
-          int e = x;
-          while (e + 1 < nx && b[e + 1]) e++;
-          runs.push_back(x);
-          runs.push_back(e);
-          x = e + 1;
-        }
-      }
-    }
-    off[2 * rows] = (int)(runs.size() / 2);
-    ctx->run_off_len = (2 * rows + 2);
-    CK(ctx->band_runs.ensure((off.size() + std::max<size_t>(runs.size(), 2)) * sizeof(int)));
-    CK(cudaMemcpy(ctx->band_runs.p, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
-    if (!runs.empty())
-      CK(cudaMemcpy(ctx->band_runs.as<int>() + off.size(), runs.data(), runs.size() * sizeof(int),
-                    cudaMemcpyHostToDevice));
   }
   CK(ctx->own.ensure(2 * V * sizeof(uint2)));
   for (int s = 0; s < 2; s++)
@@ -1016,7 +917,6 @@ int morea_set_mesh(morea_ctx* ctx, int n_points, const float* base_xyz, int n_te
     CK(cudaMemcpyAsync(ctx->d_inc.p, inc.data(), inc.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
                        ctx->stream));
   ctx->tet_size = size;
-  ctx->baseQ = Q;
   std::vector<int> order(n_tets), all(n_tets);
   std::iota(order.begin(), order.end(), 0);
   std::iota(all.begin(), all.end(), 0);
@@ -1052,16 +952,11 @@ int morea_set_mesh(morea_ctx* ctx, int n_points, const float* base_xyz, int n_te
     a.offsets = zoff.as<float>();
     plan_args(ctx, *ctx->full, a);
     a.sampler = MOREA_SAMPLER_VOXEL;  // the coverage reference is always voxel centres
-    a.n_slabs = ctx->full->n_slabs;
-    a.slab_off = ctx->full->slab_off;
-    a.slab_entry = ctx->full->slab_entry;
-    a.slab_z = ctx->full->slab_z;
-    a.slab_sched = ctx->full->slab_sched;
     a.n_setup_versions = 1;
     a.n_raster_versions = 1;
     a.expect[0] = a.expect[1] = -1;
     CK(run_eval(ctx, a));
-    std::vector<HGN> hg(a.n_slabs);
+    std::vector<HGN> hg(n_tets);
     CK(cudaMemcpyAsync(hg.data(), ctx->hgn.p, hg.size() * sizeof(HGN), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     long long c0 = 0, c1 = 0;
@@ -1252,11 +1147,6 @@ static int export_args(morea_ctx* ctx, const float* offsets_one, EvalArgs& a) {
   a.offsets = off;
   plan_args(ctx, *ctx->full, a);
   a.sampler = MOREA_SAMPLER_VOXEL;  // the exports always use the voxel-centre sample set
-  a.n_slabs = ctx->full->n_slabs;
-  a.slab_off = ctx->full->slab_off;
-  a.slab_entry = ctx->full->slab_entry;
-  a.slab_z = ctx->full->slab_z;
-  a.slab_sched = ctx->full->slab_sched;
   a.n_setup_versions = 1;
   a.n_raster_versions = 1;
   a.expect[0] = a.expect[1] = -1;
@@ -1279,7 +1169,7 @@ int morea_label_counts(morea_ctx* ctx, const float* offsets_one, int side, const
   CK(in_dev(ctx, masks, (size_t)ctx->V, ctx->st_masks, (const void**)&m));
   OutView ov[1];
   CK(out_dev(counts, (size_t)ctx->T * (M + 1) * sizeof(int64_t), ctx->st_counts, ov[0]));
-  CK(launch_label_counts(a, sweep_grid(ctx), side, m, M, (long long*)ov[0].dev, ctx->stream));
+  CK(launch_label_counts(a, side, m, M, (long long*)ov[0].dev, ctx->stream));
   ctx->kernels += 2;
   CK(finish_outputs(ctx, ov, 1));
   return MOREA_OK;
@@ -1328,7 +1218,7 @@ int morea_dvf(morea_ctx* ctx, const float* offsets_one, int side, float* dvf, ui
   CK(out_dev(coverage, (size_t)ctx->V, ctx->st_cov, ov[1]));
   unsigned char* cov = ov[1].dev ? (unsigned char*)ov[1].dev : ctx->st_cov.as<unsigned char>();
   CK(ctx->scratch_owner.ensure((size_t)ctx->V * sizeof(int)));
-  CK(launch_dvf(a, sweep_grid(ctx), side, ctx->scratch_owner.as<int>(), (float*)ov[0].dev, cov, ctx->stream));
+  CK(launch_dvf(a, side, ctx->scratch_owner.as<int>(), (float*)ov[0].dev, cov, ctx->stream));
   ctx->kernels += 4;
   CK(finish_outputs(ctx, ov, 2));
   return MOREA_OK;
@@ -1496,17 +1386,12 @@ int morea_owner_map(morea_ctx* ctx, const float* offsets_one, int side, int32_t*
   a.offsets = off;
   plan_args(ctx, *ctx->full, a);
   a.sampler = MOREA_SAMPLER_VOXEL;
-  a.n_slabs = ctx->full->n_slabs;
-  a.slab_off = ctx->full->slab_off;
-  a.slab_entry = ctx->full->slab_entry;
-  a.slab_z = ctx->full->slab_z;
-  a.slab_sched = ctx->full->slab_sched;
   a.n_setup_versions = 1;
   a.n_raster_versions = 1;
   a.expect[0] = a.expect[1] = -1;
   CK(eval_scratch(ctx, a));
-  CK(launch_owner_map(a, sweep_grid(ctx), side, (int*)ov[0].dev, ctx->stream));
-  ctx->kernels += 2;
+  CK(launch_owner_map(a, side, (int*)ov[0].dev, ctx->stream));
+  ctx->kernels += 3;
   CK(finish_outputs(ctx, ov, 1));
   return MOREA_OK;
 }

@@ -7,31 +7,50 @@
 
 #include "morea.h"
 
+// Debug builds (-DMOREA_DEBUG_CHECKS, tests/test_gpu_debug_checks.py) check index
+// ranges and invariants on the device (assert traps); release builds compile the
+// checks away.  (compute-sanitizer is closed on the GPU pool this was built on.)
+#ifdef MOREA_DEBUG_CHECKS
+#undef NDEBUG
+#include <cassert>
+#define MOREA_CHECK(c) assert(c)
+#else
+#define MOREA_CHECK(c) ((void)0)
+#endif
+
 namespace morea {
 
 constexpr int kMaxPairs = 8;
-#ifndef MOREA_TEX_PAD
-#define MOREA_TEX_PAD 1  // edge-replicated border of the gather textures (voxels; 0 or 1)
-#endif
-constexpr int kTexPad = MOREA_TEX_PAD;
+constexpr int kTexPad = 1;  // edge-replicated border of the gather textures (voxels)
 constexpr int kQLo = -256 * 1024;  // Q.10 window (O1)
 constexpr int kQHi = 768 * 1024;
-// Voxel-centre sweep (k_sweep): one warp per (version, entry,
-// z-slab, group of 32 solutions), lane = solution.  Per (item, side) each lane
-// builds the fp32 fast view of its own tet side; the exact integer decisions of
-// the rare fallbacks are re-derived from the lane's Q.10 vertices (LaneQ).  The
-// per-slice fields live in the warp's global scratch slot as float4 fields
-// [field][lane] (coalesced), the per-row fields in shared memory, the per-sample
-// ones in registers.
-constexpr int kSliceF4 = 7;  // float4 per lane in the slice scratch (see morea_sweep.cuh)
-struct __align__(16) LaneQ {  // Q.10 vertices of both sides of one lane's tet
-  int q[2][4][3];
+constexpr int kWarpsPerBlock = 2;  // k_owner_map / export blocks (one WarpSmem per warp)
+constexpr int kRasterThreads = 32 * kWarpsPerBlock;
+
+// Geometry of one (version, entry, solution, side) item, written by k_setup and
+// read by k_raster.  384 bytes, 16-byte aligned.  The fp32 fields
+// are roundings of exact (or fp64) values; each comes with an error bound so the
+// rasterizer can detect when only the exact integer fields can decide.
+struct __align__(16) SideRec {
+  float4 face[4];             // (fa, fb, fc, thr): crossing x*(y,z) = fa + fb (y - lo_y) + fc (z - lo_z)
+                              // and the bound on its fp32 error (voxels)
+  int ftype[4];               // +-1: lower/upper bound face (n_x >< 0), 0: flat, +-2: exact search
+  long long nrm[4][3];        // exact inward normals (|n| < 2^41)
+  long long cst[4];           // e_k(q) = 1024 n_k . q - cst_k  (exact)
+  float A[3][3];              // displacement gradient du_a / dq_b
+  float d0[3];                // displacement at lo
+  float eps[3];               // fp32 position filter bound per axis (0 = exact axis)
+  int flags;                  // bit 0: rasterize; bit 1: every position of the bbox is inside
+                              // [0, n-1) with margin (no clamp needed); bit 2: every face is a
+                              // regular lower/upper face (fast row intervals); bit 3: every
+                              // position is inside (-1, n) with margin (no clamp needed on the
+                              // edge-padded gather textures)
+  float vy[4], vz[4];         // vertex y, z (voxel units, exact) for per-slice y ranges
+  int lo[3], hi[3];           // lattice bbox clipped to the image
+  int U[4][3];                // Q_other - Q_own per vertex
+  long long absdet;           // |Delta|
 };
-static_assert(sizeof(LaneQ) == 96, "LaneQ layout");
-struct __align__(16) WarpScratch {  // one warp slot of k_sweep
-  float4 slice[kSliceF4][32];
-  LaneQ Q[32];
-};
+static_assert(sizeof(SideRec) == 384, "SideRec layout");
 
 // NEXT-1 (Sobol sampler, DESIGN.md §3 S1-S9): what k_sobol needs of one (version,
 // entry, solution, side) item.  Written by k_setup into the item's SideRec slot.
@@ -59,8 +78,7 @@ struct Scal {
 };
 static_assert(sizeof(Scal) == 32, "Scal layout");
 
-// Sample sums of one (version, z-slab, solution), both sides (voxel-centre mode);
-// in Sobol mode every entry is one slab.
+// Sample sums of one (version, entry, solution), both sides.
 struct HGN {
   double h, g;
   long long n;   // samples (both sides)
@@ -77,10 +95,6 @@ struct Volumes {
   // per voxel (bits of I_side(q), band bits): one 8-byte load; one allocation,
   // own[1] = own[0] + V, so side s of voxel q is own[0][s V + q]
   const uint2* own[2];
-  // band runs: side s, image row rho = z ny + y: runs[run_off[s ny nz + rho] .. run_off[.. + 1])
-  // = inclusive x-ranges of voxels with band bits (the guidance pass of a row)
-  const int* run_off;
-  const int2* runs;
   const float* dmap[2];          // K * V fp32 per side
   int K;
   double r, inv_r;
@@ -119,12 +133,9 @@ struct MeshDev {
   int spoke_mode;
 };
 
-// One evaluation launch sequence: k_setup -> k_sweep (or k_sobol) -> k_reduce.
-// Version 0 = the new (evaluated) geometry, version 1 = the base geometry of a
-// stateless partial evaluation.  k_setup items: (version, canonical entry,
-// solution).  k_sweep items: (version, slab, group of 32 solutions); every
-// canonical entry is split into z-slabs (slab_off) so no single item dominates
-// a launch.  HGN index: (version * n_slabs + slab) * P + solution.
+// One evaluation launch sequence: k_setup -> k_raster -> k_reduce.
+// Item index space: (version, canonical entry, solution); version 0 = the new
+// (evaluated) geometry, version 1 = the base geometry of a partial evaluation.
 struct EvalArgs {
   Volumes vol;
   MeshDev mesh;
@@ -133,18 +144,14 @@ struct EvalArgs {
   int n_entries;
   const int* canon_tet;      // canonical entry -> tet (nullptr: identity, full evaluation)
   const int4* canon_slots;   // canonical entry -> per vertex slot into new_vals, or -1
-  const int* sched;          // queue position -> canonical entry (large tets first; k_setup, k_sobol)
-  int n_slabs;               // z-slabs over all entries (Sobol mode: = n_entries)
-  const int* slab_off;       // entry -> first slab (n_entries + 1)
-  const int* slab_entry;     // slab -> entry
-  const int2* slab_z;        // slab -> [z_begin, z_end) lattice slices
-  const int* slab_sched;     // queue position -> slab (large slabs first)
-  WarpScratch* scratch;      // k_sweep: one slot per resident warp
+  const int* sched;          // queue position -> canonical entry (large tets first)
+  const int* group_off;      // G + 1 offsets of the groups' canonical entries (k_reduce)
   const float* new_vals;     // P*S_total*6
   int S_total;
   int partial;
   int n_setup_versions;      // 1 (full) or 2 (partial)
   int n_raster_versions;     // 1, or 2 when a partial evaluation recomputes the base
+  SideRec* geom;             // voxel-centre mode: [version][entry][sol][side]
   SobolRec* sgeom;           // Sobol mode: [version][entry][sol][side]
   Scal* scal;                // [version][entry][sol]
   HGN* hgn;                  // [version][entry][sol]
@@ -154,7 +161,7 @@ struct EvalArgs {
   const unsigned* sobol_v;   // [4][32] Sobol direction numbers (device)
   int sobol_force_exact;     // test hook (env MOREA_SOBOL_FORCE_EXACT): every sample takes the fp64 path
   unsigned long long* counter;  // work queue head (zeroed before launch)
-  unsigned long long* stats;    // [samples, band entries, items, warp-steps]
+  unsigned long long* stats;    // [samples, band entries, items]
   float* dump_h;                // test hook morea_sample_map: per-voxel h and fg of side dump_side
   unsigned char* dump_fg;
   int dump_side;
@@ -170,18 +177,18 @@ cudaError_t launch_pad_volume(const float* src, int nx, int ny, int nz, int pad,
 cudaError_t launch_own_records(const float* I, const unsigned char* band, long long V, uint2* out,
                                cudaStream_t s);
 cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s);
-cudaError_t launch_sweep(const EvalArgs& a, int grid, cudaStream_t s);
-int sweep_blocks_per_sm(bool tex);
-int sweep_block_warps();
+cudaError_t launch_raster(const EvalArgs& a, int grid, cudaStream_t s);
+int raster_blocks_per_sm(bool tex);
+int raster_block_warps();
 cudaError_t launch_sobol(const EvalArgs& a, int grid, cudaStream_t s);
 int sobol_blocks_per_sm(bool tex);
 int sobol_block_warps();
 cudaError_t launch_repair(const MeshDev& m, const double sp[3], int P, long long sol_base, float* offsets,
                           const unsigned char* fixed, const int* inc_off, const int* inc,
                           unsigned long long seed, int* moved, int* aborted, cudaStream_t s);
-cudaError_t launch_label_counts(const EvalArgs& a, int grid, int side, const unsigned char* masks, int M,
+cudaError_t launch_label_counts(const EvalArgs& a, int side, const unsigned char* masks, int M,
                                 long long* counts, cudaStream_t s);
-cudaError_t launch_dvf(const EvalArgs& a, int grid, int side, int* owner, float* dvf, unsigned char* cov,
+cudaError_t launch_dvf(const EvalArgs& a, int side, int* owner, float* dvf, unsigned char* cov,
                        cudaStream_t s);
 // NEXT-3 sampling arguments (morea_mix.cuh)
 struct MixArgs {
@@ -215,7 +222,7 @@ cudaError_t launch_reduce(const EvalArgs& a, int G, const int* group_off, const 
                           const int* grp_off, double* obj, void* acc, cudaStream_t s);
 cudaError_t launch_check_folds(const MeshDev& m, const double sp[3], int P, const float* offsets,
                                int* count, double* sev, unsigned char* flags, cudaStream_t s);
+cudaError_t launch_owner_map(const EvalArgs& a, int side, int* owner, cudaStream_t s);
 cudaError_t launch_fill(float* h, unsigned char* fg, long long V, cudaStream_t s);
-cudaError_t launch_owner_map(const EvalArgs& a, int grid, int side, int* owner, cudaStream_t s);
 
 }  // namespace morea

@@ -3,25 +3,33 @@
 // Rows of SURVEY.md §8(a) and where they live:
 //   a0 load-time maps          k_distance_maps, k_band_mask, k_validate_volume
 //   a1 genotype decode          canon_q (fp64, exact Q.10 rounding)
-//   a2 per-tet geometry + fold  k_setup (folds, severity, magnitude per item);
-//                               build_lane in k_sweep (per-lane fast geometry)
+//   a2 per-tet geometry + fold  k_setup (build_side, folds, severity)
 //   a3 magnitude                k_setup (magnitude)
-//   a4 ownership rasterizer     k_sweep: per-lane exact row intervals (morea_sweep.cuh)
-//   a5 map + sample + h         k_sweep: eval_row (exact case split, exact_fg)
-//   a6 guidance term            k_sweep: eval_row (warp-uniform band bits, in place)
-//   a7 reductions               per-lane sums in k_sweep, fixed-order k_reduce
+//   a4 ownership rasterizer     k_raster: row_interval() + raster() (exact intervals)
+//   a5 map + sample + h         k_raster: Sample<>::sample (exact case split, exact_fg)
+//   a6 guidance term            k_raster: Sample<>::enqueue / entry (band bits, per-warp queue)
+//   a7 reductions               warp shuffles (fixed order), k_reduce
 //   a8 partial evaluation       version 0/1 items + k_reduce with base_acc
 //   a9 fold check               k_check_folds
 // The readings of the paper (O1..O13) are cited per function.
 //
-// Work decomposition (DESIGN.md §4.2).  k_setup: one thread per (version, tet,
-// solution) computes the per-tet scalar terms (folds, severity, magnitude).
-// k_sweep: one 28-warp block per SM pulls items (version, tet z-slab, group of
-// 32 solutions) from a global queue; lane l of a warp evaluates solution
-// 32 g + l, the warp walking the union of the lanes' lattice rows (see
-// morea_sweep.cuh).  Further sm_100a kernels: morea_sobol*.cuh (NEXT-1 Sobol
-// sampler), morea_repair.cuh (NEXT-2 fold repair), morea_mix.cuh (NEXT-3 optimal
-// mixing), morea_sweep.cuh exports (NEXT-4 object counts and DVF).
+// Work decomposition (DESIGN.md §5).  k_setup: one thread per (version, tet,
+// solution) computes the exact integer geometry of both sides (int64/int128)
+// and writes a 384-byte SideRec per side.  k_raster: one 28-warp block per SM
+// pulls chunks of up to 112 items from a global queue in solution-minor order
+// and its warps take them one at a time without a block barrier (BlockQueue)
+// (consecutive items = same tet, next solution, so the warps of an SM share
+// their texel and record footprints in L1; large tets first).  Inside an item
+// the 32 lanes compute the exact x-intervals of 32 bbox rows, prefix-sum their
+// lengths and sweep the flattened samples 32 at a time.  The other volume is
+// gathered with tld4 from edge-padded textures (the O5 clamp is needed only by
+// items whose other-side vertices leave (-1, n), a separate instantiation).
+// Hot paths carry no divergent branches: rare exact fallbacks sit behind
+// warp-uniform votes, shared-memory records are written with predicated
+// stores (DESIGN.md §4.4 lists what was measured and why).
+// Further sm_100a kernels: morea_sobol*.cuh (NEXT-1 Sobol sampler),
+// morea_repair.cuh (NEXT-2 fold repair), morea_mix.cuh (NEXT-3 optimal
+// mixing), morea_export.cuh (NEXT-4 object counts and DVF).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -29,16 +37,20 @@
 #include "morea.h"
 #include "morea_internal.h"
 
+#ifndef MOREA_SM_BLOCK
+#define MOREA_SM_BLOCK 28  // k_raster: one block of this many warps per SM
+#endif
+
 #ifndef MOREA_SOBOL_WARPS
 #define MOREA_SOBOL_WARPS 28  // k_sobol: warps of its one block per SM
 #endif
 
 #ifndef MOREA_CLAIM_CHUNK
-#define MOREA_CLAIM_CHUNK 112  // k_sweep, k_sobol: at most this many items per global claim of BlockQueue
+#define MOREA_CLAIM_CHUNK 112  // k_raster, k_sobol: at most this many items per global claim of BlockQueue
 #endif
 
 #ifndef MOREA_CLAIM_SPREAD
-#define MOREA_CLAIM_SPREAD 16  // k_sweep, k_sobol: at least this many claims per block per launch where possible
+#define MOREA_CLAIM_SPREAD 16  // k_raster, k_sobol: at least this many claims per block per launch where possible
 #endif
 
 namespace morea {
@@ -78,6 +90,7 @@ __device__ __forceinline__ bool load_tet(const EvalArgs& A, int sol, int4 tv, in
 #pragma unroll
   for (int k = 0; k < 4; k++) {
     const int j = vid[k];
+    MOREA_CHECK(j >= 0 && j < A.mesh.N && sl[k] < A.S_total && sol >= 0 && sol < A.P);
     const float* o = sl[k] >= 0 ? A.new_vals + ((long long)sol * A.S_total + sl[k]) * 6
                                 : A.offsets + ((long long)sol * A.mesh.N + j) * 6;
 #pragma unroll
@@ -92,6 +105,121 @@ __device__ __forceinline__ bool load_tet(const EvalArgs& A, int sol, int4 tv, in
     }
   }
   return ok;
+}
+
+// ---------------------------------------------------------------------------
+// a2: exact geometry of one side (O2, O3, O4).  |Q| < 2^19.6 so edge components
+// < 2^20, normals < 2^41, |Delta| < 2^62.6, e_k(q) < 3 2^61.
+// ---------------------------------------------------------------------------
+__device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny, int nz,
+                           SideRec& G) {
+  G.flags = 0;
+  const i64 det = det3(Q);
+  if (det == 0) return;  // degenerate: owns nothing (O3)
+  G.absdet = det < 0 ? -det : det;
+  const int dims[3] = {nx, ny, nz};
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    const int mn = min(min(Q[0][a], Q[1][a]), min(Q[2][a], Q[3][a]));
+    const int mx = max(max(Q[0][a], Q[1][a]), max(Q[2][a], Q[3][a]));
+    G.lo[a] = max(ceildiv1024(mn), 0);
+    G.hi[a] = min(floordiv1024(mx), dims[a] - 1);
+    if (G.lo[a] > G.hi[a]) return;  // no lattice point of the image inside
+  }
+  const double Ly = (double)(G.hi[1] - G.lo[1]), Lz = (double)(G.hi[2] - G.lo[2]);
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    G.vy[k] = (float)Q[k][1] * (1.0f / 1024.0f);  // exact: |Q| < 2^20
+    G.vz[k] = (float)Q[k][2] * (1.0f / 1024.0f);
+    const int f0 = (k == 0) ? 1 : 0;
+    const int f1 = (k <= 1) ? 2 : 1;
+    const int f2 = (k <= 2) ? 3 : 2;
+    const i64 u0 = Q[f1][0] - Q[f0][0], u1 = Q[f1][1] - Q[f0][1], u2 = Q[f1][2] - Q[f0][2];
+    const i64 v0 = Q[f2][0] - Q[f0][0], v1 = Q[f2][1] - Q[f0][1], v2 = Q[f2][2] - Q[f0][2];
+    i64 n0 = u1 * v2 - u2 * v1, n1 = u2 * v0 - u0 * v2, n2 = u0 * v1 - u1 * v0;
+    const i64 s = n0 * (Q[k][0] - Q[f0][0]) + n1 * (Q[k][1] - Q[f0][1]) + n2 * (Q[k][2] - Q[f0][2]);
+    if (s < 0) { n0 = -n0; n1 = -n1; n2 = -n2; }  // inward: towards vertex k
+    G.nrm[k][0] = n0; G.nrm[k][1] = n1; G.nrm[k][2] = n2;
+    G.cst[k] = n0 * (i64)Q[f0][0] + n1 * (i64)Q[f0][1] + n2 * (i64)Q[f0][2];
+#pragma unroll
+    for (int a = 0; a < 3; a++) G.U[k][a] = Qo[k][a] - Q[k][a];
+    // row crossing x*(y, z): 1024 (n0 x + n1 y + n2 z) = cst, evaluated in fp32 per row
+    if (n0 != 0) {
+      const i128 num = (i128)G.cst[k] - (i128)1024 * ((i128)n1 * G.lo[1] + (i128)n2 * G.lo[2]);
+      const double fa = (double)num / (1024.0 * (double)n0);
+      const double fb = -(double)n1 / (double)n0, fc = -(double)n2 / (double)n0;
+      G.face[k].x = (float)fa;
+      G.face[k].y = (float)fb;
+      G.face[k].z = (float)fc;
+      // fp32 rounding of 3 coefficients + 2 fma: < 2^-22 (|fa| + |fb| Ly + |fc| Lz); 4x margin
+      const double thr = ldexp(fabs(fa) + fabs(fb) * Ly + fabs(fc) * Lz + 1.0, -20);
+      G.face[k].w = (float)thr;
+      G.ftype[k] = (n0 > 0 ? 1 : -1) * (thr >= 0.25 ? 2 : 1);
+    } else {
+      G.ftype[k] = 0;
+      G.face[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  // O4: displacement u(p) = sum_k lambda_k(p) U_k / 1024, lambda_k = e_k / |Delta|.
+  // Gradient du_a/dp_b = sum_k n_kb U_ka / |Delta|; value at lo from exact e_k(lo).
+  const double inv_det = 1.0 / (double)G.absdet;
+  const double L[3] = {(double)(G.hi[0] - G.lo[0]), Ly, Lz};
+  i64 elo[4];
+#pragma unroll
+  for (int k = 0; k < 4; k++)
+    elo[k] = 1024 * (G.nrm[k][0] * G.lo[0] + G.nrm[k][1] * G.lo[1] + G.nrm[k][2] * G.lo[2]) - G.cst[k];
+  bool inside = true;   // positions in [0, n-1) (plain-load path needs no clamp)
+  bool inside_p = true; // positions in (-1, n) (edge-padded textures need no clamp)
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    bool exact = true;
+    double Aab[3];
+#pragma unroll
+    for (int b = 0; b < 3; b++) {
+      i128 num = 0;
+#pragma unroll
+      for (int k = 0; k < 4; k++) num += (i128)G.nrm[k][b] * (i128)G.U[k][a];
+      if (num != 0) exact = false;
+      Aab[b] = (double)num * inv_det;
+      G.A[a][b] = (float)Aab[b];
+    }
+    if (exact) {
+      // every vertex moves by the same U_a: x_a = q_a + U_a / 1024 exactly (fp32-exact)
+      G.d0[a] = (float)G.U[0][a] * (1.0f / 1024.0f);
+      G.eps[a] = 0.0f;
+    } else {
+      i128 N = 0;
+#pragma unroll
+      for (int k = 0; k < 4; k++) N += (i128)elo[k] * (i128)G.U[k][a];
+      const double d0 = (double)N / (1024.0 * (double)G.absdet);
+      G.d0[a] = (float)d0;
+      double amax = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        const double v = d0 + Aab[0] * ((c & 1) ? L[0] : 0.0) + Aab[1] * ((c & 2) ? L[1] : 0.0) +
+                         Aab[2] * ((c & 4) ? L[2] : 0.0);
+        amax = fmax(amax, fabs(v));
+      }
+      // fp32 error of d = fma(A_x0, k, d_row(fp32 fma chain)) and of frac(d):
+      // <= 2^-24 (5 (|u|max + sum_b |A_ab| L_b) + 1); eps = 3x that
+      const double bound = amax + fabs(Aab[0]) * L[0] + fabs(Aab[1]) * L[1] + fabs(Aab[2]) * L[2] + 1.0;
+      G.eps[a] = (float)ldexp(bound, -19);
+    }
+    // An owned sample q lies in the closed tet, so its exact position x = T(q)
+    // (a convex combination of the other side's vertices) lies in the other
+    // side's vertex bbox.  The margin covers the fp32 position error, so floor()
+    // of the fp32 position stays in range.
+    const int omn = min(min(Qo[0][a], Qo[1][a]), min(Qo[2][a], Qo[3][a]));
+    const int omx = max(max(Qo[0][a], Qo[1][a]), max(Qo[2][a], Qo[3][a]));
+    const double xmin = (double)omn / 1024.0, xmax = (double)omx / 1024.0;
+    const double mg = 1e-3 + 2.0 * (double)G.eps[a];
+    if (!(xmin >= mg && xmax <= (double)(dims[a] - 1) - mg)) inside = false;
+    if (!(xmin >= -1.0 + mg && xmax <= (double)dims[a] - mg)) inside_p = false;
+  }
+  bool regular = true;
+#pragma unroll
+  for (int k = 0; k < 4; k++) regular = regular && (G.ftype[k] == 1 || G.ftype[k] == -1);
+  G.flags = 1 | (inside ? 2 : 0) | (regular ? 4 : 0) | (inside_p ? 8 : 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -143,9 +271,7 @@ __device__ double magnitude(const int Q[2][4][3], double c, const double sp2[3],
 #include "morea_sobol_setup.cuh"
 
 // ---------------------------------------------------------------------------
-// k_setup: one thread per (version, canonical entry, solution): the per-tet
-// scalar terms (folds, severity, magnitude, domain flag); in Sobol mode also the
-// SobolRec of each side.  (The voxel-centre sweep builds its geometry per lane.)
+// k_setup: one thread per (version, canonical entry, solution).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_setup(const EvalArgs A) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -163,13 +289,18 @@ __global__ void __launch_bounds__(128) k_setup(const EvalArgs A) {
   sc.m = sc.sev = 0.0;
   sc.folds = sc.flags = 0;
   sc.pad[0] = sc.pad[1] = 0;
-  const bool sobol = A.sampler == 1 && v < A.n_raster_versions;
+  const bool raster = v < A.n_raster_versions;
   if (!load_tet(A, sol, A.mesh.tets[tet], slots, Q)) {
     sc.flags = 1;  // domain: the tet contributes nothing
     A.scal[i] = sc;
-    if (sobol) {
-      A.sgeom[2 * i].flags = 0;
-      A.sgeom[2 * i + 1].flags = 0;
+    if (raster) {
+      if (A.sampler == 1) {
+        A.sgeom[2 * i].flags = 0;
+        A.sgeom[2 * i + 1].flags = 0;
+      } else {
+        A.geom[2 * i].flags = 0;
+        A.geom[2 * i + 1].flags = 0;
+      }
     }
     return;
   }
@@ -187,22 +318,31 @@ __global__ void __launch_bounds__(128) k_setup(const EvalArgs A) {
       sc.sev += vol * V.sp[0] * V.sp[1] * V.sp[2];
     }
   }
-  if (!sobol) {
+  if (!raster) {
     A.scal[i] = sc;
     return;
   }
 #pragma unroll 1
   for (int s = 0; s < 2; s++) {
-    SobolRec G;
-    build_sobol(Q[s], Q[1 - s], V, A.rate, G);
-    if (G.N > 0x7fffffffLL) {  // beyond the 32-bit point counter: flagged like a domain
-      sc.flags = 1;            // error (objectives NaN), the side contributes nothing
-      G.flags = 0;
-    }
-    const int4* src = reinterpret_cast<const int4*>(&G);
-    int4* dst = reinterpret_cast<int4*>(&A.sgeom[2 * i + s]);
+    if (A.sampler == 1) {
+      SobolRec G;
+      build_sobol(Q[s], Q[1 - s], V, A.rate, G);
+      if (G.N > 0x7fffffffLL) {  // beyond the 32-bit point counter: flagged like a domain
+        sc.flags = 1;            // error (objectives NaN), the side contributes nothing
+        G.flags = 0;
+      }
+      const int4* src = reinterpret_cast<const int4*>(&G);
+      int4* dst = reinterpret_cast<int4*>(&A.sgeom[2 * i + s]);
 #pragma unroll
-    for (int t = 0; t < (int)(sizeof(SobolRec) / 16); t++) dst[t] = src[t];
+      for (int t = 0; t < (int)(sizeof(SobolRec) / 16); t++) dst[t] = src[t];
+    } else {
+      SideRec G;
+      build_side(Q[s], Q[1 - s], V.nx, V.ny, V.nz, G);
+      const int4* src = reinterpret_cast<const int4*>(&G);
+      int4* dst = reinterpret_cast<int4*>(&A.geom[2 * i + s]);
+#pragma unroll
+      for (int t = 0; t < (int)(sizeof(SideRec) / 16); t++) dst[t] = src[t];
+    }
   }
   A.scal[i] = sc;
 }
@@ -213,6 +353,610 @@ cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s) {
   k_setup<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(a);
   return cudaGetLastError();
 }
+
+// ---------------------------------------------------------------------------
+// a4: exact x-interval of owned lattice points on row (y, z) (O3).  Face k owns
+// q iff e_k(q) > 0, or e_k = 0 and lexpos(n_k) (perturbation q + (e, e^2, e^3)).
+// Along x, e_k(x) = 1024 n_kx x + const: a half-line bounded at the crossing
+// x*, evaluated in fp64; exact int64 evaluation only when x* is within the
+// (tiny) fp64 error bound of an integer.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ i64 face_e(const SideRec& R, int k, int x, int y, int z) {
+  return 1024 * (R.nrm[k][0] * x + R.nrm[k][1] * y + R.nrm[k][2] * z) - R.cst[k];
+}
+
+__device__ __noinline__ void row_interval_exact(const SideRec& R, int y, int z, int& xl, int& xh) {
+  const int lo = R.lo[0], hi = R.hi[0];
+  xl = lo;
+  xh = hi;
+  const float dy = (float)(y - R.lo[1]), dz = (float)(z - R.lo[2]);
+  const int4 types = *reinterpret_cast<const int4*>(R.ftype);
+  const int tk[4] = {types.x, types.y, types.z, types.w};
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const int t = tk[k];
+    if (t == 0) {
+      const i64 E = face_e(R, k, 0, y, z);
+      const bool own = E > 0 || (E == 0 && (R.nrm[k][1] > 0 || (R.nrm[k][1] == 0 && R.nrm[k][2] > 0)));
+      if (!own) xh = lo - 1;
+      continue;
+    }
+    const float4 fc4 = R.face[k];
+    float xs = fmaf(fc4.z, dz, fmaf(fc4.y, dy, fc4.x));
+    xs = fminf(fmaxf(xs, (float)lo - 4.5f), (float)hi + 4.5f);
+    const float xr = rintf(xs);
+    if (t == 2 || t == -2) {  // exact monotone search (rare: nearly x-parallel face)
+      int x = (int)xr;
+      if (t > 0) {  // smallest x in [lo, hi+1] with e >= 0
+        x = min(max(x, lo), hi + 1);
+        while (x > lo && face_e(R, k, x - 1, y, z) >= 0) --x;
+        while (x <= hi && face_e(R, k, x, y, z) < 0) ++x;
+        xl = max(xl, x);
+      } else {      // largest x in [lo-1, hi] with e > 0
+        x = min(max(x, lo - 1), hi);
+        while (x < hi && face_e(R, k, x + 1, y, z) > 0) ++x;
+        while (x >= lo && face_e(R, k, x, y, z) <= 0) --x;
+        xh = min(xh, x);
+      }
+      continue;
+    }
+    int xi;
+    if (fabsf(xs - xr) > fc4.w) {
+      xi = (int)ceilf(xs) - (t < 0 ? 1 : 0);  // lower: smallest x > x*; upper: largest x < x*
+    } else {  // x* within the error bound of the integer c: decide exactly
+      const int c = (int)xr;
+      const i64 e = face_e(R, k, c, y, z);
+      xi = t > 0 ? (e >= 0 ? c : c + 1) : (e > 0 ? c : c - 1);
+    }
+    if (t > 0) xl = max(xl, xi);
+    else xh = min(xh, xi);
+  }
+}
+
+// all lanes call it (warp-uniform branch); lanes with ex = false keep (xl, xh)
+__device__ __noinline__ int2 row_interval_exact_if(bool ex, const SideRec& R, int y, int z, int xl, int xh) {
+  if (ex) row_interval_exact(R, y, z, xl, xh);
+  return make_int2(xl, xh);
+}
+
+// Fast path for items whose four faces are regular (n_x != 0, small crossing
+// error bound): four fp32 crossings; the exact routine only when a crossing is
+// within its bound of an integer.  Warp-collective: every lane calls it (rv:
+// the lane's row is real), the exact routine runs under a warp-uniform branch.
+__device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, bool rv, int& xl, int& xh) {
+  if (__all_sync(FULLMASK, !(R.flags & 4))) {  // item-uniform (R in shared memory)
+    const int2 r = row_interval_exact_if(rv, R, y, z, R.lo[0], R.hi[0]);
+    xl = r.x;
+    xh = r.y;
+    return;
+  }
+  const int lo = R.lo[0], hi = R.hi[0];
+  const float dy = (float)(y - R.lo[1]), dz = (float)(z - R.lo[2]);
+  const float flo = (float)lo - 4.5f, fhi = (float)hi + 4.5f;
+  const int4 types = *reinterpret_cast<const int4*>(R.ftype);
+  const int tk[4] = {types.x, types.y, types.z, types.w};
+  int l = lo, h = hi;
+  bool amb = false;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const float4 fc4 = R.face[k];
+    const float xs = fminf(fmaxf(fmaf(fc4.z, dz, fmaf(fc4.y, dy, fc4.x)), flo), fhi);
+    amb = amb || (fabsf(xs - rintf(xs)) <= fc4.w);
+    const int c = __float2int_ru(xs);  // lower face: smallest x > x*; upper: largest x < x* = c - 1
+    if (tk[k] > 0) l = max(l, c);
+    else h = min(h, c - 1);
+  }
+  xl = l;
+  xh = h;
+  amb = amb && rv;
+  if (__any_sync(FULLMASK, amb)) {
+    const int2 r = row_interval_exact_if(amb, R, y, z, xl, xh);
+    xl = r.x;
+    xh = r.y;
+  }
+}
+
+// Conservative y range of the tet's cross-section with the plane z (exact
+// vertex coordinates; edge intersections in fp32 with a 1e-3 voxel margin).
+__device__ __noinline__ void slice_y_range(const SideRec& R, int z, int& ylo, int& yhi) {
+  float ymin = 3.0e38f, ymax = -3.0e38f;
+  const float zf = (float)z;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+#pragma unroll
+    for (int j = i + 1; j < 4; j++) {
+      const float zi = R.vz[i], zj = R.vz[j];
+      const float lo = fminf(zi, zj), hi = fmaxf(zi, zj);
+      if (zf < lo || zf > hi) continue;
+      float y0, y1;
+      if (hi > lo) {
+        const float t = __fdividef(zf - zi, zj - zi);  // ~2 ulp: covered by the 1e-3 margin
+        y0 = y1 = fmaf(t, R.vy[j] - R.vy[i], R.vy[i]);
+      } else {
+        y0 = R.vy[i];
+        y1 = R.vy[j];
+      }
+      ymin = fminf(ymin, fminf(y0, y1));
+      ymax = fmaxf(ymax, fmaxf(y0, y1));
+    }
+  }
+  ylo = max(R.lo[1], (int)ceilf(fmaxf(ymin - 1e-3f, -1.0e6f)));
+  yhi = min(R.hi[1], (int)floorf(fminf(ymax + 1e-3f, 1.0e6f)));
+}
+
+constexpr int kQueueCap = 64;     // < 32 pending + one round of <= 32
+// per-warp shared memory <= 3.5 KB, so the 28-warp block stays <= 99 KB (the
+// 100 KB carve-out step; see kRasterDynSmem)
+constexpr int kStartWords = 64;  // row-start bitmap window: 2048 samples
+
+struct WarpSmem {
+  SideRec R;
+  unsigned starts[kStartWords];  // row-start bitmap of the current row chunk
+  int4 row_a[32];    // (exclusive prefix, linear index of row start, dx0, dy0 as float bits)
+  float4 row_b[32];  // (dz0, xl, y, z): fp32 displacement z at the row start, row start as floats
+  float4 sc0, sc1;   // per-side sample constants (see Sample)
+  int2 slices[32];   // non-empty z-slices of the current 32-slice chunk: (first row, ylo | slice << 16)
+  unsigned long long stat[3];  // samples, band entries, items of this warp (profiling)
+  // band-entry queue of the guidance term (a6): entries are evaluated 32 at a time
+  float4 qa[kQueueCap];  // (u, v, fx, fy): footprint texel coordinates and weights
+  int2 qb[kQueueCap];    // (fz bits, own linear index)
+  unsigned char qi[kQueueCap];  // pair i
+};
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(FULLMASK, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+
+// Generic rasterizer: visits every owned sample of the side.  Rows are
+// enumerated per z-slice over the slice's y range, 32 rows per step (lanes
+// compute the exact x-intervals); non-empty rows are compacted into shared
+// memory and their flattened samples are swept 32 per step.  A lane finds its
+// row from the shared-memory bitmap of row starts: one broadcast word per
+// 32-sample window and a popc.  Lanes past the end evaluate sample 0 of the last row with
+// valid = false (no divergence).  All lanes of the warp must call it.
+template <class F>
+__device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int loff, WarpSmem& S,
+                                       int lane, F& f) {
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int z0 = R.lo[2]; z0 <= R.hi[2]; z0 += 32) {
+    const int zl = z0 + lane;
+    int ylo, yhi;
+    slice_y_range(R, zl, ylo, yhi);  // every lane (no divergent call); masked below
+    const int cnt = zl <= R.hi[2] ? max(0, yhi - ylo + 1) : 0;
+    const int zincl = warp_incl_scan(cnt, lane);
+    const int nrows = __shfl_sync(FULLMASK, zincl, 31);
+    // non-empty slices of the chunk, compacted: (first row, ylo, slice) by rank
+    const int zstart = zincl - cnt;
+    const bool zne = cnt > 0;
+    {
+      const unsigned nem = __ballot_sync(FULLMASK, zne);
+      const unsigned addr = (unsigned)__cvta_generic_to_shared(&S.slices[__popc(nem & lt_mask)]);
+      __syncwarp();
+      // ylo < 768 (Q.10 window) and the slice index < 32 share one word
+      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.shared.v2.b32 [%1], {%2, %3};\n}"
+                   :
+                   : "r"((unsigned)zne), "r"(addr), "r"(zstart), "r"(ylo | (lane << 16))
+                   : "memory");
+      __syncwarp();
+    }
+    const unsigned le_mask0 = (2u << lane) - 1u;
+    for (int r0 = 0; r0 < nrows; r0 += 32) {
+      const int r = r0 + lane;
+      // the lane's slice: rank = (non-empty slices starting before r0) + (slice
+      // starts in [r0, r]) - 1, from one OR-reduction of start bits and a ballot
+      const unsigned sb = __reduce_or_sync(
+          FULLMASK, (zne && zstart >= r0 && zstart < r0 + 32) ? (1u << (zstart - r0)) : 0u);
+      const int before = __popc(__ballot_sync(FULLMASK, zne && zstart < r0));
+      MOREA_CHECK(before + __popc(sb & le_mask0) - 1 >= 0 && before + __popc(sb & le_mask0) - 1 < 32);
+      const int2 sl = S.slices[before + __popc(sb & le_mask0) - 1];
+      int xl, xh;
+      const int z = z0 + (sl.y >> 16);
+      const int y = (sl.y & 0xffff) + (r - sl.x);
+      const bool rv = r < nrows;
+      row_interval(R, y, z, rv, xl, xh);  // every lane (warp-collective)
+      const int len = rv ? max(0, xh - xl + 1) : 0;
+      const int incl = warp_incl_scan(len, lane);
+      const int total = __shfl_sync(FULLMASK, incl, 31);
+      if (total == 0) continue;
+      const unsigned ne = __ballot_sync(FULLMASK, len > 0);
+      const int start = incl - len;
+      __syncwarp();
+      {
+        // every lane computes its row record; lanes with a non-empty row store it
+        // (predicated stores: no divergent branch)
+        const int c = __popc(ne & lt_mask);
+        const float ox = (float)(xl - R.lo[0]), oy = (float)(y - R.lo[1]), oz = (float)(z - R.lo[2]);
+        float4 drow;
+        drow.x = fmaf(R.A[0][2], oz, fmaf(R.A[0][1], oy, fmaf(R.A[0][0], ox, R.d0[0])));
+        drow.y = fmaf(R.A[1][2], oz, fmaf(R.A[1][1], oy, fmaf(R.A[1][0], ox, R.d0[1])));
+        drow.z = fmaf(R.A[2][2], oz, fmaf(R.A[2][1], oy, fmaf(R.A[2][0], ox, R.d0[2])));
+        const unsigned ra_addr = (unsigned)__cvta_generic_to_shared(&S.row_a[c]);
+        const unsigned rb_addr = (unsigned)__cvta_generic_to_shared(&S.row_b[c]);
+        asm volatile(
+            "{\n .reg .pred p;\n setp.gt.s32 p, %0, 0;\n"
+            " @p st.shared.v4.b32 [%1], {%3, %4, %5, %6};\n"
+            " @p st.shared.v4.f32 [%2], {%7, %8, %9, %10};\n}"
+            :
+            : "r"(len), "r"(ra_addr), "r"(rb_addr), "r"(start), "r"((z * ny + y) * nx + xl + loff),
+              "r"(__float_as_int(drow.x)), "r"(__float_as_int(drow.y)), "f"(drow.z), "f"((float)xl),
+              "f"((float)y), "f"((float)z)
+            : "memory");
+      }
+      f.count_only(lane == 0 ? total : 0);
+      // Sweep in windows of 32 kStartWords samples.  The bitmap holds the row
+      // starts of the window (bit s of word s/32); a lane's row is the number of
+      // starts <= its sample index, minus one.  Past the end that is the last row
+      // (no starts there), evaluated with valid = false.  Blocks of 16 steps; the
+      // fp32 partial sums are flushed between blocks.
+      const unsigned le_mask = (2u << lane) - 1u;
+      int rprev = -1;
+      for (int base = 0; base < total; base += 32 * kStartWords) {
+        const int nw = min(kStartWords, (total - base + 31) >> 5);
+        __syncwarp();
+        // clear the whole bitmap window: one 16-byte store per lane
+        static_assert(kStartWords == 64, "one uint2 per lane clears the window");
+        reinterpret_cast<uint2*>(S.starts)[lane] = make_uint2(0u, 0u);
+        __syncwarp();
+        if (len > 0 && start >= base && start < base + 32 * kStartWords)
+          atomicOr(&S.starts[(start - base) >> 5], 1u << (start & 31));
+        __syncwarp();
+        for (int w0 = 0; w0 < nw; w0 += 16) {
+          const int wend = min(nw, w0 + 16);
+          for (int w = w0; w < wend; w++) {
+            MOREA_CHECK(w >= 0 && w < kStartWords);
+            const unsigned M = S.starts[w];
+            const int row = rprev + __popc(M & le_mask);
+            rprev += __popc(M);
+            const int idx = base + (w << 5) + lane;
+            const bool valid = idx < total;
+            MOREA_CHECK(row >= 0 && row < 32);
+            const int4 ra = S.row_a[row];
+            f.sample(ra, S.row_b[row], valid ? idx - ra.x : 0, valid);
+          }
+          f.flush_h();
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// O6 slow path: exact contributing corner set when the fp32 position is within
+// eps of a lattice plane on some axis.  x_a = (q_a M + N_a) / M exactly, with
+// M = 1024 |Delta| and N_a = sum_k e_k(q) U_ka (int128).
+// ---------------------------------------------------------------------------
+__device__ __noinline__ bool exact_fg(const SideRec& R, int qx, int qy, int qz, float dx, float dy,
+                                      float dz, const float* __restrict__ vol, int nx, int ny,
+                                      int nz) {
+  const int q[3] = {qx, qy, qz};
+  const float d[3] = {dx, dy, dz};
+  const int dims[3] = {nx, ny, nz};
+  i64 e[4];
+  for (int k = 0; k < 4; k++) e[k] = face_e(R, k, qx, qy, qz);
+  const i128 M = (i128)1024 * (i128)R.absdet;
+  int cnt[3], idx[3][2];
+  for (int a = 0; a < 3; a++) {
+    i128 N = 0;
+    for (int k = 0; k < 4; k++) N += (i128)e[k] * (i128)R.U[k][a];
+    const i128 Pn = (i128)q[a] * M + N;
+    if (Pn <= 0) {
+      cnt[a] = 1; idx[a][0] = 0;
+    } else if (Pn >= (i128)(dims[a] - 1) * M) {
+      cnt[a] = 1; idx[a][0] = dims[a] - 1;
+    } else {
+      i64 k0 = (i64)q[a] + (i64)floorf(d[a]);
+      while (Pn < (i128)k0 * M) --k0;
+      while (Pn >= (i128)(k0 + 1) * M) ++k0;
+      idx[a][0] = (int)k0;
+      if (Pn == (i128)k0 * M) {
+        cnt[a] = 1;
+      } else {
+        cnt[a] = 2; idx[a][1] = (int)k0 + 1;
+      }
+    }
+  }
+  for (int k = 0; k < cnt[2]; k++)
+    for (int j = 0; j < cnt[1]; j++)
+      for (int i = 0; i < cnt[0]; i++)
+        if (__ldg(&vol[((long long)idx[2][k] * ny + idx[1][j]) * nx + idx[0][i]]) > 0.0f) return true;
+  return false;
+}
+
+// all lanes of the warp call it (warp-uniform branch); lanes without an
+// ambiguous position keep their fg
+__device__ __noinline__ bool exact_fg_if(bool amb, bool fg, const SideRec& R, int qx, int qy, int qz,
+                                         float dx, float dy, float dz, const float* __restrict__ vol,
+                                         int nx, int ny, int nz) {
+  if (!amb) return fg;
+  return exact_fg(R, qx, qy, qz, dx, dy, dz, vol, nx, ny, nz);
+}
+
+__device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
+
+// Positivity-exact lerp: (1 - t) a + t b as fma(t, b, (1 - t) a).  For a, b >= 0
+// and t in [0, 1] it is > 0 iff a contributing value (a with t < 1, b with
+// t > 0) is > 0, barring underflow (excluded by the value precondition of
+// morea_load_images: non-zero intensities >= 2^-40).
+__device__ __forceinline__ float plerp(float a, float b, float t, float omt) {
+  return fmaf(t, b, omt * a);
+}
+
+// a5 + a6: one sample of side SIDE.  The footprint weights are exact: 0 / 1 on
+// clamped axes and exact-integer axes, and in [eps, 1 - eps] otherwise unless the
+// position is ambiguous (then exact_fg decides), so fg = (b > 0) is exact.
+// Volume pointers and texture handles are read from the kernel parameters with
+// compile-time offsets (constant bank): no registers, and texture handles are
+// provably warp-uniform (no waterfall loop around tld4).
+struct Acc {
+  double h, g;  // per-lane sums of h and of the guidance term (fp64)
+  float hf;     // fp32 partial sum of h over the last < 16 steps (flushed into h)
+  float gf;     // fp32 partial sum of guidance terms since the last flush (into g)
+  int n, nb;    // samples, band entries
+  int qn;       // band entries in the per-warp queue (warp-uniform)
+};
+
+template <bool TEX, int SIDE_T, bool CLAMP, bool DUMP>
+struct Sample {
+  const Volumes& V;
+  const SideRec& R;
+  WarpSmem& S;
+  const float4& sc0;  // shared: (A_x0, A_y0, A_z0, 0.5 - eps_x)  displacement gradient along x
+  const float4& sc1;  // shared: (0.5 - eps_y, 0.5 - eps_z, uoff, -): ambiguity thresholds on
+                      // |f - 0.5|; uoff = texel x offset of corner i0 + 1 in the gather layout
+  Acc& acc;
+  int side;           // runtime side when SIDE_T < 0 (warp-uniform)
+  float* dump_h;      // DUMP (test hook morea_sample_map): per-voxel h and fg of this side
+  unsigned char* dump_fg;
+  // CLAMP: some position of the item may leave the range the gather covers
+  // exactly, apply the O5 clamp (a separate instantiation: no predicated clamp
+  // instructions in the common loop)
+
+  // per-side data selected by a warp-uniform branch on compile-time parameter
+  // offsets, so texture handles stay in uniform registers
+  __device__ __forceinline__ const float* vol(int s) const { return s == 0 ? V.I[0] : V.I[1]; }
+
+  // the 8 corners (i0 .. i0+1)^3: two 2x2 texture gathers (tld4) or 8 loads
+  __device__ __forceinline__ void gather(const float* __restrict__ vol, unsigned long long tex,
+                                         float u, float v, int base, float c[8]) const {
+    if (TEX) {
+      const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v, 0);
+      const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v + V.fnyp, 0);
+      // gather order: (x0,y1) (x1,y1) (x1,y0) (x0,y0)
+      c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
+      c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
+    } else {
+      const int sy = V.nx, sz = V.nx * V.ny;
+      c[0] = __ldg(&vol[base]); c[1] = __ldg(&vol[base + 1]);
+      c[2] = __ldg(&vol[base + sy]); c[3] = __ldg(&vol[base + sy + 1]);
+      c[4] = __ldg(&vol[base + sz]); c[5] = __ldg(&vol[base + sz + 1]);
+      c[6] = __ldg(&vol[base + sz + sy]); c[7] = __ldg(&vol[base + sz + sy + 1]);
+    }
+  }
+
+  // tld4 pair (slices i0_z and i0_z + 1); u carries the volume's x offset
+  __device__ __forceinline__ void gather_tex(float u, float v, float c[8]) const {
+    const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texI, u, v, 0);
+    const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texI, u, v + V.fnyp, 0);
+    // gather order: (x0,y1) (x1,y1) (x1,y0) (x0,y0)
+    c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
+    c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
+  }
+
+  __device__ __forceinline__ static float tri(const float c[8], float fx, float fy, float fz,
+                                              float gx, float gy, float gz) {
+    return plerp(plerp(plerp(c[0], c[1], fx, gx), plerp(c[2], c[3], fx, gx), fy, gy),
+                 plerp(plerp(c[4], c[5], fx, gx), plerp(c[6], c[7], fx, gx), fy, gy), fz, gz);
+  }
+
+  // guidance term of one band entry (a6, O8): pair i of the side-s sample with
+  // own-record index lin = s V + q, mapped to texel u, v and weights fx, fy, fz
+  __device__ __forceinline__ void entry(float u, float v, float fx, float fy, float fz, int lin,
+                                        int i, int s) {
+    const int o = 1 - s;
+    const float d = __ldg(&(s == 0 ? V.dmap[0] : V.dmap[1])[(long long)(i - s) * V.V + lin]);
+    float e[8];
+    if (TEX) {
+      // u = i0_x + uoff0 + o fnxp (texel of I_o); map (o, i) is volume o K + i of texM
+      const float uu = fmaf((float)(o * (V.K - 1) + i), V.fnxp, u);
+      const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texM, uu, v, 0);
+      const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)V.texM, uu, v + V.fnyp, 0);
+      e[0] = g0.w; e[1] = g0.z; e[2] = g0.x; e[3] = g0.y;
+      e[4] = g1.w; e[5] = g1.z; e[6] = g1.x; e[7] = g1.y;
+    } else {
+      const int base = (int)(v - 1.0f) * V.nx + (int)(u - 1.0f);
+      gather((o == 0 ? V.dmap[0] : V.dmap[1]) + (long long)i * V.V, 0ull, 0.f, 0.f, base, e);
+    }
+    const float Dp = tri(e, fx, fy, fz, 1.f - fx, 1.f - fy, 1.f - fz);
+    const float dd = d - Dp;
+    // O8: w_i (r - d)/r (d - D'(x))^2, only where d < r (band bit).  r - d as
+    // (r_f - d) + (r - r_f): exact first difference for d >= r_f / 2, so the
+    // relative error of the small differences near the band edge stays at ulp
+    // level.  Term in fp32, partial sums in fp32 (flushed with h), sum in fp64.
+    const float rd = (V.rf - d) + V.rlo;
+    acc.gf += V.wf[s][i] * rd * (dd * dd);
+  }
+
+  // Band entries of this step's samples, one round per set bit, go to the
+  // per-warp queue, evaluated 32 at a time (acc.qn: queued count, warp-uniform).
+  __device__ __forceinline__ void enqueue(unsigned bm, int lin, float u, float v, float fx, float fy,
+                                          float fz, int s) {
+    const int lane = threadIdx.x & 31;
+    acc.nb += __popc(bm);
+    while (true) {
+      const unsigned take = __ballot_sync(FULLMASK, bm != 0u);
+      if (!take) break;
+      {
+        // computed by every lane, stored by lanes with a bit: predicated stores,
+        // no divergent branch (no convergence barrier per round)
+        const int i = __ffs(bm) - 1;
+        const int pos = acc.qn + __popc(take & ((1u << lane) - 1u));
+        MOREA_CHECK(pos < kQueueCap);
+        const unsigned qa_addr = (unsigned)__cvta_generic_to_shared(&S.qa[pos]);
+        const unsigned qb_addr = (unsigned)__cvta_generic_to_shared(&S.qb[pos]);
+        const unsigned qi_addr = (unsigned)__cvta_generic_to_shared(&S.qi[pos]);
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n"
+            " @p st.shared.v4.f32 [%1], {%4, %5, %6, %7};\n"
+            " @p st.shared.v2.b32 [%2], {%8, %9};\n"
+            " @p st.shared.u8 [%3], %10;\n}"
+            :
+            : "r"(bm), "r"(qa_addr), "r"(qb_addr), "r"(qi_addr), "f"(u), "f"(v), "f"(fx), "f"(fy),
+              "r"(__float_as_int(fz)), "r"(lin), "r"(i)
+            : "memory");
+        bm &= bm - 1u;
+      }
+      acc.qn += __popc(take);
+      if (__all_sync(FULLMASK, acc.qn >= 32)) {  // warp-uniform (VOTE): no BSSY
+        acc.qn -= 32;
+        __syncwarp();
+        const float4 ea = S.qa[acc.qn + lane];
+        const int2 eb = S.qb[acc.qn + lane];
+        entry(ea.x, ea.y, ea.z, ea.w, __int_as_float(eb.x), eb.y, (int)S.qi[acc.qn + lane], s);
+        __syncwarp();
+      }
+    }
+  }
+
+  __device__ __forceinline__ void count_only(int t) { acc.n += t; }
+
+  __device__ __forceinline__ void flush_h() {
+    acc.h += (double)acc.hf;
+    acc.hf = 0.f;
+    acc.g += (double)acc.gf;
+    acc.gf = 0.f;
+  }
+
+  // evaluate what is left in the queue (end of a side)
+  __device__ __forceinline__ void drain(int s) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    if (lane < acc.qn) {
+      const float4 ea = S.qa[lane];
+      const int2 eb = S.qb[lane];
+      entry(ea.x, ea.y, ea.z, ea.w, __int_as_float(eb.x), eb.y, (int)S.qi[lane], s);
+    }
+    __syncwarp();
+    acc.qn = 0;
+    flush_h();
+  }
+
+  __device__ __forceinline__ void sample(const int4& ra, const float4& rb, int k, bool valid) {
+    const int SIDE = SIDE_T >= 0 ? SIDE_T : side;
+    const int OTH = 1 - SIDE;
+    const int nx = V.nx, ny = V.ny, nz = V.nz;
+    const int lin = ra.y + k;
+    MOREA_CHECK(!valid || (lin >= (long long)SIDE * V.V && lin < (long long)(SIDE + 1) * V.V));
+    const uint2 own = __ldg(&V.own[0][lin]);  // lin = SIDE V + q
+    const float a = __uint_as_float(own.x);
+    const unsigned bm = valid ? own.y : 0u;
+    const float kf = (float)k;
+    const float4 s0 = sc0;
+    const float dx = fmaf(s0.x, kf, __int_as_float(ra.z)), dy = fmaf(s0.y, kf, __int_as_float(ra.w)),
+                dz = fmaf(s0.z, kf, rb.x);
+    const float flx = floorf(dx), fly = floorf(dy), flz = floorf(dz);
+    float fx = dx - flx, fy = dy - fly, fz = dz - flz;
+    const float4 s1 = sc1;
+    const bool amb = (fabsf(fx - 0.5f) > s0.w) | (fabsf(fy - 0.5f) > s1.x) | (fabsf(fz - 0.5f) > s1.y);
+    // lattice corner i0 as exact floats (< 2^24)
+    float ix = rb.y + kf + flx, iy = rb.z + fly, iz = rb.w + flz;
+    if (CLAMP) {
+      // O5 clamp: x <= 0 -> (0, f = 0), x >= n-1 -> (n-2, f = 1)
+      fx = ix < 0.f ? 0.f : (ix > V.fnx2 ? 1.f : fx);
+      fy = iy < 0.f ? 0.f : (iy > V.fny2 ? 1.f : fy);
+      fz = iz < 0.f ? 0.f : (iz > V.fnz2 ? 1.f : fz);
+      ix = fminf(fmaxf(ix, 0.f), V.fnx2);
+      iy = fminf(fmaxf(iy, 0.f), V.fny2);
+      iz = fminf(fmaxf(iz, 0.f), V.fnz2);
+    }
+    const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
+    // gather coordinates of corner i0 (Volumes::fnxp; exact floats)
+    const float u = ix + s1.z, v = fmaf(iz, V.fnyp, iy) + V.voff;
+    const int base = TEX ? 0 : ((int)iz * ny + (int)iy) * nx + (int)ix;
+    float c[8];
+    // the footprint lies inside the padded layout (positions in (-1, n) or clamped)
+    MOREA_CHECK(!TEX || !valid || (u >= 0.f && u + 1.f < 2.f * V.fnxp && v >= 0.f && v + V.fnyp + 1.f <= V.fnyp * (float)(nz + 2)));
+    MOREA_CHECK(TEX || !valid || (base >= 0 && (long long)base + (long long)nx * ny + nx + 1 < V.V));
+    if (TEX) gather_tex(u, v, c);
+    else gather(vol(OTH), 0ull, u, v, base, c);
+    const float b = tri(c, fx, fy, fz, gx, gy, gz);
+    bool fg = b > 0.f;
+    // warp-uniform branch around the rare exact path: no convergence barrier
+    // (BSSY/BMOV/BSYNC) in the common path (measured 2% faster)
+    if (__any_sync(FULLMASK, amb))
+      fg = exact_fg_if(amb, fg, R, (int)rb.y + k, (int)rb.z, (int)rb.w, dx, dy, dz, vol(OTH), nx, ny, nz);
+    // h of PAPER.md §4.1.2 (L318-322) with the exact case split (O6)
+    float h;
+    if (a > 0.f && fg) {
+      const float t = a - b;
+      h = t * t;
+    } else {
+      h = (a == 0.f && !fg) ? 0.f : 1.f;
+    }
+    // fp32 partial sum over at most 16 steps; raster() flushes it into the fp64
+    // lane sum (flush_h) every 16 steps
+    acc.hf += valid ? h : 0.f;
+    if (DUMP && valid) {  // the values just computed, at voxel q = lin - SIDE V
+      const long long q = (long long)lin - (long long)SIDE * V.V;
+      dump_h[q] = h;
+      dump_fg[q] = fg ? 1 : 0;
+    }
+    // a6: band entries go to the per-warp queue, evaluated 32 at a time
+    if (__reduce_or_sync(FULLMASK, bm)) enqueue(bm, lin, u, v, fx, fy, fz, SIDE);
+  }
+};
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+  return v;
+}
+
+// warp-cooperative copy of one SideRec into shared memory
+__device__ __forceinline__ void load_rec(WarpSmem& S, const SideRec* src, int lane) {
+  constexpr int kVec = (int)(sizeof(SideRec) / 16);
+  __syncwarp();
+  if (lane < kVec)
+    reinterpret_cast<int4*>(&S.R)[lane] = __ldg(reinterpret_cast<const int4*>(src) + lane);
+  __syncwarp();
+}
+
+template <bool TEX, int SIDE_T, bool DUMP>
+__device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int lane, Acc& acc,
+                                            int side, float* dump_h, unsigned char* dump_fg) {
+  const SideRec& R = S.R;
+  if (lane == 0) {
+    S.sc0 = make_float4(R.A[0][0], R.A[1][0], R.A[2][0], 0.5f - R.eps[0]);
+    // gather x of corner i0: I_o is volume o of texI (TEX), else a plain index + 1
+    const float uoff = TEX ? fmaf((float)(1 - (SIDE_T >= 0 ? SIDE_T : side)), V.fnxp, V.uoff0) : 1.0f;
+    S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], uoff, 0.f);
+  }
+  __syncwarp();
+  // O5 clamp only where a position can leave the range the gather covers exactly:
+  // [0, n-1) for plain loads, (-1, n) on the edge-padded textures (warp-uniform)
+  const int loff = (SIDE_T >= 0 ? SIDE_T : side) * (int)V.V;
+  if ((R.flags & ((TEX && kTexPad) ? 8 : 2)) == 0) {
+    Sample<TEX, SIDE_T, true, DUMP> f{V, R, S, S.sc0, S.sc1, acc, side, dump_h, dump_fg};
+    raster(R, V.nx, V.ny, loff, S, lane, f);
+    f.drain(SIDE_T >= 0 ? SIDE_T : side);
+  } else {
+    Sample<TEX, SIDE_T, false, DUMP> f{V, R, S, S.sc0, S.sc1, acc, side, dump_h, dump_fg};
+    raster(R, V.nx, V.ny, loff, S, lane, f);
+    f.drain(SIDE_T >= 0 ? SIDE_T : side);
+  }
+}
+
 
 // Block-local item dispenser for the one-block-per-SM kernels: warps take
 // consecutive items of the block's current chunk (the same tet for consecutive
@@ -258,29 +1002,105 @@ struct BlockQueue {
   }
 };
 
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
-  return v;
-}
-__device__ __forceinline__ int warp_sum_i(int v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
-  return v;
-}
+// ---------------------------------------------------------------------------
+// k_raster: persistent warps over the item queue (a4 + a5 + a6 + per-tet a7).
+// ---------------------------------------------------------------------------
+// one block per SM: its warps take consecutive items (the same tet for
+// consecutive solutions) together, so their footprints share the SM's L1
+constexpr int kRasterBlockWarps = MOREA_SM_BLOCK;
+constexpr int kRasterBlockThreads = 32 * kRasterBlockWarps;
+#define RASTER_BOUNDS __launch_bounds__(kRasterBlockThreads, 1)
 
-#include "morea_sweep.cuh"
-
-// per-tet sums of one (version, entry, solution): its z-slabs in order
-__device__ __forceinline__ HGN hgn_sum(const EvalArgs& A, int v, int e, int sol) {
-  HGN r;
-  r.h = r.g = 0.0;
-  r.n = r.n0 = 0;
-  for (int s = A.slab_off[e]; s < A.slab_off[e + 1]; s++) {
-    const HGN x = A.hgn[((long long)v * A.n_slabs + s) * A.P + sol];
-    r.h += x.h; r.g += x.g; r.n += x.n; r.n0 += x.n0;
+template <bool TEX, bool DUMP>
+__global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpSmem* smem = reinterpret_cast<WarpSmem*>(smem_raw);
+  __shared__ BlockQueue bq;
+  bq.init();
+  // warp index and lane through volatile asm: kept in registers instead of being
+  // re-derived from special registers at every use
+  int warp, lane;
+  asm volatile("shr.u32 %0, %1, 5;" : "=r"(warp) : "r"(threadIdx.x));
+  asm volatile("and.b32 %0, %1, 31;" : "=r"(lane) : "r"(threadIdx.x));
+  WarpSmem& S = smem[warp];
+  const long long per_v = (long long)A.n_entries * A.P;
+  const long long n_items = per_v * A.n_raster_versions;
+  if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0ull;
+  while (true) {
+    unsigned long long item = 0;
+    item = bq.claim(A.counter, lane, n_items, MOREA_CLAIM_CHUNK, MOREA_CLAIM_SPREAD);
+    if ((long long)item >= n_items) break;
+    const int v = (int)(item / (unsigned long long)per_v);
+    const long long rem = (long long)item - (long long)v * per_v;
+    const int es = (int)(rem / A.P);
+    const int sol = (int)(rem - (long long)es * A.P);
+    const int e = A.sched[es];
+    MOREA_CHECK(e >= 0 && e < A.n_entries && v < A.n_raster_versions);
+    const long long i = ((long long)v * A.n_entries + e) * A.P + sol;
+    Acc acc{0.0, 0.0, 0.f, 0.f, 0, 0, 0};
+    int n_side0 = 0;
+#pragma unroll 1
+    for (int side = 0; side < 2; side++) {
+      if (DUMP && side != A.dump_side) continue;
+      load_rec(S, &A.geom[2 * i + side], lane);
+      if (S.R.flags & 1) raster_side<TEX, -1, DUMP>(A.vol, S, lane, acc, side, A.dump_h, A.dump_fg);
+      if (side == 0) n_side0 = acc.n;
+    }
+    HGN out;
+    out.h = warp_sum_d(acc.h + (double)acc.hf);
+    out.g = warp_sum_d(acc.g);
+    out.n = warp_sum_i(acc.n);
+    out.n0 = warp_sum_i(n_side0);
+    const int nb = warp_sum_i(acc.nb);
+    if (lane == 0) {
+      A.hgn[i] = out;
+      S.stat[0] += out.n;
+      S.stat[1] += nb;
+      S.stat[2] += 1;
+    }
   }
-  return r;
+  if (lane == 0 && A.stats) {
+    atomicAdd(&A.stats[0], S.stat[0]);
+    atomicAdd(&A.stats[1], S.stat[1]);
+    atomicAdd(&A.stats[2], S.stat[2]);
+  }
+}
+
+constexpr size_t kRasterDynSmem = MOREA_SM_BLOCK ? sizeof(WarpSmem) * kRasterBlockWarps : 0;
+// shared memory decides the L1/shared carve-out of the SM (steps 100, 132, ...
+// KB, 1 KB per block reserved by the system): at <= 99 KB the carve-out is
+// 100 KB and the texture/L1 cache keeps 156 KB (measured: 8 KB more shared
+// memory, crossing a step, costs 2.3%)
+static_assert(!MOREA_SM_BLOCK || kRasterDynSmem + 1024 + 64 <= 100 * 1024,
+              "k_raster shared memory above the 100 KB carve-out step");
+
+int raster_blocks_per_sm(bool tex) {
+  if (kRasterDynSmem) {
+    cudaFuncSetAttribute(k_raster<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRasterDynSmem);
+    cudaFuncSetAttribute(k_raster<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRasterDynSmem);
+    cudaFuncSetAttribute(k_raster<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRasterDynSmem);
+    cudaFuncSetAttribute(k_raster<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRasterDynSmem);
+  }
+  int nb = 0;
+  cudaError_t e = tex ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_raster<true, false>,
+                                                                      kRasterBlockThreads, kRasterDynSmem)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_raster<false, false>,
+                                                                      kRasterBlockThreads, kRasterDynSmem);
+  if (e != cudaSuccess) return 1;
+  return nb > 0 ? nb : 1;
+}
+
+int raster_block_warps() { return kRasterBlockWarps; }
+
+cudaError_t launch_raster(const EvalArgs& a, int grid, cudaStream_t s) {
+  if (a.dump_h) {  // test hook morea_sample_map
+    if (a.vol.use_tex) k_raster<true, true><<<grid, kRasterBlockThreads, kRasterDynSmem, s>>>(a);
+    else k_raster<false, true><<<grid, kRasterBlockThreads, kRasterDynSmem, s>>>(a);
+  } else {
+    if (a.vol.use_tex) k_raster<true, false><<<grid, kRasterBlockThreads, kRasterDynSmem, s>>>(a);
+    else k_raster<false, false><<<grid, kRasterBlockThreads, kRasterDynSmem, s>>>(a);
+  }
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -305,7 +1125,7 @@ __global__ void k_reduce(const EvalArgs A, int G, const int* __restrict__ group_
   for (int e = group_off[g] + lane; e < group_off[g + 1]; e += 32) {
     const long long i0 = (long long)e * P + sol;
     const Scal s0 = A.scal[i0];
-    HGN r0 = hgn_sum(A, 0, e, sol);
+    const HGN r0 = A.hgn[i0];
     const int tet = A.canon_tet ? A.canon_tet[e] : e;
     dom |= s0.flags & 1;
     if (!A.partial) {
@@ -322,7 +1142,7 @@ __global__ void k_reduce(const EvalArgs A, int G, const int* __restrict__ group_
         const double* c = cache_in + ((long long)sol * T + tet) * 4;
         oh = c[0]; og = c[1]; on = (long long)c[2];
       } else {
-        const HGN r1 = hgn_sum(A, 1, e, sol);
+        const HGN r1 = A.hgn[i0 + per_v];
         oh = r1.h; og = r1.g; on = r1.n;
       }
       h += r0.h - oh; gs += r0.g - og; m += s0.m - s1.m; sev += s0.sev - s1.sev;
@@ -464,6 +1284,63 @@ cudaError_t launch_check_folds(const MeshDev& m, const double sp[3], int P, cons
 }
 
 // ---------------------------------------------------------------------------
+// Owner-map test hook: the same SideRec + rasterizer, one warp per tet.
+// ---------------------------------------------------------------------------
+struct OwnerSample {
+  int* owner;
+  int tet;
+  __device__ __forceinline__ void flush_h() {}
+  __device__ __forceinline__ void count_only(int) {}
+  __device__ __forceinline__ void sample(const int4& ra, const float4&, int k, bool valid) {
+    if (!valid) return;
+    const int lin = ra.y + k;
+    const int old = atomicCAS(&owner[lin], -1, tet);
+    if (old != -1) atomicExch(&owner[lin], -2);
+  }
+};
+
+__global__ void __launch_bounds__(kRasterThreads) k_owner_map(const EvalArgs A, int side,
+                                                              int* __restrict__ owner) {
+  __shared__ WarpSmem smem[kWarpsPerBlock];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tet = blockIdx.x * kWarpsPerBlock + warp;
+  if (tet >= A.mesh.T) return;
+  WarpSmem& S = smem[warp];
+  load_rec(S, &A.geom[2 * (long long)tet + side], lane);
+  if (!(S.R.flags & 1)) return;
+  OwnerSample f{owner, tet};
+  raster(S.R, A.vol.nx, A.vol.ny, 0, S, lane, f);
+}
+
+__global__ void k_fill_int(int* p, long long n, int v) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_fill_dump(float* h, unsigned char* fg, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    h[i] = __int_as_float(0x7fc00000);
+    fg[i] = 255;
+  }
+}
+
+cudaError_t launch_fill(float* h, unsigned char* fg, long long V, cudaStream_t s) {
+  k_fill_dump<<<1024, 256, 0, s>>>(h, fg, V);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_owner_map(const EvalArgs& a, int side, int* owner, cudaStream_t s) {
+  k_fill_int<<<1024, 256, 0, s>>>(owner, a.vol.V, -1);
+  cudaError_t e = launch_setup(a, s);
+  if (e != cudaSuccess) return e;
+  const int blocks = (a.mesh.T + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  k_owner_map<<<blocks, kRasterThreads, 0, s>>>(a, side, owner);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // a0: load-time work.
 // ---------------------------------------------------------------------------
 __global__ void k_validate_volume(const float* __restrict__ I, long long V, int* bad) {
@@ -574,6 +1451,7 @@ cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, un
 }
 
 #include "morea_repair.cuh"
+#include "morea_export.cuh"
 #include "morea_mix.cuh"
 
 }  // namespace morea

@@ -1,13 +1,13 @@
 """Bit-exact ownership and the exact h case split at paper scale (run with -m gpu).
 
 north_star: "bit-exact ownership/fold results ... on all five configs".  The
-owner map of the evaluation's own rasterizer (morea_owner_map: k_sweep's
-per-lane rows, one solution) is compared voxel by voxel with the oracle's
+owner map of the evaluation's own rasterizer (morea_owner_map: k_raster's
+exact row intervals, one solution) is compared voxel by voxel with the oracle's
 per-voxel bbox loop (O3, App. A.2) at C3, C4 and one C5
 shard, on the identity, a solution with alpha ~ 1 (k = P - 1) and a forced fold
 (k = 7 mod 16).  The per-sample h-case decision fg (O6, eq. L316-323) of one
 full C4 solution comes from the evaluation kernel itself (morea_sample_map, a
-dump instantiation of k_sweep) and must agree with the oracle's exact int128
+dump instantiation of k_raster) and must agree with the oracle's exact int128
 decision on every voxel of both sides.
 """
 import numpy as np

@@ -1,5 +1,5 @@
 """Dev tool: key metrics, stall reasons and per-source-line instruction / stall shares of
-the k_sweep launches in an ncu report.  usage: python tools/ncu_sweep.py report [n_lines]"""
+the captured launches in an ncu report (k_raster).  usage: python tools/ncu_sweep.py report [n_lines]"""
 import collections
 import csv
 import subprocess
