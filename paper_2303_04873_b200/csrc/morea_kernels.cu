@@ -880,8 +880,10 @@ struct Sample {
     const float u = ix + s1.z, v = fmaf(iz, V.fnyp, iy) + V.voff;
     const int base = TEX ? 0 : ((int)iz * ny + (int)iy) * nx + (int)ix;
     float c[8];
-    // the footprint lies inside the padded layout (positions in (-1, n) or clamped)
-    MOREA_CHECK(!TEX || !valid || (u >= 0.f && u + 1.f < 2.f * V.fnxp && v >= 0.f && v + V.fnyp + 1.f <= V.fnyp * (float)(nz + 2)));
+    // the footprint lies inside the padded layout (positions in (-1, n) or clamped):
+    // gather at integer (u, v) reads texel columns u-1, u and rows v-1, v (+ fnyp)
+    MOREA_CHECK(!TEX || !valid || (u >= 1.f && u <= 2.f * V.fnxp - 1.f));
+    MOREA_CHECK(!TEX || !valid || (v >= 1.f && v + V.fnyp <= V.fnyp * (float)(nz + 2) - 1.f));
     MOREA_CHECK(TEX || !valid || (base >= 0 && (long long)base + (long long)nx * ny + nx + 1 < V.V));
     if (TEX) gather_tex(u, v, c);
     else gather(vol(OTH), 0ull, u, v, base, c);
