@@ -59,9 +59,9 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
             raise RuntimeError(f"nvcc failed on {s}")
         if verbose:
             sys.stderr.write(se)
-        if out is None:
+        if out is None:  # the resource report of this build (compile times dropped: reproducible)
             with open(os.path.join(CSRC, s + ".ptxas.txt"), "w") as f:
-                f.write(se)
+                f.write("".join(l for l in se.splitlines(True) if "Compile time" not in l))
     tmp = lib + ".tmp"
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
            "-Xcompiler", "-fPIC"]
