@@ -361,7 +361,7 @@ cudaError_t eval_scratch(morea_ctx* ctx, EvalArgs& a) {
     if (e != cudaSuccess) return e;
     a.geom = ctx->geom.as<SideRec>();
   }
-  e = ctx->counter.ensure(sizeof(unsigned long long));
+  e = ctx->counter.ensure(3 * sizeof(unsigned long long));
   if (e != cudaSuccess) return e;
   a.counter = ctx->counter.as<unsigned long long>();
   a.stats = ctx->prof ? ctx->stats.as<unsigned long long>() : nullptr;
@@ -389,7 +389,7 @@ cudaError_t run_eval(morea_ctx* ctx, EvalArgs& a) {
   if (e != cudaSuccess) return e;
   const long long n_items = (long long)a.n_entries * a.P * a.n_raster_versions;
   if (n_items == 0) return cudaSuccess;
-  e = cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), ctx->stream);
+  e = cudaMemsetAsync(ctx->counter.p, 0, 3 * sizeof(unsigned long long), ctx->stream);
   if (e != cudaSuccess) return e;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (ctx->prof) {

@@ -160,7 +160,8 @@ struct EvalArgs {
   double rate;               // Sobol samples per voxel of tet volume
   const unsigned* sobol_v;   // [4][32] Sobol direction numbers (device)
   int sobol_force_exact;     // test hook (env MOREA_SOBOL_FORCE_EXACT): every sample takes the fp64 path
-  unsigned long long* counter;  // work queue head (zeroed before launch)
+  unsigned long long* counter;  // work queue head (zeroed before launch); debug builds: counter[1] =
+                                // items processed, counter[2] = blocks finished (exactly-once check)
   unsigned long long* stats;    // [samples, band entries, items]
   float* dump_h;                // test hook morea_sample_map: per-voxel h and fg of side dump_side
   unsigned char* dump_fg;

@@ -91,14 +91,19 @@ __device__ __forceinline__ bool load_tet(const EvalArgs& A, int sol, int4 tv, in
   for (int k = 0; k < 4; k++) {
     const int j = vid[k];
     MOREA_CHECK(j >= 0 && j < A.mesh.N && sl[k] < A.S_total && sol >= 0 && sol < A.P);
-    const float* o = sl[k] >= 0 ? A.new_vals + ((long long)sol * A.S_total + sl[k]) * 6
-                                : A.offsets + ((long long)sol * A.mesh.N + j) * 6;
+    // the point's 6 offsets (24 contiguous bytes) as three 8-byte loads; the API
+    // stages offsets / new values that are not 8-byte aligned
+    const float2* o = reinterpret_cast<const float2*>(
+        sl[k] >= 0 ? A.new_vals + ((long long)sol * A.S_total + sl[k]) * 6
+                   : A.offsets + ((long long)sol * A.mesh.N + j) * 6);
+    const float2 o01 = __ldg(o), o23 = __ldg(o + 1), o45 = __ldg(o + 2);
+    const float oo[6] = {o01.x, o01.y, o23.x, o23.y, o45.x, o45.y};
 #pragma unroll
     for (int a = 0; a < 3; a++) {
       const float b = __ldg(&A.mesh.base[3 * j + a]);
 #pragma unroll
       for (int s = 0; s < 2; s++) {
-        const i64 q = canon_q(b, __ldg(&o[3 * s + a]));
+        const i64 q = canon_q(b, oo[3 * s + a]);
         ok = ok && (q >= kQLo) && (q < kQHi);
         Q[s][k][a] = (int)q;
       }
@@ -273,7 +278,7 @@ __device__ double magnitude(const int Q[2][4][3], double c, const double sp2[3],
 // ---------------------------------------------------------------------------
 // k_setup: one thread per (version, canonical entry, solution).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_setup(const EvalArgs A) {
+__global__ void __launch_bounds__(128, 3) k_setup(const EvalArgs A) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long per_v = (long long)A.n_entries * A.P;
   if (i >= per_v * A.n_setup_versions) return;
@@ -914,6 +919,29 @@ struct Sample {
   }
 };
 
+
+// Debug builds: the BlockQueue hands out every item exactly once.  Each processed
+// item is counted; the last block to finish checks the count against n_items (a
+// lost or a duplicated claim fails the check).
+__device__ __forceinline__ void debug_count_item(const EvalArgs& A) {
+#ifdef MOREA_DEBUG_CHECKS
+  atomicAdd(&A.counter[1], 1ull);
+#endif
+}
+__device__ __forceinline__ void debug_check_items(const EvalArgs& A, long long n_items) {
+#ifdef MOREA_DEBUG_CHECKS
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long done = atomicAdd(&A.counter[2], 1ull);
+    if (done == gridDim.x - 1) {
+      __threadfence();
+      MOREA_CHECK(atomicAdd(&A.counter[1], 0ull) == (unsigned long long)n_items);
+    }
+  }
+#endif
+}
+
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
@@ -1059,8 +1087,10 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
       S.stat[0] += out.n;
       S.stat[1] += nb;
       S.stat[2] += 1;
+      debug_count_item(A);
     }
   }
+  debug_check_items(A, n_items);
   if (lane == 0 && A.stats) {
     atomicAdd(&A.stats[0], S.stat[0]);
     atomicAdd(&A.stats[1], S.stat[1]);
@@ -1244,13 +1274,17 @@ __global__ void k_check_folds(MeshDev M, double sp0, double sp1, double sp2, int
     const int vid[4] = {tv.x, tv.y, tv.z, tv.w};
     int Q[2][4][3];
     bool ok = true;
-    for (int k = 0; k < 4; k++)
+    for (int k = 0; k < 4; k++) {
+      const float2* o = reinterpret_cast<const float2*>(offsets + ((long long)sol * M.N + vid[k]) * 6);
+      const float2 o01 = __ldg(o), o23 = __ldg(o + 1), o45 = __ldg(o + 2);  // 24 contiguous bytes
+      const float oo[6] = {o01.x, o01.y, o23.x, o23.y, o45.x, o45.y};
       for (int a = 0; a < 3; a++)
         for (int s = 0; s < 2; s++) {
-          const i64 q = canon_q(M.base[3 * vid[k] + a], offsets[((long long)sol * M.N + vid[k]) * 6 + 3 * s + a]);
+          const i64 q = canon_q(M.base[3 * vid[k] + a], oo[3 * s + a]);
           ok = ok && q >= kQLo && q < kQHi;
           Q[s][k][a] = (int)q;
         }
+    }
     for (int s = 0; s < 2; s++) {
       int f = 0;
       if (ok) {

@@ -368,8 +368,10 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
       S.stat[0] += n_tot;
       S.stat[1] += nb_w;
       S.stat[2] += 1;
+      debug_count_item(A);
     }
   }
+  debug_check_items(A, n_items);
   if (lane == 0 && A.stats) {
     atomicAdd(&A.stats[0], S.stat[0]);
     atomicAdd(&A.stats[1], S.stat[1]);
