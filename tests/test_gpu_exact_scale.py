@@ -141,3 +141,60 @@ def test_plan_cache_every_colour_class(wl):
             else:
                 assert np.array_equal(r[0], first[i][0]) and np.array_equal(r[1], first[i][1])
     ctx.close()
+
+
+def test_plan_cache_eviction_and_input_staging(wl):
+    """ADVICE r1 follow-ups on the host layer: (1) more distinct FOS requests than the LRU
+    holds (64) evict and rebuild plans with identical results; (2) pinned host inputs are
+    consumed before the call returns (refilling the buffer at once does not change the
+    result); (3) device offsets that are not 8-byte aligned are staged, bitwise equal."""
+    w = wl(2)
+    ctx = _ctx(w)
+    plan = fos_plan(w.tets, w.N)
+    dev = torch.device("cuda:0")
+    P = w.P
+    off = torch.from_numpy(w.offsets).to(dev)
+    obj = torch.empty((P, 3), dtype=torch.float64, device=dev)
+    acc = torch.empty((P, 6), dtype=torch.int64, device=dev)
+    tc = torch.empty((P, w.T, 4), dtype=torch.float64, device=dev)
+    ctx.eval_full(off, obj, acc, tc)
+    go, ch, nv = partial_request(w, plan, "class", 0)
+    nv_d = torch.from_numpy(nv).to(dev)
+    G = len(go) - 1
+
+    def part(goo, chh, nvv):
+        g = len(goo) - 1
+        po = torch.empty((P * g, 3), dtype=torch.float64, device=dev)
+        pa = torch.empty((P * g, 6), dtype=torch.int64, device=dev)
+        ctx.eval_partial(off, acc, goo, chh, nvv, tc, po, pa)
+        torch.cuda.synchronize()
+        return po.cpu().numpy(), pa.cpu().numpy()
+
+    ref = part(go, ch, nv_d)
+    # (1) 70 single-group requests (one per edge of the class, then repeats), then the first again
+    for i in range(70):
+        g = i % G
+        s0, s1 = go[g], go[g + 1]
+        gg = np.array([0, s1 - s0], np.int32)
+        part(gg, ch[s0:s1], torch.from_numpy(np.ascontiguousarray(nv[:, s0:s1])).to(dev))
+    again = part(go, ch, nv_d)
+    assert np.array_equal(again[0], ref[0]) and np.array_equal(again[1], ref[1])
+    # (2) pinned host input, refilled right after the call
+    nv_h = torch.from_numpy(nv.copy()).pin_memory()
+    po = torch.empty((P * G, 3), dtype=torch.float64, device=dev)
+    pa = torch.empty((P * G, 6), dtype=torch.int64, device=dev)
+    ctx.eval_partial(off, acc, go, ch, nv_h, tc, po, pa)
+    nv_h.fill_(1000.0)  # would put every point outside the window if still being read
+    torch.cuda.synchronize()
+    assert np.array_equal(po.cpu().numpy(), ref[0]) and np.array_equal(pa.cpu().numpy(), ref[1])
+    # (3) misaligned device offsets (4-byte offset into a larger buffer)
+    big = torch.empty(off.numel() + 1, dtype=torch.float32, device=dev)
+    big[1:] = off.reshape(-1)
+    mis = big[1:].view(P, w.N, 6)
+    assert mis.data_ptr() % 8 == 4
+    obj2 = torch.empty_like(obj)
+    acc2 = torch.empty_like(acc)
+    ctx.eval_full(mis, obj2, acc2, None)
+    torch.cuda.synchronize()
+    assert torch.equal(obj2, obj) and torch.equal(acc2, acc)
+    ctx.close()
