@@ -318,14 +318,14 @@ int morea_distance_map(morea_ctx *ctx, int side, int pair, float *out);
  * the rasterize/evaluate kernel is bracketed by CUDA events on the context
  * stream and its algorithmic work is counted.  morea_prof_read synchronises
  * and returns: launches, summed kernel milliseconds, sampled voxels, band
- * entries, (slab, solution) items and the warp-steps of the voxel sweep (32
- * lane-steps each: the lane utilisation is samples / (32 warp_steps)).
- * Reading resets the counters. */
+ * entries, (tet, solution) items, and the sampled voxels whose 32-sample step
+ * was skipped as empty space (background on both sides, no band entry: h = 0
+ * exactly, no gather).  Reading resets the counters. */
 int morea_prof_enable(morea_ctx *ctx, int on);
 /* Number of kernels this context has launched since it was created. */
 int64_t morea_kernel_launches(const morea_ctx *ctx);
 int morea_prof_read(morea_ctx *ctx, int64_t *launches, double *ms, int64_t *samples,
-                    int64_t *band_entries, int64_t *items, int64_t *warp_steps);
+                    int64_t *band_entries, int64_t *items, int64_t *skipped);
 
 #ifdef __cplusplus
 }

@@ -106,7 +106,8 @@ struct morea_ctx {
   double sp[3] = {1, 1, 1};
   double r = 0;
   double w[2][kMaxPairs] = {};
-  DevBuf I[2], band[2], dmap[2], wts, own;
+  DevBuf I[2], band[2], dmap[2], wts, own, qst;
+  int qlevels = 0;
   // Sobol sampler (NEXT-1): mode, rate, dilated band masks (2 V bytes), direction numbers
   int sampler = MOREA_SAMPLER_VOXEL;
   double rate = 1.0;
@@ -299,6 +300,9 @@ Volumes volumes_of(const morea_ctx* c) {
     for (int i = 0; i < kMaxPairs; i++) v.wf[s][i] = c->r > 0 ? (float)(c->w[s][i] / c->r) : 0.f;
   v.rf = (float)c->r;
   v.rlo = (float)(c->r - (double)v.rf);
+  for (int s = 0; s < 2; s++)
+    v.qst[s] = c->qst.p ? c->qst.as<unsigned char>() + (size_t)s * c->qlevels * c->V : nullptr;
+  v.qlevels = c->qlevels;
   v.own[0] = c->own.as<uint2>();
   v.own[1] = v.own[0] ? v.own[0] + c->V : nullptr;
   v.use_tex = c->use_tex ? 1 : 0;
@@ -725,7 +729,7 @@ void morea_destroy(morea_ctx* ctx) {
     cudaEventDestroy(p.second);
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
-                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->st_masks, &ctx->st_counts, &ctx->st_dvf, &ctx->st_cov,
+                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->qst, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->st_masks, &ctx->st_counts, &ctx->st_dvf, &ctx->st_cov,
                     &ctx->scratch_owner, &ctx->zero_off, &ctx->mx_off, &ctx->mx_acc,
                     &ctx->mx_obj, &ctx->mx_cache, &ctx->mx_nv, &ctx->mx_pobj, &ctx->mx_pacc, &ctx->mx_dep,
                     &ctx->mx_base, &ctx->mx_accepted, &ctx->mx_cluster, &ctx->mx_mu, &ctx->mx_L, &ctx->mx_arch,
@@ -824,9 +828,26 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
     CK(cudaMemcpy((char*)ctx->wts.p + sizeof(ctx->w), wf.data(), wf.size() * sizeof(float), cudaMemcpyHostToDevice));
   }
   CK(ctx->own.ensure(2 * V * sizeof(uint2)));
-  for (int s = 0; s < 2; s++)
-    CK(launch_own_records(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr, V,
-                          ctx->own.as<uint2>() + (size_t)s * V, ctx->stream));
+  {
+    DevBuf zr, m0, m1;  // zero radius of the other volume (empty-space skipping)
+    CK(zr.ensure(V));
+    CK(m0.ensure(V));
+    CK(m1.ensure(V));
+    int levels = 1;
+    while ((2 << (levels - 1)) <= nx) levels++;  // 2^(levels-1) <= nx < 2^levels
+    ctx->qlevels = levels;
+    CK(ctx->qst.ensure((size_t)2 * levels * V));
+    for (int s = 0; s < 2; s++) {
+      CK(launch_zero_radius(ctx->I[1 - s].as<float>(), nx, ny, nz, zr.as<unsigned char>(), m0.as<unsigned char>(),
+                            m1.as<unsigned char>(), ctx->stream));
+      CK(launch_own_records(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr,
+                            zr.as<unsigned char>(), V, ctx->own.as<uint2>() + (size_t)s * V, ctx->stream));
+      CK(launch_quiet_table(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr,
+                            zr.as<unsigned char>(), nx, V, levels,
+                            ctx->qst.as<unsigned char>() + (size_t)s * levels * V, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   CK(build_textures(ctx));
   ctx->dil.release();
@@ -1449,7 +1470,7 @@ int morea_prof_enable(morea_ctx* ctx, int on) {
 }
 
 int morea_prof_read(morea_ctx* ctx, int64_t* launches, double* ms, int64_t* samples,
-                    int64_t* band_entries, int64_t* items, int64_t* warp_steps) {
+                    int64_t* band_entries, int64_t* items, int64_t* skipped) {
   if (!ctx) return MOREA_EINVAL;
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1470,7 +1491,7 @@ int morea_prof_read(morea_ctx* ctx, int64_t* launches, double* ms, int64_t* samp
   if (samples) *samples = (int64_t)st[0];
   if (band_entries) *band_entries = (int64_t)st[1];
   if (items) *items = (int64_t)st[2];
-  if (warp_steps) *warp_steps = (int64_t)st[3];
+  if (skipped) *skipped = (int64_t)st[3];
   ctx->prof_launches = 0;
   return MOREA_OK;
 }

@@ -20,6 +20,10 @@ __device__ __forceinline__ int voxel_label(unsigned m, int M) {
 }
 
 struct LabelSample {
+  static constexpr bool kQuiet = false;
+  __device__ __forceinline__ const unsigned char* quiet_table(int) const { return nullptr; }
+  __device__ __forceinline__ int quiet_radius() const { return 1 << 30; }
+  __device__ __forceinline__ void quiet_row(long long, int) {}
   const unsigned char* masks;
   int M;
   int* cnt;  // shared: M + 1 counters of this warp
@@ -52,6 +56,10 @@ __global__ void __launch_bounds__(kRasterThreads) k_label_counts(const EvalArgs 
 
 // E3 pass 1: owner = lowest owning tet id (deterministic under folds)
 struct MinOwnerSample {
+  static constexpr bool kQuiet = false;
+  __device__ __forceinline__ const unsigned char* quiet_table(int) const { return nullptr; }
+  __device__ __forceinline__ int quiet_radius() const { return 1 << 30; }
+  __device__ __forceinline__ void quiet_row(long long, int) {}
   int* owner;
   int tet;
   __device__ __forceinline__ void flush_h() {}
@@ -64,6 +72,10 @@ struct MinOwnerSample {
 // E3 pass 2: T(q) - q = sum_k e_k(q) U_k / (1024 |Delta|) (O4), exact numerator,
 // one fp64 rounding (the oracle's operations), times the spacing, fp32
 struct DvfSample {
+  static constexpr bool kQuiet = false;
+  __device__ __forceinline__ const unsigned char* quiet_table(int) const { return nullptr; }
+  __device__ __forceinline__ int quiet_radius() const { return 1 << 30; }
+  __device__ __forceinline__ void quiet_row(long long, int) {}
   const SideRec* R;  // shared
   const int* owner;
   int tet;

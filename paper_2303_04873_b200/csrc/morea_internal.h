@@ -92,9 +92,13 @@ struct Volumes {
   double sp[3];
   const float* I[2];
   const unsigned char* band[2];  // per voxel bit i = [D_i(q) < r]; nullptr when K == 0
-  // per voxel (bits of I_side(q), band bits): one 8-byte load; one allocation,
+  // per voxel (bits of I_side(q), band bits | zero radius << 8): one 8-byte load; one allocation,
   // own[1] = own[0] + V, so side s of voxel q is own[0][s V + q]
   const uint2* own[2];
+  // quiet radii (empty space): per side, sparse table along x of
+  // min(q) over [x, x + 2^L - 1], levels L = 0 .. qlevels-1, qst[s] + L V + voxel
+  const unsigned char* qst[2];
+  int qlevels;
   const float* dmap[2];          // K * V fp32 per side
   int K;
   double r, inv_r;
@@ -175,8 +179,12 @@ cudaError_t launch_distance_maps(const float* pts, const long long* off, int K, 
 cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, unsigned char* band,
                              cudaStream_t s);
 cudaError_t launch_pad_volume(const float* src, int nx, int ny, int nz, int pad, float* dst, cudaStream_t s);
-cudaError_t launch_own_records(const float* I, const unsigned char* band, long long V, uint2* out,
-                               cudaStream_t s);
+cudaError_t launch_own_records(const float* I, const unsigned char* band, const unsigned char* zr, long long V,
+                               uint2* out, cudaStream_t s);
+cudaError_t launch_quiet_table(const float* I, const unsigned char* band, const unsigned char* zr, int nx,
+                               long long V, int levels, unsigned char* table, cudaStream_t s);
+cudaError_t launch_zero_radius(const float* I, int nx, int ny, int nz, unsigned char* zr, unsigned char* m0,
+                               unsigned char* m1, cudaStream_t s);
 cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s);
 cudaError_t launch_raster(const EvalArgs& a, int grid, cudaStream_t s);
 int raster_blocks_per_sm(bool tex);

@@ -224,7 +224,18 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
   bool regular = true;
 #pragma unroll
   for (int k = 0; k < 4; k++) regular = regular && (G.ftype[k] == 1 || G.ftype[k] == -1);
-  G.flags = 1 | (inside ? 2 : 0) | (regular ? 4 : 0) | (inside_p ? 8 : 0);
+  // Empty-space radius (bits 8..15): an owned sample q maps to x = q + u(q) with u a
+  // convex combination of the vertex displacements, so |u_a| <= max_k |U_ka| / 1024 and
+  // every trilinear corner of x lies within Chebyshev distance R - 1 of q, R =
+  // ceil(max |U| / 1024) + 2.  If the other volume is zero on that box and I(q) = 0,
+  // h = 0 exactly (no contributing corner is > 0), whatever the position's rounding.
+  int maxU = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++)
+#pragma unroll
+    for (int a = 0; a < 3; a++) maxU = max(maxU, abs(G.U[k][a]));
+  const int skipR = min((maxU + 1023) / 1024 + 2, 255);
+  G.flags = 1 | (inside ? 2 : 0) | (regular ? 4 : 0) | (inside_p ? 8 : 0) | (skipR << 8);
 }
 
 // ---------------------------------------------------------------------------
@@ -501,7 +512,7 @@ struct WarpSmem {
   float4 row_b[32];  // (dz0, xl, y, z): fp32 displacement z at the row start, row start as floats
   float4 sc0, sc1;   // per-side sample constants (see Sample)
   int2 slices[32];   // non-empty z-slices of the current 32-slice chunk: (first row, ylo | slice << 16)
-  unsigned long long stat[3];  // samples, band entries, items of this warp (profiling)
+  unsigned long long stat[4];  // samples, band entries, items, skipped samples of this warp (profiling)
   // band-entry queue of the guidance term (a6): entries are evaluated 32 at a time
   float4 qa[kQueueCap];  // (u, v, fx, fy): footprint texel coordinates and weights
   int2 qb[kQueueCap];    // (fz bits, own linear index)
@@ -565,10 +576,30 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       const int y = (sl.y & 0xffff) + (r - sl.x);
       const bool rv = r < nrows;
       row_interval(R, y, z, rv, xl, xh);  // every lane (warp-collective)
-      const int len = rv ? max(0, xh - xl + 1) : 0;
+      const int len_all = rv ? max(0, xh - xl + 1) : 0;
+      // quiet rows (empty space): every voxel of the row is background
+      // with no band entry and the other volume is zero within the item's radius, so
+      // each sample's h is exactly 0 -- counted, not swept.  Range minimum of the
+      // quiet radii over [xl, xh] from the sparse table of the row (two byte loads).
+      int len = len_all;
+      if (F::kQuiet) {
+        const int L = len_all > 0 ? 31 - __clz(len_all) : 0;
+        const long long rl = (long long)(z * ny + y) * nx;
+        const long long a0 = len_all > 0 ? rl + xl : 0, a1 = len_all > 0 ? rl + xh - (1 << L) + 1 : 0;
+        const unsigned char* qt = f.quiet_table(L);
+        const int qm = min((int)__ldg(&qt[a0]), (int)__ldg(&qt[a1]));
+        if (len_all > 0 && qm >= f.quiet_radius()) {
+          len = 0;
+          f.quiet_row(rl + xl, len_all);
+        }
+      }
       const int incl = warp_incl_scan(len, lane);
       const int total = __shfl_sync(FULLMASK, incl, 31);
-      if (total == 0) continue;
+      const int tot_all = F::kQuiet ? (int)__reduce_add_sync(FULLMASK, (unsigned)len_all) : total;
+      if (total == 0) {
+        f.count_only(lane == 0 ? tot_all : 0);
+        continue;
+      }
       const unsigned ne = __ballot_sync(FULLMASK, len > 0);
       const int start = incl - len;
       __syncwarp();
@@ -593,7 +624,7 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
               "f"((float)y), "f"((float)z)
             : "memory");
       }
-      f.count_only(lane == 0 ? total : 0);
+      f.count_only(lane == 0 ? tot_all : 0);
       // Sweep in windows of 32 kStartWords samples.  The bitmap holds the row
       // starts of the window (bit s of word s/32); a lane's row is the number of
       // starts <= its sample index, minus one.  Past the end that is the last row
@@ -705,6 +736,7 @@ struct Acc {
   float gf;     // fp32 partial sum of guidance terms since the last flush (into g)
   int n, nb;    // samples, band entries
   int qn;       // band entries in the per-warp queue (warp-uniform)
+  int nq;       // samples of steps skipped as empty space (profiling)
 };
 
 template <bool TEX, int SIDE_T, bool CLAMP, bool DUMP>
@@ -831,6 +863,22 @@ struct Sample {
 
   __device__ __forceinline__ void count_only(int t) { acc.n += t; }
 
+  // quiet rows (raster): the side's sparse table of quiet radii, the item's radius
+  static constexpr bool kQuiet = true;
+  __device__ __forceinline__ const unsigned char* quiet_table(int L) const {
+    const int SIDE = SIDE_T >= 0 ? SIDE_T : side;
+    return (SIDE == 0 ? V.qst[0] : V.qst[1]) + (long long)L * V.V;
+  }
+  __device__ __forceinline__ int quiet_radius() const { return __float_as_int(sc1.w); }
+  __device__ __forceinline__ void quiet_row(long long q0, int n) {
+    acc.nq += n;
+    if (DUMP)
+      for (int i = 0; i < n; i++) {
+        dump_h[q0 + i] = 0.f;
+        dump_fg[q0 + i] = 0;
+      }
+  }
+
   __device__ __forceinline__ void flush_h() {
     acc.h += (double)acc.hf;
     acc.hf = 0.f;
@@ -860,7 +908,21 @@ struct Sample {
     MOREA_CHECK(!valid || (lin >= (long long)SIDE * V.V && lin < (long long)(SIDE + 1) * V.V));
     const uint2 own = __ldg(&V.own[0][lin]);  // lin = SIDE V + q
     const float a = __uint_as_float(own.x);
-    const unsigned bm = valid ? own.y : 0u;
+    const unsigned bm = valid ? (own.y & 0xffu) : 0u;
+    // empty-space skip (exact): I(q) = 0 and the other volume is zero within the
+    // item's radius (own.y bits 8..11: Chebyshev distance to its nearest non-zero
+    // voxel, 15 = at least 15) -> h = 0; a step where every lane is such a sample
+    // or past the end, and no lane has band entries, needs no gather
+    const bool quiet = !valid || (a == 0.f && (int)(own.y >> 8) >= __float_as_int(sc1.w));
+    if (__all_sync(FULLMASK, quiet && bm == 0u)) {
+      acc.nq += valid ? 1 : 0;
+      if (DUMP && valid) {
+        const long long q = (long long)lin - (long long)SIDE * V.V;
+        dump_h[q] = 0.f;
+        dump_fg[q] = 0;
+      }
+      return;
+    }
     const float kf = (float)k;
     const float4 s0 = sc0;
     const float dx = fmaf(s0.x, kf, __int_as_float(ra.z)), dy = fmaf(s0.y, kf, __int_as_float(ra.w)),
@@ -970,7 +1032,7 @@ __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int l
     S.sc0 = make_float4(R.A[0][0], R.A[1][0], R.A[2][0], 0.5f - R.eps[0]);
     // gather x of corner i0: I_o is volume o of texI (TEX), else a plain index + 1
     const float uoff = TEX ? fmaf((float)(1 - (SIDE_T >= 0 ? SIDE_T : side)), V.fnxp, V.uoff0) : 1.0f;
-    S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], uoff, 0.f);
+    S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], uoff, __int_as_float((R.flags >> 8) & 0xff));
   }
   __syncwarp();
   // O5 clamp only where a position can leave the range the gather covers exactly:
@@ -1055,7 +1117,7 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
   WarpSmem& S = smem[warp];
   const long long per_v = (long long)A.n_entries * A.P;
   const long long n_items = per_v * A.n_raster_versions;
-  if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0ull;
+  if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = S.stat[3] = 0ull;
   while (true) {
     unsigned long long item = 0;
     item = bq.claim(A.counter, lane, n_items, MOREA_CLAIM_CHUNK, MOREA_CLAIM_SPREAD);
@@ -1067,7 +1129,7 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
     const int e = A.sched[es];
     MOREA_CHECK(e >= 0 && e < A.n_entries && v < A.n_raster_versions);
     const long long i = ((long long)v * A.n_entries + e) * A.P + sol;
-    Acc acc{0.0, 0.0, 0.f, 0.f, 0, 0, 0};
+    Acc acc{0.0, 0.0, 0.f, 0.f, 0, 0, 0, 0};
     int n_side0 = 0;
 #pragma unroll 1
     for (int side = 0; side < 2; side++) {
@@ -1082,11 +1144,13 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
     out.n = warp_sum_i(acc.n);
     out.n0 = warp_sum_i(n_side0);
     const int nb = warp_sum_i(acc.nb);
+    const int nq = warp_sum_i(acc.nq);
     if (lane == 0) {
       A.hgn[i] = out;
       S.stat[0] += out.n;
       S.stat[1] += nb;
       S.stat[2] += 1;
+      S.stat[3] += nq;
       debug_count_item(A);
     }
   }
@@ -1095,6 +1159,7 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
     atomicAdd(&A.stats[0], S.stat[0]);
     atomicAdd(&A.stats[1], S.stat[1]);
     atomicAdd(&A.stats[2], S.stat[2]);
+    atomicAdd(&A.stats[3], S.stat[3]);
   }
 }
 
@@ -1325,6 +1390,10 @@ cudaError_t launch_check_folds(const MeshDev& m, const double sp[3], int P, cons
 struct OwnerSample {
   int* owner;
   int tet;
+  static constexpr bool kQuiet = false;
+  __device__ __forceinline__ const unsigned char* quiet_table(int) const { return nullptr; }
+  __device__ __forceinline__ int quiet_radius() const { return 1 << 30; }
+  __device__ __forceinline__ void quiet_row(long long, int) {}
   __device__ __forceinline__ void flush_h() {}
   __device__ __forceinline__ void count_only(int) {}
   __device__ __forceinline__ void sample(const int4& ra, const float4&, int k, bool valid) {
@@ -1449,12 +1518,89 @@ __global__ void k_band_mask(const float* __restrict__ dmap, int K, long long V, 
   }
 }
 
-// own-side record per voxel: (bits of I(q), band bits) -> one 8-byte load per sample
+// own-side record per voxel: (bits of I(q), band bits | zero radius << 8) -> one
+// 8-byte load per sample.  zr = Chebyshev distance from q to the nearest non-zero
+// voxel of the OTHER volume (boxes clipped to the image), 15 = at least 15.
 __global__ void k_own_records(const float* __restrict__ I, const unsigned char* __restrict__ band,
-                              long long V, uint2* __restrict__ out) {
+                              const unsigned char* __restrict__ zr, long long V, uint2* __restrict__ out) {
   for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
        v += (long long)gridDim.x * blockDim.x)
-    out[v] = make_uint2(__float_as_uint(I[v]), band ? (unsigned)band[v] : 0u);
+    out[v] = make_uint2(__float_as_uint(I[v]), (band ? (unsigned)band[v] : 0u) | ((unsigned)zr[v] << 8));
+}
+
+// zero radius of a volume by dilation: m = [I != 0], then per radius r = 1..15
+// m = max over the 3x3x3 neighbourhood (one axis at a time), zr = the first r with m
+__global__ void k_zr_init(const float* __restrict__ I, long long V, unsigned char* __restrict__ m,
+                          unsigned char* __restrict__ zr) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
+       v += (long long)gridDim.x * blockDim.x) {
+    const bool nz = I[v] != 0.0f;
+    m[v] = nz ? 1 : 0;
+    zr[v] = nz ? 0 : 15;
+  }
+}
+
+__global__ void k_zr_dilate(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, int nx,
+                            int ny, int nz, int axis) {
+  const long long V = (long long)nx * ny * nz;
+  const long long st = axis == 0 ? 1 : (axis == 1 ? nx : (long long)nx * ny);
+  const int n = axis == 0 ? nx : (axis == 1 ? ny : nz);
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
+       v += (long long)gridDim.x * blockDim.x) {
+    const int c = axis == 0 ? (int)(v % nx) : (axis == 1 ? (int)((v / nx) % ny) : (int)(v / ((long long)nx * ny)));
+    unsigned char x = src[v];
+    if (c > 0) x |= src[v - st];
+    if (c < n - 1) x |= src[v + st];
+    dst[v] = x;
+  }
+}
+
+__global__ void k_zr_update(const unsigned char* __restrict__ m, long long V, int r, unsigned char* __restrict__ zr) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
+       v += (long long)gridDim.x * blockDim.x)
+    if (m[v] && zr[v] > r) zr[v] = (unsigned char)r;
+}
+
+// quiet radius of a voxel of one side: 0 unless I(q) = 0 and q has no band entry, else
+// the zero radius of the other volume; level 0 of the side's x sparse table
+__global__ void k_quiet_level0(const float* __restrict__ I, const unsigned char* __restrict__ band,
+                               const unsigned char* __restrict__ zr, long long V, unsigned char* __restrict__ q) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
+       v += (long long)gridDim.x * blockDim.x)
+    q[v] = (I[v] != 0.0f || (band && band[v])) ? 0 : zr[v];
+}
+
+// level L from level L-1: min over [x, x + 2^L - 1] clipped to the row
+__global__ void k_quiet_level(const unsigned char* __restrict__ prev, unsigned char* __restrict__ next, int nx,
+                              long long V, int half) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
+       v += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(v % nx);
+    const unsigned char a = prev[v];
+    next[v] = x + half < nx ? min(a, prev[v + half]) : a;
+  }
+}
+
+cudaError_t launch_quiet_table(const float* I, const unsigned char* band, const unsigned char* zr, int nx,
+                               long long V, int levels, unsigned char* table, cudaStream_t s) {
+  k_quiet_level0<<<2048, 256, 0, s>>>(I, band, zr, V, table);
+  for (int L = 1; L < levels; L++)
+    k_quiet_level<<<2048, 256, 0, s>>>(table + (long long)(L - 1) * V, table + (long long)L * V, nx, V, 1 << (L - 1));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zero_radius(const float* I, int nx, int ny, int nz, unsigned char* zr, unsigned char* m0,
+                               unsigned char* m1, cudaStream_t s) {
+  const long long V = (long long)nx * ny * nz;
+  k_zr_init<<<2048, 256, 0, s>>>(I, V, m0, zr);
+  for (int r = 1; r < 15; r++) {
+    k_zr_dilate<<<2048, 256, 0, s>>>(m0, m1, nx, ny, nz, 0);
+    k_zr_dilate<<<2048, 256, 0, s>>>(m1, m0, nx, ny, nz, 1);
+    k_zr_dilate<<<2048, 256, 0, s>>>(m0, m1, nx, ny, nz, 2);
+    k_zr_update<<<2048, 256, 0, s>>>(m1, V, r, zr);
+    unsigned char* t = m0; m0 = m1; m1 = t;
+  }
+  return cudaGetLastError();
 }
 
 // edge-padded copy of one volume for the gather textures (Volumes::texI):
@@ -1474,9 +1620,9 @@ cudaError_t launch_pad_volume(const float* src, int nx, int ny, int nz, int pad,
   return cudaGetLastError();
 }
 
-cudaError_t launch_own_records(const float* I, const unsigned char* band, long long V, uint2* out,
-                               cudaStream_t s) {
-  k_own_records<<<2048, 256, 0, s>>>(I, band, V, out);
+cudaError_t launch_own_records(const float* I, const unsigned char* band, const unsigned char* zr, long long V,
+                               uint2* out, cudaStream_t s) {
+  k_own_records<<<2048, 256, 0, s>>>(I, band, zr, V, out);
   return cudaGetLastError();
 }
 

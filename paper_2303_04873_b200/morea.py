@@ -356,7 +356,7 @@ class Context:
                                          ctypes.byref(sa), ctypes.byref(ba), ctypes.byref(it),
                                          ctypes.byref(stp)))
         return dict(launches=la.value, ms=ms.value, samples=sa.value, band_entries=ba.value,
-                    items=it.value, steps=stp.value)
+                    items=it.value, skipped=stp.value)
 
 
 # ---------------------------------------------------------------------------- helpers

@@ -32,7 +32,9 @@ def t(fn, reps):
     return a.elapsed_time(b) / reps
 full = t(lambda: ctx.eval_full(off, obj, acc, tc), 3 if os.environ.get("AB_SOBOL") else 5)
 part = t(lambda: ctx.eval_partial(off, acc, go, ch, nvd, tc, pobj, pacc), 5)
-print(json.dumps({"full_ms": full, "partial_ms": part, "h0": float(acc[1, 0].item())}))
+import hashlib
+dig = hashlib.sha1(obj.cpu().numpy().tobytes() + acc.cpu().numpy().tobytes() + pobj.cpu().numpy().tobytes() + pacc.cpu().numpy().tobytes()).hexdigest()[:12]
+print(json.dumps({"full_ms": full, "partial_ms": part, "h0": float(acc[1, 0].item()), "digest": dig}))
 '''
 
 def main():
