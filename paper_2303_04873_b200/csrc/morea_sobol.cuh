@@ -88,8 +88,56 @@ __device__ __noinline__ void exact_sobol(const SobolRec& R, const unsigned xm[4]
 // ---------------------------------------------------------------------------
 struct SobolWarp {
   SobolRec R;
-  unsigned long long stat[3];
+  unsigned long long stat[4];
 };
+
+// Empty space, one side of an item: true when every voxel a point
+// of the tet or its image can read is quiet -- background (I = 0) with no band entry
+// on this side, and the other volume zero within Chebyshev radius Rq - 1.  The points
+// lie in the bbox of the side's vertices and read the corners of their cells, so the
+// box [floor(min) - 1, floor(max) + 2] covers every own footprint (and the cells the
+// guidance prefilter reads).  An image is T(p) = p + sum_k l_k U_k with |U_k| <= m
+// (Chebyshev), so its cell corners lie within 1 + m + 1 of any own corner of p's cell,
+// plus rounding: Rq = ceil(m) + 3.  Then a = b = 0 and every distance is >= r at every
+// point, so h = g = 0 for all N points, exactly.  Range minima along x of the side's
+// quiet table (two byte loads per row of the box), early exit on the first miss.
+__device__ __forceinline__ bool sobol_quiet(const SobolRec& R, const Volumes& V, int side, int lane) {
+  const unsigned char* qt = side == 0 ? V.qst[0] : V.qst[1];
+  if (!qt) return false;
+  const int dims[3] = {V.nx, V.ny, V.nz};
+  int lo[3], hi[3], mU = 0;
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    int qmin = R.Q[0][a], qmax = R.Q[0][a];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      qmin = min(qmin, R.Q[k][a]);
+      qmax = max(qmax, R.Q[k][a]);
+      mU = max(mU, abs(R.Qo[k][a] - R.Q[k][a]));
+    }
+    lo[a] = max((qmin >> 10) - 1, 0);
+    hi[a] = min((qmax >> 10) + 2, dims[a] - 1);
+    if (lo[a] > hi[a]) return false;
+  }
+  const int Rq = (mU + 1023) / 1024 + 3;
+  if (Rq > 15) return false;  // beyond the zero radius the maps carry
+  const int len = hi[0] - lo[0] + 1;
+  const int L = 31 - __clz(len);
+  const unsigned char* t = qt + (long long)L * V.V;
+  const int nyb = hi[1] - lo[1] + 1;
+  const int nrows = nyb * (hi[2] - lo[2] + 1);
+  for (int r0 = 0; r0 < nrows; r0 += 32) {
+    const int r = r0 + lane;
+    bool miss = false;
+    if (r < nrows) {
+      const int z = lo[2] + r / nyb, y = lo[1] + r % nyb;
+      const long long row = ((long long)z * V.ny + y) * V.nx;
+      miss = min(__ldg(&t[row + lo[0]]), __ldg(&t[row + hi[0] - (1 << L) + 1])) < Rq;
+    }
+    if (__any_sync(FULLMASK, miss)) return false;
+  }
+  return true;
+}
 
 __device__ __forceinline__ float sb_plerp(float a, float b, float t, float omt) {
   return fmaf(t, b, omt * a);  // positivity-exact lerp (see plerp)
@@ -225,7 +273,7 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
   }
   const long long per_v = (long long)A.n_entries * A.P;
   const long long n_items = per_v * A.n_raster_versions;
-  if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0ull;
+  if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = S.stat[3] = 0ull;
   while (true) {
     const unsigned long long item = bq.claim(A.counter, lane, n_items, MOREA_CLAIM_CHUNK, MOREA_CLAIM_SPREAD);
     if ((long long)item >= n_items) break;
@@ -252,6 +300,12 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
       const long long N = R.N;
       n_tot += N;
       if (side == 0) n_side0 = N;
+      // empty space: h = g = 0 for every point (counted, not sampled); the fp64
+      // test hook keeps every side on the sampling path
+      if (!A.sobol_force_exact && sobol_quiet(R, V, side, lane)) {
+        if (lane == 0) S.stat[3] += N;
+        continue;
+      }
       // O5 clamp only where a position can leave the range the gathers cover
       // exactly: [0, n-1] vertices for plain loads, (-1, n) (bit 2) on the
       // edge-padded textures; warp-uniform, so the common path skips the clamp
@@ -376,6 +430,7 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
     atomicAdd(&A.stats[0], S.stat[0]);
     atomicAdd(&A.stats[1], S.stat[1]);
     atomicAdd(&A.stats[2], S.stat[2]);
+    atomicAdd(&A.stats[3], S.stat[3]);
   }
 }
 

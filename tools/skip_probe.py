@@ -27,3 +27,7 @@ p = ctx.prof_read()
 for name, d in (("full", f), ("partial", p)):
     print(name, "samples", d["samples"], "skipped frac", d["skipped"] / d["samples"], "band/sample",
           d["band_entries"] / d["samples"], "ms", d["ms"])
+ctx.set_sampler(morea.SAMPLER_SOBOL, 1.0)
+ctx.eval_full(off, obj, acc, tc)
+s = ctx.prof_read()
+print("sobol full", "samples", s["samples"], "skipped frac", s["skipped"] / max(s["samples"], 1), "ms", s["ms"])
