@@ -610,7 +610,7 @@ def main():
                 "mix_class_evals_per_s": _fin(P * Gs[0] * 1e3 / t_mix),
                 "mix_class_accept_frac": _fin(mix_accept_frac),
                 "samples_per_launch": prof["samples"] / max(prof["launches"], 1),
-                "empty_space_skipped_frac": (prof["skipped"] / prof["samples"]) if prof["samples"] else None,
+                "quiet_row_sample_frac": (prof["skipped"] / prof["samples"]) if prof["samples"] else None,
                 "band_entries_per_launch": prof["band_entries"] / max(prof["launches"], 1),
                 "partial_fos_sweep": sweep,
                 "plain_load_full_evals_per_s": _fin(P * 1e3 / t_plain),

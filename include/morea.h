@@ -318,9 +318,11 @@ int morea_distance_map(morea_ctx *ctx, int side, int pair, float *out);
  * the rasterize/evaluate kernel is bracketed by CUDA events on the context
  * stream and its algorithmic work is counted.  morea_prof_read synchronises
  * and returns: launches, summed kernel milliseconds, sampled voxels, band
- * entries, (tet, solution) items, and the sampled voxels whose 32-sample step
- * was skipped as empty space (background on both sides, no band entry: h = 0
- * exactly, no gather).  Reading resets the counters. */
+ * entries, (tet, solution) items, and the samples counted without being
+ * swept: voxel sampler, those of quiet rows (every voxel background with no
+ * band entry and the other volume zero within the item's reach: h = g = 0
+ * exactly); Sobol sampler, the points of quiet item sides.
+ * Reading resets the counters. */
 int morea_prof_enable(morea_ctx *ctx, int on);
 /* Number of kernels this context has launched since it was created. */
 int64_t morea_kernel_launches(const morea_ctx *ctx);

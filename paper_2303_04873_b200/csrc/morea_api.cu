@@ -840,8 +840,8 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
     for (int s = 0; s < 2; s++) {
       CK(launch_zero_radius(ctx->I[1 - s].as<float>(), nx, ny, nz, zr.as<unsigned char>(), m0.as<unsigned char>(),
                             m1.as<unsigned char>(), ctx->stream));
-      CK(launch_own_records(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr,
-                            zr.as<unsigned char>(), V, ctx->own.as<uint2>() + (size_t)s * V, ctx->stream));
+      CK(launch_own_records(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr, V,
+                            ctx->own.as<uint2>() + (size_t)s * V, ctx->stream));
       CK(launch_quiet_table(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr,
                             zr.as<unsigned char>(), nx, V, levels,
                             ctx->qst.as<unsigned char>() + (size_t)s * levels * V, ctx->stream));

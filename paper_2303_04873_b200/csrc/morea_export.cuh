@@ -23,7 +23,7 @@ struct LabelSample {
   static constexpr bool kQuiet = false;
   __device__ __forceinline__ const unsigned char* quiet_table(int) const { return nullptr; }
   __device__ __forceinline__ int quiet_radius() const { return 1 << 30; }
-  __device__ __forceinline__ void quiet_row(long long, int) {}
+  __device__ __forceinline__ void quiet_row(int, int) {}
   const unsigned char* masks;
   int M;
   int* cnt;  // shared: M + 1 counters of this warp
@@ -59,7 +59,7 @@ struct MinOwnerSample {
   static constexpr bool kQuiet = false;
   __device__ __forceinline__ const unsigned char* quiet_table(int) const { return nullptr; }
   __device__ __forceinline__ int quiet_radius() const { return 1 << 30; }
-  __device__ __forceinline__ void quiet_row(long long, int) {}
+  __device__ __forceinline__ void quiet_row(int, int) {}
   int* owner;
   int tet;
   __device__ __forceinline__ void flush_h() {}
@@ -75,7 +75,7 @@ struct DvfSample {
   static constexpr bool kQuiet = false;
   __device__ __forceinline__ const unsigned char* quiet_table(int) const { return nullptr; }
   __device__ __forceinline__ int quiet_radius() const { return 1 << 30; }
-  __device__ __forceinline__ void quiet_row(long long, int) {}
+  __device__ __forceinline__ void quiet_row(int, int) {}
   const SideRec* R;  // shared
   const int* owner;
   int tet;

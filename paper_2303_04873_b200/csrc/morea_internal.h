@@ -92,7 +92,7 @@ struct Volumes {
   double sp[3];
   const float* I[2];
   const unsigned char* band[2];  // per voxel bit i = [D_i(q) < r]; nullptr when K == 0
-  // per voxel (bits of I_side(q), band bits | zero radius << 8): one 8-byte load; one allocation,
+  // per voxel (bits of I_side(q), band bits): one 8-byte load; one allocation,
   // own[1] = own[0] + V, so side s of voxel q is own[0][s V + q]
   const uint2* own[2];
   // quiet radii (empty space): per side, sparse table along x of
@@ -179,7 +179,7 @@ cudaError_t launch_distance_maps(const float* pts, const long long* off, int K, 
 cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, unsigned char* band,
                              cudaStream_t s);
 cudaError_t launch_pad_volume(const float* src, int nx, int ny, int nz, int pad, float* dst, cudaStream_t s);
-cudaError_t launch_own_records(const float* I, const unsigned char* band, const unsigned char* zr, long long V,
+cudaError_t launch_own_records(const float* I, const unsigned char* band, long long V,
                                uint2* out, cudaStream_t s);
 cudaError_t launch_quiet_table(const float* I, const unsigned char* band, const unsigned char* zr, int nx,
                                long long V, int levels, unsigned char* table, cudaStream_t s);

@@ -584,8 +584,8 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       int len = len_all;
       if (F::kQuiet) {
         const int L = len_all > 0 ? 31 - __clz(len_all) : 0;
-        const long long rl = (long long)(z * ny + y) * nx;
-        const long long a0 = len_all > 0 ? rl + xl : 0, a1 = len_all > 0 ? rl + xh - (1 << L) + 1 : 0;
+        const int rl = (z * ny + y) * nx;  // 2 V < 2^31 (the own-record index is an int)
+        const int a0 = len_all > 0 ? rl + xl : 0, a1 = len_all > 0 ? rl + xh - (1 << L) + 1 : 0;
         const unsigned char* qt = f.quiet_table(L);
         const int qm = min((int)__ldg(&qt[a0]), (int)__ldg(&qt[a1]));
         if (len_all > 0 && qm >= f.quiet_radius()) {
@@ -736,7 +736,7 @@ struct Acc {
   float gf;     // fp32 partial sum of guidance terms since the last flush (into g)
   int n, nb;    // samples, band entries
   int qn;       // band entries in the per-warp queue (warp-uniform)
-  int nq;       // samples of steps skipped as empty space (profiling)
+  int nq;       // samples of quiet rows (empty space, counted not swept; profiling)
 };
 
 template <bool TEX, int SIDE_T, bool CLAMP, bool DUMP>
@@ -777,6 +777,12 @@ struct Sample {
     }
   }
 
+  __device__ __forceinline__ static float tri(const float c[8], float fx, float fy, float fz,
+                                              float gx, float gy, float gz) {
+    return plerp(plerp(plerp(c[0], c[1], fx, gx), plerp(c[2], c[3], fx, gx), fy, gy),
+                 plerp(plerp(c[4], c[5], fx, gx), plerp(c[6], c[7], fx, gx), fy, gy), fz, gz);
+  }
+
   // tld4 pair (slices i0_z and i0_z + 1); u carries the volume's x offset
   __device__ __forceinline__ void gather_tex(float u, float v, float c[8]) const {
     const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)V.texI, u, v, 0);
@@ -784,12 +790,6 @@ struct Sample {
     // gather order: (x0,y1) (x1,y1) (x1,y0) (x0,y0)
     c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
     c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
-  }
-
-  __device__ __forceinline__ static float tri(const float c[8], float fx, float fy, float fz,
-                                              float gx, float gy, float gz) {
-    return plerp(plerp(plerp(c[0], c[1], fx, gx), plerp(c[2], c[3], fx, gx), fy, gy),
-                 plerp(plerp(c[4], c[5], fx, gx), plerp(c[6], c[7], fx, gx), fy, gy), fz, gz);
   }
 
   // guidance term of one band entry (a6, O8): pair i of the side-s sample with
@@ -870,7 +870,7 @@ struct Sample {
     return (SIDE == 0 ? V.qst[0] : V.qst[1]) + (long long)L * V.V;
   }
   __device__ __forceinline__ int quiet_radius() const { return __float_as_int(sc1.w); }
-  __device__ __forceinline__ void quiet_row(long long q0, int n) {
+  __device__ __forceinline__ void quiet_row(int q0, int n) {
     acc.nq += n;
     if (DUMP)
       for (int i = 0; i < n; i++) {
@@ -909,20 +909,6 @@ struct Sample {
     const uint2 own = __ldg(&V.own[0][lin]);  // lin = SIDE V + q
     const float a = __uint_as_float(own.x);
     const unsigned bm = valid ? (own.y & 0xffu) : 0u;
-    // empty-space skip (exact): I(q) = 0 and the other volume is zero within the
-    // item's radius (own.y bits 8..11: Chebyshev distance to its nearest non-zero
-    // voxel, 15 = at least 15) -> h = 0; a step where every lane is such a sample
-    // or past the end, and no lane has band entries, needs no gather
-    const bool quiet = !valid || (a == 0.f && (int)(own.y >> 8) >= __float_as_int(sc1.w));
-    if (__all_sync(FULLMASK, quiet && bm == 0u)) {
-      acc.nq += valid ? 1 : 0;
-      if (DUMP && valid) {
-        const long long q = (long long)lin - (long long)SIDE * V.V;
-        dump_h[q] = 0.f;
-        dump_fg[q] = 0;
-      }
-      return;
-    }
     const float kf = (float)k;
     const float4 s0 = sc0;
     const float dx = fmaf(s0.x, kf, __int_as_float(ra.z)), dy = fmaf(s0.y, kf, __int_as_float(ra.w)),
@@ -1393,7 +1379,7 @@ struct OwnerSample {
   static constexpr bool kQuiet = false;
   __device__ __forceinline__ const unsigned char* quiet_table(int) const { return nullptr; }
   __device__ __forceinline__ int quiet_radius() const { return 1 << 30; }
-  __device__ __forceinline__ void quiet_row(long long, int) {}
+  __device__ __forceinline__ void quiet_row(int, int) {}
   __device__ __forceinline__ void flush_h() {}
   __device__ __forceinline__ void count_only(int) {}
   __device__ __forceinline__ void sample(const int4& ra, const float4&, int k, bool valid) {
@@ -1518,14 +1504,12 @@ __global__ void k_band_mask(const float* __restrict__ dmap, int K, long long V, 
   }
 }
 
-// own-side record per voxel: (bits of I(q), band bits | zero radius << 8) -> one
-// 8-byte load per sample.  zr = Chebyshev distance from q to the nearest non-zero
-// voxel of the OTHER volume (boxes clipped to the image), 15 = at least 15.
-__global__ void k_own_records(const float* __restrict__ I, const unsigned char* __restrict__ band,
-                              const unsigned char* __restrict__ zr, long long V, uint2* __restrict__ out) {
+// own-side record per voxel: (bits of I(q), band bits) -> one 8-byte load per sample
+__global__ void k_own_records(const float* __restrict__ I, const unsigned char* __restrict__ band, long long V,
+                              uint2* __restrict__ out) {
   for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
        v += (long long)gridDim.x * blockDim.x)
-    out[v] = make_uint2(__float_as_uint(I[v]), (band ? (unsigned)band[v] : 0u) | ((unsigned)zr[v] << 8));
+    out[v] = make_uint2(__float_as_uint(I[v]), band ? (unsigned)band[v] : 0u);
 }
 
 // zero radius of a volume by dilation: m = [I != 0], then per radius r = 1..15
@@ -1562,7 +1546,9 @@ __global__ void k_zr_update(const unsigned char* __restrict__ m, long long V, in
 }
 
 // quiet radius of a voxel of one side: 0 unless I(q) = 0 and q has no band entry, else
-// the zero radius of the other volume; level 0 of the side's x sparse table
+// zr = the zero radius of the other volume (Chebyshev distance from q to its nearest
+// non-zero voxel, boxes clipped to the image, 15 = at least 15); level 0 of the
+// side's x sparse table
 __global__ void k_quiet_level0(const float* __restrict__ I, const unsigned char* __restrict__ band,
                                const unsigned char* __restrict__ zr, long long V, unsigned char* __restrict__ q) {
   for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
@@ -1620,9 +1606,9 @@ cudaError_t launch_pad_volume(const float* src, int nx, int ny, int nz, int pad,
   return cudaGetLastError();
 }
 
-cudaError_t launch_own_records(const float* I, const unsigned char* band, const unsigned char* zr, long long V,
+cudaError_t launch_own_records(const float* I, const unsigned char* band, long long V,
                                uint2* out, cudaStream_t s) {
-  k_own_records<<<2048, 256, 0, s>>>(I, band, zr, V, out);
+  k_own_records<<<2048, 256, 0, s>>>(I, band, V, out);
   return cudaGetLastError();
 }
 
