@@ -217,14 +217,20 @@ template <bool TEX>
 __device__ __forceinline__ float sb_trilinear(const Volumes& V, unsigned long long tex,
                                               const float* __restrict__ vol, float uoff,
                                               const SbPos& P) {
-  float c[8];
+  const float gx = 1.f - P.fx, gy = 1.f - P.fy, gz = 1.f - P.fz;
   if (TEX) {
+    // gather order (x0y1, x1y1, x1y0, x0y0); z first in packed fp32x2 on the aligned
+    // pairs .xy / .zw, then y, then x (positivity-exact lerps, like k_raster)
     const float u = P.ix + uoff, v = fmaf(P.iz, V.fnyp, P.iy) + V.voff;
     const float4 g0 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v, 0);
     const float4 g1 = tex2Dgather<float4>((cudaTextureObject_t)tex, u, v + V.fnyp, 0);
-    c[0] = g0.w; c[1] = g0.z; c[2] = g0.x; c[3] = g0.y;
-    c[4] = g1.w; c[5] = g1.z; c[6] = g1.x; c[7] = g1.y;
-  } else {
+    const float2 tz = make_float2(P.fz, P.fz), oz = make_float2(gz, gz);
+    const float2 y1 = __ffma2_rn(tz, make_float2(g1.x, g1.y), __fmul2_rn(oz, make_float2(g0.x, g0.y)));
+    const float2 y0 = __ffma2_rn(tz, make_float2(g1.z, g1.w), __fmul2_rn(oz, make_float2(g0.z, g0.w)));
+    return sb_plerp(sb_plerp(y0.y, y1.x, P.fy, gy), sb_plerp(y0.x, y1.y, P.fy, gy), P.fx, gx);
+  }
+  float c[8];
+  {
     // plain loads; the corner indices are clamped into the volume (only ambiguous
     // samples at the border can ask for index -1 or n, with weight ~0)
     const int x0 = min(max((int)P.ix, 0), V.nx - 2), y0 = min(max((int)P.iy, 0), V.ny - 2),
@@ -234,7 +240,6 @@ __device__ __forceinline__ float sb_trilinear(const Volumes& V, unsigned long lo
     c[0] = __ldg(b); c[1] = __ldg(b + 1); c[2] = __ldg(b + sy); c[3] = __ldg(b + sy + 1);
     c[4] = __ldg(b + sz); c[5] = __ldg(b + sz + 1); c[6] = __ldg(b + sz + sy); c[7] = __ldg(b + sz + sy + 1);
   }
-  const float gx = 1.f - P.fx, gy = 1.f - P.fy, gz = 1.f - P.fz;
   return sb_plerp(sb_plerp(sb_plerp(c[0], c[1], P.fx, gx), sb_plerp(c[2], c[3], P.fx, gx), P.fy, gy),
                   sb_plerp(sb_plerp(c[4], c[5], P.fx, gx), sb_plerp(c[6], c[7], P.fx, gx), P.fy, gy),
                   P.fz, gz);
