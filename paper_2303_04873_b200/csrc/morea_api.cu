@@ -106,8 +106,7 @@ struct morea_ctx {
   double sp[3] = {1, 1, 1};
   double r = 0;
   double w[2][kMaxPairs] = {};
-  DevBuf I[2], band[2], dmap[2], wts, own, qst;
-  int qlevels = 0;
+  DevBuf I[2], band[2], dmap[2], wts, own, qhull;
   // Sobol sampler (NEXT-1): mode, rate, dilated band masks (2 V bytes), direction numbers
   int sampler = MOREA_SAMPLER_VOXEL;
   double rate = 1.0;
@@ -301,8 +300,8 @@ Volumes volumes_of(const morea_ctx* c) {
   v.rf = (float)c->r;
   v.rlo = (float)(c->r - (double)v.rf);
   for (int s = 0; s < 2; s++)
-    v.qst[s] = c->qst.p ? c->qst.as<unsigned char>() + (size_t)s * c->qlevels * c->V : nullptr;
-  v.qlevels = c->qlevels;
+    v.qhull[s] = c->qhull.p ? c->qhull.as<short2>() + (size_t)s * (kQuietRmax - kQuietRmin + 1) * c->ny * c->nz
+                            : nullptr;
   v.own[0] = c->own.as<uint2>();
   v.own[1] = v.own[0] ? v.own[0] + c->V : nullptr;
   v.use_tex = c->use_tex ? 1 : 0;
@@ -729,7 +728,7 @@ void morea_destroy(morea_ctx* ctx) {
     cudaEventDestroy(p.second);
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
-                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->qst, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->st_masks, &ctx->st_counts, &ctx->st_dvf, &ctx->st_cov,
+                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->qhull, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->st_masks, &ctx->st_counts, &ctx->st_dvf, &ctx->st_cov,
                     &ctx->scratch_owner, &ctx->zero_off, &ctx->mx_off, &ctx->mx_acc,
                     &ctx->mx_obj, &ctx->mx_cache, &ctx->mx_nv, &ctx->mx_pobj, &ctx->mx_pacc, &ctx->mx_dep,
                     &ctx->mx_base, &ctx->mx_accepted, &ctx->mx_cluster, &ctx->mx_mu, &ctx->mx_L, &ctx->mx_arch,
@@ -833,18 +832,15 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
     CK(zr.ensure(V));
     CK(m0.ensure(V));
     CK(m1.ensure(V));
-    int levels = 1;
-    while ((2 << (levels - 1)) <= nx) levels++;  // 2^(levels-1) <= nx < 2^levels
-    ctx->qlevels = levels;
-    CK(ctx->qst.ensure((size_t)2 * levels * V));
+    const size_t nh = (size_t)(kQuietRmax - kQuietRmin + 1) * ny * nz;
+    CK(ctx->qhull.ensure(2 * nh * sizeof(short2)));
     for (int s = 0; s < 2; s++) {
       CK(launch_zero_radius(ctx->I[1 - s].as<float>(), nx, ny, nz, zr.as<unsigned char>(), m0.as<unsigned char>(),
                             m1.as<unsigned char>(), ctx->stream));
       CK(launch_own_records(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr, V,
                             ctx->own.as<uint2>() + (size_t)s * V, ctx->stream));
-      CK(launch_quiet_table(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr,
-                            zr.as<unsigned char>(), nx, V, levels,
-                            ctx->qst.as<unsigned char>() + (size_t)s * levels * V, ctx->stream));
+      CK(launch_quiet_hull(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr,
+                           zr.as<unsigned char>(), nx, ny, nz, ctx->qhull.as<short2>() + (size_t)s * nh, ctx->stream));
     }
     CK(cudaStreamSynchronize(ctx->stream));
   }

@@ -24,6 +24,7 @@ constexpr int kMaxPairs = 8;
 constexpr int kTexPad = 1;  // edge-replicated border of the gather textures (voxels)
 constexpr int kQLo = -256 * 1024;  // Q.10 window (O1)
 constexpr int kQHi = 768 * 1024;
+constexpr int kQuietRmin = 2, kQuietRmax = 15;  // radii of the empty-space row hulls (§4.10)
 constexpr int kWarpsPerBlock = 2;  // k_owner_map / export blocks (one WarpSmem per warp)
 constexpr int kRasterThreads = 32 * kWarpsPerBlock;
 
@@ -95,10 +96,10 @@ struct Volumes {
   // per voxel (bits of I_side(q), band bits): one 8-byte load; one allocation,
   // own[1] = own[0] + V, so side s of voxel q is own[0][s V + q]
   const uint2* own[2];
-  // quiet radii (empty space): per side, sparse table along x of
-  // min(q) over [x, x + 2^L - 1], levels L = 0 .. qlevels-1, qst[s] + L V + voxel
-  const unsigned char* qst[2];
-  int qlevels;
+  // empty space: per side, radius R in [kQuietRmin, kQuietRmax] and
+  // image row (y, z), the first and last x whose quiet radius is < R ((nx, -1): none);
+  // qhull[s] + (R - kQuietRmin) ny nz + z ny + y
+  const short2* qhull[2];
   const float* dmap[2];          // K * V fp32 per side
   int K;
   double r, inv_r;
@@ -181,8 +182,8 @@ cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, un
 cudaError_t launch_pad_volume(const float* src, int nx, int ny, int nz, int pad, float* dst, cudaStream_t s);
 cudaError_t launch_own_records(const float* I, const unsigned char* band, long long V,
                                uint2* out, cudaStream_t s);
-cudaError_t launch_quiet_table(const float* I, const unsigned char* band, const unsigned char* zr, int nx,
-                               long long V, int levels, unsigned char* table, cudaStream_t s);
+cudaError_t launch_quiet_hull(const float* I, const unsigned char* band, const unsigned char* zr, int nx, int ny,
+                              int nz, short2* hull, cudaStream_t s);
 cudaError_t launch_zero_radius(const float* I, int nx, int ny, int nz, unsigned char* zr, unsigned char* m0,
                                unsigned char* m1, cudaStream_t s);
 cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s);

@@ -583,14 +583,13 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       // quiet radii over [xl, xh] from the sparse table of the row (two byte loads).
       int len = len_all;
       if (F::kQuiet) {
-        const int L = len_all > 0 ? 31 - __clz(len_all) : 0;
-        const int rl = (z * ny + y) * nx;  // 2 V < 2^31 (the own-record index is an int)
-        const int a0 = len_all > 0 ? rl + xl : 0, a1 = len_all > 0 ? rl + xh - (1 << L) + 1 : 0;
-        const unsigned char* qt = f.quiet_table(L);
-        const int qm = min((int)__ldg(&qt[a0]), (int)__ldg(&qt[a1]));
-        if (len_all > 0 && qm >= f.quiet_radius()) {
-          len = 0;
-          f.quiet_row(rl + xl, len_all);
+        const short2* qh = f.quiet_hull();  // item-uniform; nullptr: radius beyond the hulls
+        if (qh) {
+          const short2 hb = rv ? __ldg(&qh[z * ny + y]) : make_short2(0, -1);
+          if (len_all > 0 && (xh < hb.x || xl > hb.y)) {
+            len = 0;
+            f.quiet_row((z * ny + y) * nx + xl, len_all);  // 2 V < 2^31 (own-record index is an int)
+          }
         }
       }
       const int incl = warp_incl_scan(len, lane);
@@ -863,13 +862,14 @@ struct Sample {
 
   __device__ __forceinline__ void count_only(int t) { acc.n += t; }
 
-  // quiet rows (raster): the side's sparse table of quiet radii, the item's radius
+  // quiet rows (raster): the side's row hulls at the item's radius R (SideRec flags)
   static constexpr bool kQuiet = true;
-  __device__ __forceinline__ const unsigned char* quiet_table(int L) const {
+  __device__ __forceinline__ const short2* quiet_hull() const {
     const int SIDE = SIDE_T >= 0 ? SIDE_T : side;
-    return (SIDE == 0 ? V.qst[0] : V.qst[1]) + (long long)L * V.V;
+    const int R = __float_as_int(sc1.w);
+    const short2* h = SIDE == 0 ? V.qhull[0] : V.qhull[1];
+    return (h && R <= kQuietRmax) ? h + (R - kQuietRmin) * V.ny * V.nz : nullptr;
   }
-  __device__ __forceinline__ int quiet_radius() const { return __float_as_int(sc1.w); }
   __device__ __forceinline__ void quiet_row(int q0, int n) {
     acc.nq += n;
     if (DUMP)
@@ -1377,8 +1377,7 @@ struct OwnerSample {
   int* owner;
   int tet;
   static constexpr bool kQuiet = false;
-  __device__ __forceinline__ const unsigned char* quiet_table(int) const { return nullptr; }
-  __device__ __forceinline__ int quiet_radius() const { return 1 << 30; }
+  __device__ __forceinline__ const short2* quiet_hull() const { return nullptr; }
   __device__ __forceinline__ void quiet_row(int, int) {}
   __device__ __forceinline__ void flush_h() {}
   __device__ __forceinline__ void count_only(int) {}
@@ -1545,33 +1544,36 @@ __global__ void k_zr_update(const unsigned char* __restrict__ m, long long V, in
     if (m[v] && zr[v] > r) zr[v] = (unsigned char)r;
 }
 
-// quiet radius of a voxel of one side: 0 unless I(q) = 0 and q has no band entry, else
-// zr = the zero radius of the other volume (Chebyshev distance from q to its nearest
-// non-zero voxel, boxes clipped to the image, 15 = at least 15); level 0 of the
-// side's x sparse table
-__global__ void k_quiet_level0(const float* __restrict__ I, const unsigned char* __restrict__ band,
-                               const unsigned char* __restrict__ zr, long long V, unsigned char* __restrict__ q) {
-  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
-       v += (long long)gridDim.x * blockDim.x)
-    q[v] = (I[v] != 0.0f || (band && band[v])) ? 0 : zr[v];
-}
-
-// level L from level L-1: min over [x, x + 2^L - 1] clipped to the row
-__global__ void k_quiet_level(const unsigned char* __restrict__ prev, unsigned char* __restrict__ next, int nx,
-                              long long V, int half) {
-  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
-       v += (long long)gridDim.x * blockDim.x) {
-    const int x = (int)(v % nx);
-    const unsigned char a = prev[v];
-    next[v] = x + half < nx ? min(a, prev[v + half]) : a;
+// Row hulls of the non-quiet voxels of one side.  The quiet radius of voxel q is 0
+// unless I(q) = 0 and q has no band entry, else zr(q) = the zero radius of the other
+// volume (Chebyshev distance from q to its nearest non-zero voxel, boxes clipped to
+// the image, 15 = at least 15).  Per image row (y, z) and radius R, the first and last
+// x with quiet radius < R, (nx, -1) when there is none: a row interval outside that
+// hull is quiet at R.  One thread per (row, R).
+__global__ void k_quiet_hull(const float* __restrict__ I, const unsigned char* __restrict__ band,
+                             const unsigned char* __restrict__ zr, int nx, int ny, int nz, short2* __restrict__ hull) {
+  const int rows = ny * nz;
+  const int nR = kQuietRmax - kQuietRmin + 1;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < rows * nR; t += gridDim.x * blockDim.x) {
+    const int row = t % rows, R = kQuietRmin + t / rows;
+    const long long base = (long long)row * nx;
+    int first = nx, last = -1;
+    for (int x = 0; x < nx; x++) {
+      const long long v = base + x;
+      const int q = (I[v] != 0.0f || (band && band[v])) ? 0 : zr[v];
+      if (q < R) {
+        first = min(first, x);
+        last = x;
+      }
+    }
+    hull[t] = make_short2((short)first, (short)last);
   }
 }
 
-cudaError_t launch_quiet_table(const float* I, const unsigned char* band, const unsigned char* zr, int nx,
-                               long long V, int levels, unsigned char* table, cudaStream_t s) {
-  k_quiet_level0<<<2048, 256, 0, s>>>(I, band, zr, V, table);
-  for (int L = 1; L < levels; L++)
-    k_quiet_level<<<2048, 256, 0, s>>>(table + (long long)(L - 1) * V, table + (long long)L * V, nx, V, 1 << (L - 1));
+cudaError_t launch_quiet_hull(const float* I, const unsigned char* band, const unsigned char* zr, int nx, int ny,
+                              int nz, short2* hull, cudaStream_t s) {
+  const int n = ny * nz * (kQuietRmax - kQuietRmin + 1);
+  k_quiet_hull<<<(n + 255) / 256, 256, 0, s>>>(I, band, zr, nx, ny, nz, hull);
   return cudaGetLastError();
 }
 

@@ -99,11 +99,12 @@ struct SobolWarp {
 // guidance prefilter reads).  An image is T(p) = p + sum_k l_k U_k with |U_k| <= m
 // (Chebyshev), so its cell corners lie within 1 + m + 1 of any own corner of p's cell,
 // plus rounding: Rq = ceil(m) + 3.  Then a = b = 0 and every distance is >= r at every
-// point, so h = g = 0 for all N points, exactly.  Range minima along x of the side's
-// quiet table (two byte loads per row of the box), early exit on the first miss.
+// point, so h = g = 0 for all N points, exactly.  Every image row (y, z) of the box
+// must have its x range outside the row's hull of non-quiet voxels at Rq (one 4-byte
+// load per row), early exit on the first miss.
 __device__ __forceinline__ bool sobol_quiet(const SobolRec& R, const Volumes& V, int side, int lane) {
-  const unsigned char* qt = side == 0 ? V.qst[0] : V.qst[1];
-  if (!qt) return false;
+  const short2* qh = side == 0 ? V.qhull[0] : V.qhull[1];
+  if (!qh) return false;
   const int dims[3] = {V.nx, V.ny, V.nz};
   int lo[3], hi[3], mU = 0;
 #pragma unroll
@@ -120,10 +121,8 @@ __device__ __forceinline__ bool sobol_quiet(const SobolRec& R, const Volumes& V,
     if (lo[a] > hi[a]) return false;
   }
   const int Rq = (mU + 1023) / 1024 + 3;
-  if (Rq > 15) return false;  // beyond the zero radius the maps carry
-  const int len = hi[0] - lo[0] + 1;
-  const int L = 31 - __clz(len);
-  const unsigned char* t = qt + (long long)L * V.V;
+  if (Rq > kQuietRmax) return false;  // beyond the radii the hulls carry
+  const short2* h = qh + (Rq - kQuietRmin) * V.ny * V.nz;
   const int nyb = hi[1] - lo[1] + 1;
   const int nrows = nyb * (hi[2] - lo[2] + 1);
   for (int r0 = 0; r0 < nrows; r0 += 32) {
@@ -131,8 +130,8 @@ __device__ __forceinline__ bool sobol_quiet(const SobolRec& R, const Volumes& V,
     bool miss = false;
     if (r < nrows) {
       const int z = lo[2] + r / nyb, y = lo[1] + r % nyb;
-      const long long row = ((long long)z * V.ny + y) * V.nx;
-      miss = min(__ldg(&t[row + lo[0]]), __ldg(&t[row + hi[0] - (1 << L) + 1])) < Rq;
+      const short2 hb = __ldg(&h[z * V.ny + y]);
+      miss = !(hi[0] < hb.x || lo[0] > hb.y);
     }
     if (__any_sync(FULLMASK, miss)) return false;
   }
