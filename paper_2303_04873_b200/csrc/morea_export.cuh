@@ -21,7 +21,9 @@ __device__ __forceinline__ int voxel_label(unsigned m, int M) {
 
 struct LabelSample {
   static constexpr bool kQuiet = false;
-  __device__ __forceinline__ const short2* quiet_hull() const { return nullptr; }
+  __device__ __forceinline__ int quiet_off() const { return -1; }
+  __device__ __forceinline__ short2 quiet_hull(int) const { return make_short2(0, -1); }
+  __device__ __forceinline__ void count_quiet(int) {}
   __device__ __forceinline__ void quiet_row(int, int) {}
   const unsigned char* masks;
   int M;
@@ -56,7 +58,9 @@ __global__ void __launch_bounds__(kRasterThreads) k_label_counts(const EvalArgs 
 // E3 pass 1: owner = lowest owning tet id (deterministic under folds)
 struct MinOwnerSample {
   static constexpr bool kQuiet = false;
-  __device__ __forceinline__ const short2* quiet_hull() const { return nullptr; }
+  __device__ __forceinline__ int quiet_off() const { return -1; }
+  __device__ __forceinline__ short2 quiet_hull(int) const { return make_short2(0, -1); }
+  __device__ __forceinline__ void count_quiet(int) {}
   __device__ __forceinline__ void quiet_row(int, int) {}
   int* owner;
   int tet;
@@ -71,7 +75,9 @@ struct MinOwnerSample {
 // one fp64 rounding (the oracle's operations), times the spacing, fp32
 struct DvfSample {
   static constexpr bool kQuiet = false;
-  __device__ __forceinline__ const short2* quiet_hull() const { return nullptr; }
+  __device__ __forceinline__ int quiet_off() const { return -1; }
+  __device__ __forceinline__ short2 quiet_hull(int) const { return make_short2(0, -1); }
+  __device__ __forceinline__ void count_quiet(int) {}
   __device__ __forceinline__ void quiet_row(int, int) {}
   const SideRec* R;  // shared
   const int* owner;

@@ -583,9 +583,10 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       // quiet radii over [xl, xh] from the sparse table of the row (two byte loads).
       int len = len_all;
       if (F::kQuiet) {
-        const short2* qh = f.quiet_hull();  // item-uniform; nullptr: radius beyond the hulls
-        if (qh) {
-          const short2 hb = rv ? __ldg(&qh[z * ny + y]) : make_short2(0, -1);
+        const int qo = f.quiet_off();  // item-uniform; -1: radius beyond the hulls
+        if (qo >= 0) {
+          // unconditional load (lanes past the chunk read the plane's first row)
+          const short2 hb = f.quiet_hull(qo + (rv ? z * ny + y : 0));
           if (len_all > 0 && (xh < hb.x || xl > hb.y)) {
             len = 0;
             f.quiet_row((z * ny + y) * nx + xl, len_all);  // 2 V < 2^31 (own-record index is an int)
@@ -595,6 +596,7 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       const int incl = warp_incl_scan(len, lane);
       const int total = __shfl_sync(FULLMASK, incl, 31);
       const int tot_all = F::kQuiet ? (int)__reduce_add_sync(FULLMASK, (unsigned)len_all) : total;
+      if (F::kQuiet && lane == 0) f.count_quiet(tot_all - total);
       if (total == 0) {
         f.count_only(lane == 0 ? tot_all : 0);
         continue;
@@ -735,7 +737,6 @@ struct Acc {
   float gf;     // fp32 partial sum of guidance terms since the last flush (into g)
   int n, nb;    // samples, band entries
   int qn;       // band entries in the per-warp queue (warp-uniform)
-  int nq;       // samples of quiet rows (empty space, counted not swept; profiling)
 };
 
 template <bool TEX, int SIDE_T, bool CLAMP, bool DUMP>
@@ -750,6 +751,8 @@ struct Sample {
   int side;           // runtime side when SIDE_T < 0 (warp-uniform)
   float* dump_h;      // DUMP (test hook morea_sample_map): per-voxel h and fg of this side
   unsigned char* dump_fg;
+  int qoff;           // row hulls of this side at the item's radius: V.qhull[side] + qoff
+                      // + z ny + y; -1 when there are none (empty-space skip off)
   // CLAMP: some position of the item may leave the range the gather covers
   // exactly, apply the O5 clamp (a separate instantiation: no predicated clamp
   // instructions in the common loop)
@@ -864,14 +867,14 @@ struct Sample {
 
   // quiet rows (raster): the side's row hulls at the item's radius R (SideRec flags)
   static constexpr bool kQuiet = true;
-  __device__ __forceinline__ const short2* quiet_hull() const {
+  __device__ __forceinline__ int quiet_off() const { return qoff; }
+  __device__ __forceinline__ short2 quiet_hull(int idx) const {
     const int SIDE = SIDE_T >= 0 ? SIDE_T : side;
-    const int R = __float_as_int(sc1.w);
-    const short2* h = SIDE == 0 ? V.qhull[0] : V.qhull[1];
-    return (h && R <= kQuietRmax) ? h + (R - kQuietRmin) * V.ny * V.nz : nullptr;
+    return __ldg(&(SIDE == 0 ? V.qhull[0] : V.qhull[1])[idx]);
   }
+  // samples of a chunk's quiet rows (profiling; lane 0, per-warp shared counter)
+  __device__ __forceinline__ void count_quiet(int n) { S.stat[3] += (unsigned long long)n; }
   __device__ __forceinline__ void quiet_row(int q0, int n) {
-    acc.nq += n;
     if (DUMP)
       for (int i = 0; i < n; i++) {
         dump_h[q0 + i] = 0.f;
@@ -1018,18 +1021,20 @@ __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int l
     S.sc0 = make_float4(R.A[0][0], R.A[1][0], R.A[2][0], 0.5f - R.eps[0]);
     // gather x of corner i0: I_o is volume o of texI (TEX), else a plain index + 1
     const float uoff = TEX ? fmaf((float)(1 - (SIDE_T >= 0 ? SIDE_T : side)), V.fnxp, V.uoff0) : 1.0f;
-    S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], uoff, __int_as_float((R.flags >> 8) & 0xff));
+    S.sc1 = make_float4(0.5f - R.eps[1], 0.5f - R.eps[2], uoff, 0.f);
   }
   __syncwarp();
   // O5 clamp only where a position can leave the range the gather covers exactly:
   // [0, n-1) for plain loads, (-1, n) on the edge-padded textures (warp-uniform)
   const int loff = (SIDE_T >= 0 ? SIDE_T : side) * (int)V.V;
+  const int qR = (R.flags >> 8) & 0xff;  // empty-space radius of the item (k_setup)
+  const int qoff = (V.qhull[0] && qR <= kQuietRmax) ? (qR - kQuietRmin) * V.ny * V.nz : -1;
   if ((R.flags & ((TEX && kTexPad) ? 8 : 2)) == 0) {
-    Sample<TEX, SIDE_T, true, DUMP> f{V, R, S, S.sc0, S.sc1, acc, side, dump_h, dump_fg};
+    Sample<TEX, SIDE_T, true, DUMP> f{V, R, S, S.sc0, S.sc1, acc, side, dump_h, dump_fg, qoff};
     raster(R, V.nx, V.ny, loff, S, lane, f);
     f.drain(SIDE_T >= 0 ? SIDE_T : side);
   } else {
-    Sample<TEX, SIDE_T, false, DUMP> f{V, R, S, S.sc0, S.sc1, acc, side, dump_h, dump_fg};
+    Sample<TEX, SIDE_T, false, DUMP> f{V, R, S, S.sc0, S.sc1, acc, side, dump_h, dump_fg, qoff};
     raster(R, V.nx, V.ny, loff, S, lane, f);
     f.drain(SIDE_T >= 0 ? SIDE_T : side);
   }
@@ -1115,7 +1120,7 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
     const int e = A.sched[es];
     MOREA_CHECK(e >= 0 && e < A.n_entries && v < A.n_raster_versions);
     const long long i = ((long long)v * A.n_entries + e) * A.P + sol;
-    Acc acc{0.0, 0.0, 0.f, 0.f, 0, 0, 0, 0};
+    Acc acc{0.0, 0.0, 0.f, 0.f, 0, 0, 0};
     int n_side0 = 0;
 #pragma unroll 1
     for (int side = 0; side < 2; side++) {
@@ -1130,13 +1135,11 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
     out.n = warp_sum_i(acc.n);
     out.n0 = warp_sum_i(n_side0);
     const int nb = warp_sum_i(acc.nb);
-    const int nq = warp_sum_i(acc.nq);
     if (lane == 0) {
       A.hgn[i] = out;
       S.stat[0] += out.n;
       S.stat[1] += nb;
       S.stat[2] += 1;
-      S.stat[3] += nq;
       debug_count_item(A);
     }
   }
@@ -1377,7 +1380,9 @@ struct OwnerSample {
   int* owner;
   int tet;
   static constexpr bool kQuiet = false;
-  __device__ __forceinline__ const short2* quiet_hull() const { return nullptr; }
+  __device__ __forceinline__ int quiet_off() const { return -1; }
+  __device__ __forceinline__ short2 quiet_hull(int) const { return make_short2(0, -1); }
+  __device__ __forceinline__ void count_quiet(int) {}
   __device__ __forceinline__ void quiet_row(int, int) {}
   __device__ __forceinline__ void flush_h() {}
   __device__ __forceinline__ void count_only(int) {}
