@@ -45,7 +45,8 @@ struct __align__(16) SideRec {
                               // [0, n-1) with margin (no clamp needed); bit 2: every face is a
                               // regular lower/upper face (fast row intervals); bit 3: every
                               // position is inside (-1, n) with margin (no clamp needed on the
-                              // edge-padded gather textures)
+                              // edge-padded gather textures); bits 8..15: empty-space radius R;
+                              // bits 16..17: nl, regular items list their nl lower faces first
   float vy[4], vz[4];         // vertex y, z (voxel units, exact) for per-slice y ranges
   int lo[3], hi[3];           // lattice bbox clipped to the image
   int U[4][3];                // Q_other - Q_own per vertex

@@ -224,6 +224,46 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
   bool regular = true;
 #pragma unroll
   for (int k = 0; k < 4; k++) regular = regular && (G.ftype[k] == 1 || G.ftype[k] == -1);
+  int nl = 0;  // regular items: lower-bound faces (n_x > 0) first, nl of them
+  if (regular) {
+    // The fast row interval (row_interval) then takes the max of the crossings of
+    // faces [0, nl) and the min of faces [nl, 4) with no per-face selects.  Each
+    // face keeps its opposite vertex (the U partner of exact_fg), and the error
+    // bounds widen to their group's maximum: the binding crossing's bound.
+    int ord[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+      if (G.ftype[k] > 0) ord[nl++] = k;
+    int c = nl;
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+      if (G.ftype[k] < 0) ord[c++] = k;
+    float4 face[4];
+    i64 nrm[4][3], cst[4];
+    int U[4][3];
+    float wl = 0.f, wh = 0.f;
+    for (int k = 0; k < 4; k++) {
+      const int o = ord[k];
+      face[k] = G.face[o];
+      cst[k] = G.cst[o];
+      for (int a = 0; a < 3; a++) {
+        nrm[k][a] = G.nrm[o][a];
+        U[k][a] = G.U[o][a];
+      }
+      if (k < nl) wl = fmaxf(wl, face[k].w);
+      else wh = fmaxf(wh, face[k].w);
+    }
+    for (int k = 0; k < 4; k++) {
+      G.face[k] = face[k];
+      G.face[k].w = k < nl ? wl : wh;
+      G.ftype[k] = k < nl ? 1 : -1;
+      G.cst[k] = cst[k];
+      for (int a = 0; a < 3; a++) {
+        G.nrm[k][a] = nrm[k][a];
+        G.U[k][a] = U[k][a];
+      }
+    }
+  }
   // Empty-space radius (bits 8..15): an owned sample q maps to x = q + u(q) with u a
   // convex combination of the vertex displacements, so |u_a| <= max_k |U_ka| / 1024 and
   // every trilinear corner of x lies within Chebyshev distance R - 1 of q, R =
@@ -235,7 +275,7 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
 #pragma unroll
     for (int a = 0; a < 3; a++) maxU = max(maxU, abs(G.U[k][a]));
   const int skipR = min((maxU + 1023) / 1024 + 2, 255);
-  G.flags = 1 | (inside ? 2 : 0) | (regular ? 4 : 0) | (inside_p ? 8 : 0) | (skipR << 8);
+  G.flags = 1 | (inside ? 2 : 0) | (regular ? 4 : 0) | (inside_p ? 8 : 0) | (skipR << 8) | (nl << 16);
 }
 
 // ---------------------------------------------------------------------------
@@ -449,21 +489,22 @@ __device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, boo
   const int lo = R.lo[0], hi = R.hi[0];
   const float dy = (float)(y - R.lo[1]), dz = (float)(z - R.lo[2]);
   const float flo = (float)lo - 4.5f, fhi = (float)hi + 4.5f;
-  const int4 types = *reinterpret_cast<const int4*>(R.ftype);
-  const int tk[4] = {types.x, types.y, types.z, types.w};
-  int l = lo, h = hi;
-  bool amb = false;
-#pragma unroll
-  for (int k = 0; k < 4; k++) {
-    const float4 fc4 = R.face[k];
-    const float xs = fminf(fmaxf(fmaf(fc4.z, dz, fmaf(fc4.y, dy, fc4.x)), flo), fhi);
-    amb = amb || (fabsf(xs - rintf(xs)) <= fc4.w);
-    const int c = __float2int_ru(xs);  // lower face: smallest x > x*; upper: largest x < x* = c - 1
-    if (tk[k] > 0) l = max(l, c);
-    else h = min(h, c - 1);
-  }
-  xl = l;
-  xh = h;
+  // faces [0, nl) bound x from below, [nl, 4) from above (k_setup order, 1 <= nl <= 3):
+  // owned x > max of the lower crossings and x < min of the upper ones.  Only the
+  // binding crossing's rounding matters, so the ambiguity test is on the max / min
+  // against the group's error bound (faces 0 and 3 carry them).
+  const int nl = (R.flags >> 16) & 3;
+  const float4 f0 = R.face[0], f1 = R.face[1], f2 = R.face[2], f3 = R.face[3];
+  const float x0 = fmaf(f0.z, dz, fmaf(f0.y, dy, f0.x)), x1 = fmaf(f1.z, dz, fmaf(f1.y, dy, f1.x));
+  const float x2 = fmaf(f2.z, dz, fmaf(f2.y, dy, f2.x)), x3 = fmaf(f3.z, dz, fmaf(f3.y, dy, f3.x));
+  float ml = fmaxf(x0, fmaxf(nl > 1 ? x1 : x0, nl > 2 ? x2 : x0));
+  float mh = fminf(x3, fminf(nl < 3 ? x2 : x3, nl < 2 ? x1 : x3));
+  ml = fminf(fmaxf(ml, flo), fhi);
+  mh = fminf(fmaxf(mh, flo), fhi);
+  bool amb = (fabsf(ml - rintf(ml)) <= f0.w) || (fabsf(mh - rintf(mh)) <= f3.w);
+  // lower: smallest x > x*; upper: largest x < x* = ceil(x*) - 1
+  xl = max(lo, __float2int_ru(ml));
+  xh = min(hi, __float2int_ru(mh) - 1);
   amb = amb && rv;
   if (__any_sync(FULLMASK, amb)) {
     const int2 r = row_interval_exact_if(amb, R, y, z, xl, xh);
