@@ -116,8 +116,8 @@ __device__ __forceinline__ bool load_tet(const EvalArgs& A, int sol, int4 tv, in
 // a2: exact geometry of one side (O2, O3, O4).  |Q| < 2^19.6 so edge components
 // < 2^20, normals < 2^41, |Delta| < 2^62.6, e_k(q) < 3 2^61.
 // ---------------------------------------------------------------------------
-__device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny, int nz,
-                           SideRec& G) {
+__device__ void build_side_ordered(const int Q[4][3], const int Qo[4][3], int nx, int ny, int nz,
+                                   SideRec& G) {
   G.flags = 0;
   const i64 det = det3(Q);
   if (det == 0) return;  // degenerate: owns nothing (O3)
@@ -224,45 +224,29 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
   bool regular = true;
 #pragma unroll
   for (int k = 0; k < 4; k++) regular = regular && (G.ftype[k] == 1 || G.ftype[k] == -1);
-  int nl = 0;  // regular items: lower-bound faces (n_x > 0) first, nl of them
+  // Regular items list their lower-bound faces (n_x > 0) first (build_side orders the
+  // vertices so), nl of them.  The fast row interval (row_interval) takes the max of
+  // the crossings of faces [0, nl) and the min of faces [nl, 4) with no per-face
+  // selects; its ambiguity test needs the binding crossing's bound, so each group's
+  // bounds widen to the group maximum.
+  int nl = 0;
   if (regular) {
-    // The fast row interval (row_interval) then takes the max of the crossings of
-    // faces [0, nl) and the min of faces [nl, 4) with no per-face selects.  Each
-    // face keeps its opposite vertex (the U partner of exact_fg), and the error
-    // bounds widen to their group's maximum: the binding crossing's bound.
-    int ord[4];
+    while (nl < 4 && G.ftype[nl] > 0) nl++;
+    regular = nl >= 1 && nl <= 3;
 #pragma unroll
-    for (int k = 0; k < 4; k++)
-      if (G.ftype[k] > 0) ord[nl++] = k;
-    int c = nl;
-#pragma unroll
-    for (int k = 0; k < 4; k++)
-      if (G.ftype[k] < 0) ord[c++] = k;
-    float4 face[4];
-    i64 nrm[4][3], cst[4];
-    int U[4][3];
+    for (int k = 1; k < 4; k++) regular = regular && (G.ftype[k] <= G.ftype[k - 1]);
+  }
+  if (regular) {
     float wl = 0.f, wh = 0.f;
+#pragma unroll
     for (int k = 0; k < 4; k++) {
-      const int o = ord[k];
-      face[k] = G.face[o];
-      cst[k] = G.cst[o];
-      for (int a = 0; a < 3; a++) {
-        nrm[k][a] = G.nrm[o][a];
-        U[k][a] = G.U[o][a];
-      }
-      if (k < nl) wl = fmaxf(wl, face[k].w);
-      else wh = fmaxf(wh, face[k].w);
+      if (k < nl) wl = fmaxf(wl, G.face[k].w);
+      else wh = fmaxf(wh, G.face[k].w);
     }
-    for (int k = 0; k < 4; k++) {
-      G.face[k] = face[k];
-      G.face[k].w = k < nl ? wl : wh;
-      G.ftype[k] = k < nl ? 1 : -1;
-      G.cst[k] = cst[k];
-      for (int a = 0; a < 3; a++) {
-        G.nrm[k][a] = nrm[k][a];
-        G.U[k][a] = U[k][a];
-      }
-    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) G.face[k].w = k < nl ? wl : wh;
+  } else {
+    nl = 0;
   }
   // Empty-space radius (bits 8..15): an owned sample q maps to x = q + u(q) with u a
   // convex combination of the vertex displacements, so |u_a| <= max_k |U_ka| / 1024 and
@@ -276,6 +260,42 @@ __device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny
     for (int a = 0; a < 3; a++) maxU = max(maxU, abs(G.U[k][a]));
   const int skipR = min((maxU + 1023) / 1024 + 2, 255);
   G.flags = 1 | (inside ? 2 : 0) | (regular ? 4 : 0) | (inside_p ? 8 : 0) | (skipR << 8) | (nl << 16);
+}
+
+// Orders the vertices so that the faces opposite them that bound x from below (inward
+// n_x > 0) come first, then the rest (a stable partition of a local copy; face k stays
+// opposite vertex k, so U_k and e_k keep their pairing), and builds the side record.
+// Vertex order changes nothing else the record holds.
+__device__ void build_side(const int Q[4][3], const int Qo[4][3], int nx, int ny, int nz, SideRec& G) {
+  int low = 0;  // bit k: the face opposite vertex k is a lower bound along x
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const int f0 = (k == 0) ? 1 : 0;
+    const int f1 = (k <= 1) ? 2 : 1;
+    const int f2 = (k <= 2) ? 3 : 2;
+    const i64 u0 = Q[f1][0] - Q[f0][0], u1 = Q[f1][1] - Q[f0][1], u2 = Q[f1][2] - Q[f0][2];
+    const i64 v0 = Q[f2][0] - Q[f0][0], v1 = Q[f2][1] - Q[f0][1], v2 = Q[f2][2] - Q[f0][2];
+    const i64 n0 = u1 * v2 - u2 * v1, n1 = u2 * v0 - u0 * v2, n2 = u0 * v1 - u1 * v0;
+    const i64 sd = n0 * (Q[k][0] - Q[f0][0]) + n1 * (Q[k][1] - Q[f0][1]) + n2 * (Q[k][2] - Q[f0][2]);
+    if ((sd < 0 ? -n0 : n0) > 0) low |= 1 << k;
+  }
+  int src[4], c = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++)
+    if (low >> k & 1) src[c++] = k;
+#pragma unroll
+  for (int k = 0; k < 4; k++)
+    if (!(low >> k & 1)) src[c++] = k;
+  int P[4][3], Po[4][3];
+#pragma unroll
+  for (int k = 0; k < 4; k++)
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      const int j = src[k];
+      P[k][a] = j == 0 ? Q[0][a] : j == 1 ? Q[1][a] : j == 2 ? Q[2][a] : Q[3][a];
+      Po[k][a] = j == 0 ? Qo[0][a] : j == 1 ? Qo[1][a] : j == 2 ? Qo[2][a] : Qo[3][a];
+    }
+  build_side_ordered(P, Po, nx, ny, nz, G);
 }
 
 // ---------------------------------------------------------------------------
