@@ -640,8 +640,8 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       const int len_all = rv ? max(0, xh - xl + 1) : 0;
       // quiet rows (empty space): every voxel of the row is background
       // with no band entry and the other volume is zero within the item's radius, so
-      // each sample's h is exactly 0 -- counted, not swept.  Range minimum of the
-      // quiet radii over [xl, xh] from the sparse table of the row (two byte loads).
+      // each sample's h is exactly 0 -- counted, not swept.  The row is quiet when
+      // [xl, xh] lies outside the hull of the image row's non-quiet voxels.
       int len = len_all;
       if (F::kQuiet) {
         const int qo = f.quiet_off();  // item-uniform; -1: radius beyond the hulls
