@@ -106,7 +106,7 @@ struct morea_ctx {
   double sp[3] = {1, 1, 1};
   double r = 0;
   double w[2][kMaxPairs] = {};
-  DevBuf I[2], band[2], dmap[2], wts, own, qhull;
+  DevBuf I[2], band[2], dmap[2], wts, own, qhull, qcell;
   // Sobol sampler (NEXT-1): mode, rate, dilated band masks (2 V bytes), direction numbers
   int sampler = MOREA_SAMPLER_VOXEL;
   double rate = 1.0;
@@ -299,9 +299,11 @@ Volumes volumes_of(const morea_ctx* c) {
     for (int i = 0; i < kMaxPairs; i++) v.wf[s][i] = c->r > 0 ? (float)(c->w[s][i] / c->r) : 0.f;
   v.rf = (float)c->r;
   v.rlo = (float)(c->r - (double)v.rf);
-  for (int s = 0; s < 2; s++)
+  for (int s = 0; s < 2; s++) {
+    v.qcell[s] = c->qcell.p ? c->qcell.as<unsigned char>() + (size_t)s * c->V : nullptr;
     v.qhull[s] = c->qhull.p ? c->qhull.as<short2>() + (size_t)s * (kQuietRmax - kQuietRmin + 1) * c->ny * c->nz
                             : nullptr;
+  }
   v.own[0] = c->own.as<uint2>();
   v.own[1] = v.own[0] ? v.own[0] + c->V : nullptr;
   v.use_tex = c->use_tex ? 1 : 0;
@@ -728,7 +730,7 @@ void morea_destroy(morea_ctx* ctx) {
     cudaEventDestroy(p.second);
   }
   DevBuf* bufs[] = {&ctx->I[0], &ctx->I[1], &ctx->band[0], &ctx->band[1], &ctx->dmap[0],
-                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->qhull, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->st_masks, &ctx->st_counts, &ctx->st_dvf, &ctx->st_cov,
+                    &ctx->dmap[1], &ctx->wts, &ctx->own, &ctx->qhull, &ctx->qcell, &ctx->dil, &ctx->sobolv, &ctx->d_inc_off, &ctx->d_inc, &ctx->st_fixed, &ctx->st_rep, &ctx->st_masks, &ctx->st_counts, &ctx->st_dvf, &ctx->st_cov,
                     &ctx->scratch_owner, &ctx->zero_off, &ctx->mx_off, &ctx->mx_acc,
                     &ctx->mx_obj, &ctx->mx_cache, &ctx->mx_nv, &ctx->mx_pobj, &ctx->mx_pacc, &ctx->mx_dep,
                     &ctx->mx_base, &ctx->mx_accepted, &ctx->mx_cluster, &ctx->mx_mu, &ctx->mx_L, &ctx->mx_arch,
@@ -834,6 +836,7 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
     CK(m1.ensure(V));
     const size_t nh = (size_t)(kQuietRmax - kQuietRmin + 1) * ny * nz;
     CK(ctx->qhull.ensure(2 * nh * sizeof(short2)));
+    CK(ctx->qcell.ensure(2 * V));
     for (int s = 0; s < 2; s++) {
       CK(launch_zero_radius(ctx->I[1 - s].as<float>(), nx, ny, nz, zr.as<unsigned char>(), m0.as<unsigned char>(),
                             m1.as<unsigned char>(), ctx->stream));
@@ -841,6 +844,9 @@ int morea_load_images(morea_ctx* ctx, int nx, int ny, int nz, const double spaci
                             ctx->own.as<uint2>() + (size_t)s * V, ctx->stream));
       CK(launch_quiet_hull(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr,
                            zr.as<unsigned char>(), nx, ny, nz, ctx->qhull.as<short2>() + (size_t)s * nh, ctx->stream));
+      CK(launch_quiet_cells(ctx->I[s].as<float>(), K > 0 ? ctx->band[s].as<unsigned char>() : nullptr,
+                            zr.as<unsigned char>(), nx, ny, nz, m0.as<unsigned char>(), m1.as<unsigned char>(),
+                            ctx->qcell.as<unsigned char>() + (size_t)s * V, ctx->stream));
     }
     CK(cudaStreamSynchronize(ctx->stream));
   }

@@ -101,6 +101,9 @@ struct Volumes {
   // image row (y, z), the first and last x whose quiet radius is < R ((nx, -1): none);
   // qhull[s] + (R - kQuietRmin) ny nz + z ny + y
   const short2* qhull[2];
+  // per side and voxel v, the minimum quiet radius over the 4^3 block v - 1 .. v + 2
+  // (clipped): the per-point empty-space test of the Sobol sampler
+  const unsigned char* qcell[2];
   const float* dmap[2];          // K * V fp32 per side
   int K;
   double r, inv_r;
@@ -183,6 +186,8 @@ cudaError_t launch_band_mask(const float* dmap, int K, long long V, double r, un
 cudaError_t launch_pad_volume(const float* src, int nx, int ny, int nz, int pad, float* dst, cudaStream_t s);
 cudaError_t launch_own_records(const float* I, const unsigned char* band, long long V,
                                uint2* out, cudaStream_t s);
+cudaError_t launch_quiet_cells(const float* I, const unsigned char* band, const unsigned char* zr, int nx, int ny,
+                               int nz, unsigned char* tmp0, unsigned char* tmp1, unsigned char* qcell, cudaStream_t s);
 cudaError_t launch_quiet_hull(const float* I, const unsigned char* band, const unsigned char* zr, int nx, int ny,
                               int nz, short2* hull, cudaStream_t s);
 cudaError_t launch_zero_radius(const float* I, int nx, int ny, int nz, unsigned char* zr, unsigned char* m0,

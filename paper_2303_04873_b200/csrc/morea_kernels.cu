@@ -1636,6 +1636,38 @@ __global__ void k_quiet_hull(const float* __restrict__ I, const unsigned char* _
   }
 }
 
+// Per-voxel quiet radius q (as k_quiet_hull), then its minimum over the 4^3 block
+// v - 1 .. v + 2 (clipped to the image), one axis at a time.
+__global__ void k_quiet_voxel(const float* __restrict__ I, const unsigned char* __restrict__ band,
+                              const unsigned char* __restrict__ zr, long long V, unsigned char* __restrict__ q) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
+       v += (long long)gridDim.x * blockDim.x)
+    q[v] = (I[v] != 0.0f || (band && band[v])) ? 0 : zr[v];
+}
+
+__global__ void k_min4(const unsigned char* __restrict__ in, unsigned char* __restrict__ out, int n, long long stride,
+                       long long V) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < V;
+       v += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)((v / stride) % n);
+    unsigned char m = in[v];
+    if (c > 0) m = min(m, in[v - stride]);
+    if (c + 1 < n) m = min(m, in[v + stride]);
+    if (c + 2 < n) m = min(m, in[v + 2 * stride]);
+    out[v] = m;
+  }
+}
+
+cudaError_t launch_quiet_cells(const float* I, const unsigned char* band, const unsigned char* zr, int nx, int ny,
+                               int nz, unsigned char* tmp0, unsigned char* tmp1, unsigned char* qcell, cudaStream_t s) {
+  const long long V = (long long)nx * ny * nz;
+  k_quiet_voxel<<<2048, 256, 0, s>>>(I, band, zr, V, tmp0);
+  k_min4<<<2048, 256, 0, s>>>(tmp0, tmp1, nx, 1, V);
+  k_min4<<<2048, 256, 0, s>>>(tmp1, tmp0, ny, nx, V);
+  k_min4<<<2048, 256, 0, s>>>(tmp0, qcell, nz, (long long)nx * ny, V);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_quiet_hull(const float* I, const unsigned char* band, const unsigned char* zr, int nx, int ny,
                               int nz, short2* hull, cudaStream_t s) {
   const int n = ny * nz * (kQuietRmax - kQuietRmin + 1);

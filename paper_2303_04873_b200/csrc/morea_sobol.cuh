@@ -86,10 +86,23 @@ __device__ __noinline__ void exact_sobol(const SobolRec& R, const unsigned xm[4]
 // ---------------------------------------------------------------------------
 // k_sobol
 // ---------------------------------------------------------------------------
+constexpr int kSbQueueCap = 64;  // < 32 pending + one step of <= 32
 struct SobolWarp {
   SobolRec R;
   unsigned long long stat[4];
+  uint4 qx[kSbQueueCap];  // Sobol states (x0..x3) of the points that are not proven quiet
 };
+
+// Item-side radius of the per-point empty-space test (see sobol_quiet): Rq = ceil(m) + 3,
+// m = max |Qo - Q| / 1024 over the vertices and axes
+__device__ __forceinline__ int sobol_radius(const SobolRec& R) {
+  int mU = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++)
+#pragma unroll
+    for (int a = 0; a < 3; a++) mU = max(mU, abs(R.Qo[k][a] - R.Q[k][a]));
+  return (mU + 1023) / 1024 + 3;
+}
 
 // Empty space, one side of an item: true when every voxel a point
 // of the tet or its image can read is quiet -- background (I = 0) with no band entry
@@ -106,7 +119,7 @@ __device__ __forceinline__ bool sobol_quiet(const SobolRec& R, const Volumes& V,
   const short2* qh = side == 0 ? V.qhull[0] : V.qhull[1];
   if (!qh) return false;
   const int dims[3] = {V.nx, V.ny, V.nz};
-  int lo[3], hi[3], mU = 0;
+  int lo[3], hi[3];
 #pragma unroll
   for (int a = 0; a < 3; a++) {
     int qmin = R.Q[0][a], qmax = R.Q[0][a];
@@ -114,13 +127,12 @@ __device__ __forceinline__ bool sobol_quiet(const SobolRec& R, const Volumes& V,
     for (int k = 0; k < 4; k++) {
       qmin = min(qmin, R.Q[k][a]);
       qmax = max(qmax, R.Q[k][a]);
-      mU = max(mU, abs(R.Qo[k][a] - R.Q[k][a]));
     }
     lo[a] = max((qmin >> 10) - 1, 0);
     hi[a] = min((qmax >> 10) + 2, dims[a] - 1);
     if (lo[a] > hi[a]) return false;
   }
-  const int Rq = (mU + 1023) / 1024 + 3;
+  const int Rq = sobol_radius(R);
   if (Rq > kQuietRmax) return false;  // beyond the radii the hulls carry
   const short2* h = qh + (Rq - kQuietRmin) * V.ny * V.nz;
   const int nyb = hi[1] - lo[1] + 1;
@@ -325,21 +337,9 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
       const unsigned char* dil = side == 0 ? V.dil[0] : V.dil[1];
       float hf = 0.f, gf = 0.f;
       int step = 0;
-      // S2: x(g(s0)) ^ x(g(lane)) ^ mask, updated per step: for s0 = 32 m,
-      // g(s0 + 32) ^ g(s0) = 2^4 ^ 2^(5 + ctz(m + 1)), so two direction numbers
-      // per dimension change (warp-uniform)
-      unsigned x0 = m0, x1 = m1, x2 = m2, x3 = m3;
-      const int Ni = (int)N;  // < 2^31: k_setup flags larger counts (DOMAIN) and clears the side
-#pragma unroll 1
-      for (int s0 = 0; s0 < Ni; s0 += 32) {
-        if (s0 > 0) {
-          const int b = 4 + __ffs(s0 >> 5);  // 5 + ctz(m + 1), m + 1 = s0 / 32
-          x0 ^= sV[0][4] ^ sV[0][b];
-          x1 ^= sV[1][4] ^ sV[1][b];
-          x2 ^= sV[2][4] ^ sV[2][b];
-          x3 ^= sV[3][4] ^ sV[3][b];
-        }
-        const bool valid = s0 + lane < Ni;
+      // One point per lane from its Sobol state (S2-S9): h and the guidance terms,
+      // fp32 partial sums flushed into fp64 every 16 calls (warp-uniform)
+      auto point = [&](unsigned x0, unsigned x1, unsigned x2, unsigned x3, bool valid) {
         // S5/S7 fast path: e = -lg2 u (the ln 2 factor cancels in the normalisation)
         const float e0 = sb_neg_lg2(x0), e1 = sb_neg_lg2(x1), e2 = sb_neg_lg2(x2), e3 = sb_neg_lg2(x3);
         const float sum = ((e0 + e1) + e2) + e3;
@@ -411,7 +411,68 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
           gsum += (double)gf;
           hf = gf = 0.f;
         }
+      };
+      // Empty space per point: a point whose cell block (the
+      // 4^3 voxels around floor(p), which hold its exact cell's corners while the
+      // fp32 error is <= 1/2) is quiet at Rq has a = b = 0 and no distance < r,
+      // so h = g = 0: it is counted (N) and not evaluated.  The others queue their
+      // Sobol state and are evaluated 32 at a time.  The fp64 test hook keeps every
+      // point on the evaluation path.
+      const int Rq = sobol_radius(R);
+      const unsigned char* qc =
+          (!A.sobol_force_exact && Rq <= kQuietRmax) ? (side == 0 ? V.qcell[0] : V.qcell[1]) : nullptr;
+      int qn = 0;  // queued points (warp-uniform)
+      int nquiet = 0;
+      // S2: x(g(s0)) ^ x(g(lane)) ^ mask, updated per step: for s0 = 32 m,
+      // g(s0 + 32) ^ g(s0) = 2^4 ^ 2^(5 + ctz(m + 1)), so two direction numbers
+      // per dimension change (warp-uniform)
+      unsigned x0 = m0, x1 = m1, x2 = m2, x3 = m3;
+      const int Ni = (int)N;  // < 2^31: k_setup flags larger counts (DOMAIN) and clears the side
+#pragma unroll 1
+      for (int s0 = 0;; s0 += 32) {
+        const bool more = s0 < Ni;  // warp-uniform
+        if (more) {
+          if (s0 > 0) {
+            const int b = 4 + __ffs(s0 >> 5);  // 5 + ctz(m + 1), m + 1 = s0 / 32
+            x0 ^= sV[0][4] ^ sV[0][b];
+            x1 ^= sV[1][4] ^ sV[1][b];
+            x2 ^= sV[2][4] ^ sV[2][b];
+            x3 ^= sV[3][4] ^ sV[3][b];
+          }
+          const bool valid = s0 + lane < Ni;
+          bool live = valid;
+          if (qc) {  // item-uniform
+            const float e0 = sb_neg_lg2(x0), e1 = sb_neg_lg2(x1), e2 = sb_neg_lg2(x2), e3 = sb_neg_lg2(x3);
+            const float rs = __frcp_rn(((e0 + e1) + e2) + e3);
+            const float l1 = e1 * rs, l2 = e2 * rs, l3 = e3 * rs;
+            const float eps = fmaf(R.epsA, rs, R.epsB);
+            const float px = fmaf(l3, R.D[2][0], fmaf(l2, R.D[1][0], fmaf(l1, R.D[0][0], R.x0[0])));
+            const float py = fmaf(l3, R.D[2][1], fmaf(l2, R.D[1][1], fmaf(l1, R.D[0][1], R.x0[1])));
+            const float pz = fmaf(l3, R.D[2][2], fmaf(l2, R.D[1][2], fmaf(l1, R.D[0][2], R.x0[2])));
+            const int cx = min(max((int)(floorf(px) + R.i0[0]), 0), V.nx - 1);
+            const int cy = min(max((int)(floorf(py) + R.i0[1]), 0), V.ny - 1);
+            const int cz = min(max((int)(floorf(pz) + R.i0[2]), 0), V.nz - 1);
+            const bool quiet = eps <= 0.5f && (int)__ldg(&qc[(cz * V.ny + cy) * V.nx + cx]) >= Rq;
+            nquiet += (valid && quiet) ? 1 : 0;
+            live = valid && !quiet;
+          }
+          const unsigned lm = __ballot_sync(FULLMASK, live);
+          if (live) S.qx[qn + __popc(lm & ((1u << lane) - 1u))] = make_uint4(x0, x1, x2, x3);
+          qn += __popc(lm);
+        }
+        // evaluate 32 queued points, or at the end what is left (one call site)
+        if (qn >= 32 || (!more && qn > 0)) {
+          const int take = min(qn, 32);
+          qn -= take;
+          __syncwarp();
+          const uint4 q = S.qx[qn + min(lane, take - 1)];
+          __syncwarp();
+          point(q.x, q.y, q.z, q.w, lane < take);
+        }
+        if (!more) break;
       }
+      nquiet = warp_sum_i(nquiet);
+      if (lane == 0) S.stat[3] += nquiet;
       hsum += (double)hf;
       gsum += (double)gf;
     }
