@@ -299,7 +299,9 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
     const int sol = (int)(rem - (long long)es * A.P);
     const int e = A.sched[es];
     const long long i = ((long long)ver * A.n_entries + e) * A.P + sol;
-    double hsum = 0.0, gsum = 0.0;
+    // per-lane fp64 sums in local memory, touched once per flush (as in k_raster)
+    double hg_local[2] = {0.0, 0.0};
+    volatile double* hg = hg_local;
     long long n_tot = 0, n_side0 = 0;
     int nb = 0;
 #pragma unroll 1
@@ -407,8 +409,8 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
           }
         }
         if ((++step & 15) == 0) {
-          hsum += (double)hf;
-          gsum += (double)gf;
+          hg[0] = hg[0] + (double)hf;
+          hg[1] = hg[1] + (double)gf;
           hf = gf = 0.f;
         }
       };
@@ -473,12 +475,12 @@ __global__ void __launch_bounds__(kSobolThreads, 1) k_sobol(const EvalArgs A) {
       }
       nquiet = warp_sum_i(nquiet);
       if (lane == 0) S.stat[3] += nquiet;
-      hsum += (double)hf;
-      gsum += (double)gf;
+      hg[0] = hg[0] + (double)hf;
+      hg[1] = hg[1] + (double)gf;
     }
     HGN out;
-    out.h = warp_sum_d(hsum);
-    out.g = warp_sum_d(gsum);
+    out.h = warp_sum_d(hg[0]);
+    out.g = warp_sum_d(hg[1]);
     out.n = n_tot;
     out.n0 = n_side0;
     const int nb_w = warp_sum_i(nb);
