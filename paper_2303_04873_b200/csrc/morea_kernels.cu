@@ -799,7 +799,7 @@ struct Acc {
   volatile double* hg;
   float hf;     // fp32 partial sum of h over the last < 16 steps (flushed into h)
   float gf;     // fp32 partial sum of guidance terms since the last flush (into g)
-  int n, nb;    // samples, band entries
+  int n;        // samples
   int qn;       // band entries in the per-warp queue (warp-uniform)
 };
 
@@ -891,7 +891,6 @@ struct Sample {
   __device__ __forceinline__ void enqueue(unsigned bm, int lin, float u, float v, float fx, float fy,
                                           float fz, int s) {
     const int lane = threadIdx.x & 31;
-    acc.nb += __popc(bm);
     while (true) {
       const unsigned take = __ballot_sync(FULLMASK, bm != 0u);
       if (!take) break;
@@ -918,6 +917,7 @@ struct Sample {
       acc.qn += __popc(take);
       if (__all_sync(FULLMASK, acc.qn >= 32)) {  // warp-uniform (VOTE): no BSSY
         acc.qn -= 32;
+        if (lane == 0) S.stat[1] += 32;  // band entries: each queued entry is evaluated once
         __syncwarp();
         const float4 ea = S.qa[acc.qn + lane];
         const int2 eb = S.qb[acc.qn + lane];
@@ -958,6 +958,7 @@ struct Sample {
   __device__ __forceinline__ void drain(int s) {
     const int lane = threadIdx.x & 31;
     __syncwarp();
+    if (lane == 0) S.stat[1] += (unsigned long long)acc.qn;
     if (lane < acc.qn) {
       const float4 ea = S.qa[lane];
       const int2 eb = S.qb[lane];
@@ -1186,7 +1187,7 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
     MOREA_CHECK(e >= 0 && e < A.n_entries && v < A.n_raster_versions);
     const long long i = ((long long)v * A.n_entries + e) * A.P + sol;
     double hg_local[2] = {0.0, 0.0};
-    Acc acc{hg_local, 0.f, 0.f, 0, 0, 0};
+    Acc acc{hg_local, 0.f, 0.f, 0, 0};
     int n_side0 = 0;
 #pragma unroll 1
     for (int side = 0; side < 2; side++) {
@@ -1200,11 +1201,9 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
     out.g = warp_sum_d(acc.hg[1]);
     out.n = warp_sum_i(acc.n);
     out.n0 = warp_sum_i(n_side0);
-    const int nb = warp_sum_i(acc.nb);
     if (lane == 0) {
       A.hgn[i] = out;
       S.stat[0] += out.n;
-      S.stat[1] += nb;
       S.stat[2] += 1;
       debug_count_item(A);
     }
