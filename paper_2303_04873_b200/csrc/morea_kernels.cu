@@ -533,42 +533,39 @@ __device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, boo
   }
 }
 
-// Conservative y range of the tet's cross-section with the plane z (exact
-// vertex coordinates; edge intersections in fp32 with a 1e-3 voxel margin).
-__device__ __noinline__ void slice_y_range(const SideRec& R, int z, int& ylo, int& yhi) {
+// Conservative y range of the tet's cross-section with the plane z, from the
+// item's edge table (WarpSmem::edge, built by load_rec: per edge its z range, the
+// y at its lower end and dy/dz).  The exact vertex coordinates are fp32-exact, so
+// an edge point y = y_lo + (z - z_lo) s errs by |y - y_lo| 2^-24 (the rounded
+// slope) plus one rounding, < 2e-4 voxels: inside the 1e-3 voxel margin.
+template <class WS>
+__device__ __forceinline__ int2 slice_y_range(const WS& S, int z) {
   float ymin = 3.0e38f, ymax = -3.0e38f;
   const float zf = (float)z;
 #pragma unroll
-  for (int i = 0; i < 4; i++) {
-#pragma unroll
-    for (int j = i + 1; j < 4; j++) {
-      const float zi = R.vz[i], zj = R.vz[j];
-      const float lo = fminf(zi, zj), hi = fmaxf(zi, zj);
-      if (zf < lo || zf > hi) continue;
-      float y0, y1;
-      if (hi > lo) {
-        const float t = __fdividef(zf - zi, zj - zi);  // ~2 ulp: covered by the 1e-3 margin
-        y0 = y1 = fmaf(t, R.vy[j] - R.vy[i], R.vy[i]);
-      } else {
-        y0 = R.vy[i];
-        y1 = R.vy[j];
-      }
-      ymin = fminf(ymin, fminf(y0, y1));
-      ymax = fmaxf(ymax, fmaxf(y0, y1));
-    }
+  for (int e = 0; e < 6; e++) {
+    const float4 a = S.edge[e];  // (z_lo, z_hi, y at z_lo, dy/dz; 0 for a horizontal edge)
+    const float b = S.edge_y1[e];  // horizontal edge: the other end's y; else NaN
+    const bool in = zf >= a.x && zf <= a.y;
+    const float y = fmaf(zf - a.x, a.w, a.z);
+    // fminf / fmaxf return the non-NaN operand
+    ymin = in ? fminf(ymin, fminf(y, b)) : ymin;
+    ymax = in ? fmaxf(ymax, fmaxf(y, b)) : ymax;
   }
-  ylo = max(R.lo[1], (int)ceilf(fmaxf(ymin - 1e-3f, -1.0e6f)));
-  yhi = min(R.hi[1], (int)floorf(fminf(ymax + 1e-3f, 1.0e6f)));
+  return make_int2(max(S.R.lo[1], (int)ceilf(fmaxf(ymin - 1e-3f, -1.0e6f))),
+                   min(S.R.hi[1], (int)floorf(fminf(ymax + 1e-3f, 1.0e6f))));
 }
 
 constexpr int kQueueCap = 64;     // < 32 pending + one round of <= 32
 // per-warp shared memory <= 3.5 KB, so the 28-warp block stays <= 99 KB (the
 // 100 KB carve-out step; see kRasterDynSmem)
-constexpr int kStartWords = 64;  // row-start bitmap window: 2048 samples
+constexpr int kStartWords = 32;  // row-start bitmap window: 1024 samples
 
 struct WarpSmem {
   SideRec R;
   unsigned starts[kStartWords];  // row-start bitmap of the current row chunk
+  float4 edge[6];    // the item side's edges for slice y ranges (load_rec, slice_y_range)
+  float edge_y1[6];
   int4 row_a[32];    // (exclusive prefix, linear index of row start, dx0, dy0 as float bits)
   float4 row_b[32];  // (dz0, xl, y, z): fp32 displacement z at the row start, row start as floats
   float4 sc0, sc1;   // per-side sample constants (see Sample)
@@ -603,8 +600,8 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
   const unsigned lt_mask = (1u << lane) - 1u;
   for (int z0 = R.lo[2]; z0 <= R.hi[2]; z0 += 32) {
     const int zl = z0 + lane;
-    int ylo, yhi;
-    slice_y_range(R, zl, ylo, yhi);  // every lane (no divergent call); masked below
+    const int2 yr = slice_y_range(S, zl);  // every lane; masked below
+    const int ylo = yr.x, yhi = yr.y;
     const int cnt = zl <= R.hi[2] ? max(0, yhi - ylo + 1) : 0;
     const int zincl = warp_incl_scan(cnt, lane);
     const int nrows = __shfl_sync(FULLMASK, zincl, 31);
@@ -636,6 +633,12 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       const int z = z0 + (sl.y >> 16);
       const int y = (sl.y & 0xffff) + (r - sl.x);
       const bool rv = r < nrows;
+      // the row's hull (quiet rows, below) is loaded before the interval is
+      // computed, so its latency overlaps the interval arithmetic
+      const int qo = F::kQuiet ? f.quiet_off() : -1;  // item-uniform; -1: radius beyond the hulls
+      short2 hb = make_short2(0, -1);
+      if (F::kQuiet && qo >= 0)  // unconditional load (lanes past the chunk read the plane's first row)
+        hb = f.quiet_hull(qo + (rv ? z * ny + y : 0));
       row_interval(R, y, z, rv, xl, xh);  // every lane (warp-collective)
       const int len_all = rv ? max(0, xh - xl + 1) : 0;
       // quiet rows (empty space): every voxel of the row is background
@@ -643,16 +646,9 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       // each sample's h is exactly 0 -- counted, not swept.  The row is quiet when
       // [xl, xh] lies outside the hull of the image row's non-quiet voxels.
       int len = len_all;
-      if (F::kQuiet) {
-        const int qo = f.quiet_off();  // item-uniform; -1: radius beyond the hulls
-        if (qo >= 0) {
-          // unconditional load (lanes past the chunk read the plane's first row)
-          const short2 hb = f.quiet_hull(qo + (rv ? z * ny + y : 0));
-          if (len_all > 0 && (xh < hb.x || xl > hb.y)) {
-            len = 0;
-            f.quiet_row((z * ny + y) * nx + xl, len_all);  // 2 V < 2^31 (own-record index is an int)
-          }
-        }
+      if (F::kQuiet && qo >= 0 && len_all > 0 && (xh < hb.x || xl > hb.y)) {
+        len = 0;
+        f.quiet_row((z * ny + y) * nx + xl, len_all);  // 2 V < 2^31 (own-record index is an int)
       }
       const int incl = warp_incl_scan(len, lane);
       const int total = __shfl_sync(FULLMASK, incl, 31);
@@ -698,8 +694,8 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
         const int nw = min(kStartWords, (total - base + 31) >> 5);
         __syncwarp();
         // clear the whole bitmap window: one 16-byte store per lane
-        static_assert(kStartWords == 64, "one uint2 per lane clears the window");
-        reinterpret_cast<uint2*>(S.starts)[lane] = make_uint2(0u, 0u);
+        static_assert(kStartWords == 32, "one word per lane clears the window");
+        S.starts[lane] = 0u;
         __syncwarp();
         if (len > 0 && start >= base && start < base + 32 * kStartWords)
           atomicOr(&S.starts[(start - base) >> 5], 1u << (start & 31));
@@ -863,7 +859,11 @@ struct Sample {
   __device__ __forceinline__ void entry(float u, float v, float fx, float fy, float fz, int lin,
                                         int i, int s) {
     const int o = 1 - s;
-    const float d = __ldg(&(s == 0 ? V.dmap[0] : V.dmap[1])[(long long)(i - s) * V.V + lin]);
+    // map i of side s at voxel q = lin - s V: element i V + q < K V <= 8 * 768^3 < 2^32
+    // (morea_load_images bounds), so the index is computed in 32-bit unsigned
+    // arithmetic (mod 2^32, exact)
+    const unsigned di = (unsigned)(i - s) * (unsigned)V.V + (unsigned)lin;
+    const float d = __ldg(&(s == 0 ? V.dmap[0] : V.dmap[1])[di]);
     float e[8];
     if (TEX) {
       // u = i0_x + uoff0 + o fnxp (texel of I_o); map (o, i) is volume o K + i of texM
@@ -1076,6 +1076,20 @@ __device__ __forceinline__ void load_rec(WarpSmem& S, const SideRec* src, int la
   __syncwarp();
   if (lane < kVec)
     reinterpret_cast<int4*>(&S.R)[lane] = __ldg(reinterpret_cast<const int4*>(src) + lane);
+  __syncwarp();
+  // edge table for slice_y_range: lane e < 6 takes edge (0,1) (0,2) (0,3) (1,2) (1,3) (2,3)
+  if (lane < 6) {
+    const int i = lane < 3 ? 0 : (lane < 5 ? 1 : 2);
+    const int j = lane < 3 ? lane + 1 : (lane < 5 ? lane - 1 : 3);
+    float zi = S.R.vz[i], zj = S.R.vz[j], yi = S.R.vy[i], yj = S.R.vy[j];
+    if (zj < zi) {
+      const float tz = zi, ty = yi;
+      zi = zj; yi = yj; zj = tz; yj = ty;
+    }
+    const bool flat = !(zj > zi);
+    S.edge[lane] = make_float4(zi, zj, yi, flat ? 0.f : (yj - yi) / (zj - zi));
+    S.edge_y1[lane] = flat ? yj : __int_as_float(0x7fffffff);  // NaN: no second end
+  }
   __syncwarp();
 }
 
