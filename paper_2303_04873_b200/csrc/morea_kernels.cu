@@ -577,12 +577,14 @@ struct WarpSmem {
   unsigned char qi[kQueueCap];  // pair i
 };
 
-__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+// inclusive warp prefix sum; the shuffle's own in-range predicate guards the add
+// (no per-step lane compare and select)
+__device__ __forceinline__ int warp_incl_scan(int v, int) {
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(FULLMASK, v, o);
-    if (lane >= o) v += t;
-  }
+  for (int o = 1; o < 32; o <<= 1)
+    asm("{\n .reg .s32 t;\n .reg .pred p;\n shfl.sync.up.b32 t|p, %0, %1, 0, -1;\n @p add.s32 %0, %0, t;\n}"
+        : "+r"(v)
+        : "r"(o));
   return v;
 }
 
@@ -811,7 +813,7 @@ struct Sample {
   int side;           // runtime side when SIDE_T < 0 (warp-uniform)
   float* dump_h;      // DUMP (test hook morea_sample_map): per-voxel h and fg of this side
   unsigned char* dump_fg;
-  int qoff;           // row hulls of this side at the item's radius: V.qhull[side] + qoff
+  int qoff;           // row hulls of this side at the item's radius: V.qhull[0] + qoff
                       // + z ny + y; -1 when there are none (empty-space skip off)
   // CLAMP: some position of the item may leave the range the gather covers
   // exactly, apply the O5 clamp (a separate instantiation: no predicated clamp
@@ -934,7 +936,7 @@ struct Sample {
   __device__ __forceinline__ int quiet_off() const { return qoff; }
   __device__ __forceinline__ short2 quiet_hull(int idx) const {
     const int SIDE = SIDE_T >= 0 ? SIDE_T : side;
-    return __ldg(&(SIDE == 0 ? V.qhull[0] : V.qhull[1])[idx]);
+    return __ldg(&V.qhull[0][idx]);  // qoff carries the side (qhull[1] follows qhull[0])
   }
   // samples of a chunk's quiet rows (profiling; lane 0, per-warp shared counter)
   __device__ __forceinline__ void count_quiet(int n) { S.stat[3] += (unsigned long long)n; }
@@ -1108,7 +1110,12 @@ __device__ __forceinline__ void raster_side(const Volumes& V, WarpSmem& S, int l
   // [0, n-1) for plain loads, (-1, n) on the edge-padded textures (warp-uniform)
   const int loff = (SIDE_T >= 0 ? SIDE_T : side) * (int)V.V;
   const int qR = (R.flags >> 8) & 0xff;  // empty-space radius of the item (k_setup)
-  const int qoff = (V.qhull[0] && qR <= kQuietRmax) ? (qR - kQuietRmin) * V.ny * V.nz : -1;
+  // row hulls of this side at radius qR, as an offset from V.qhull[0] (the two sides'
+  // tables are contiguous: qhull[1] = qhull[0] + nR ny nz, morea_api.cu)
+  const int nR = kQuietRmax - kQuietRmin + 1;
+  const int qoff = (V.qhull[0] && qR <= kQuietRmax)
+                       ? ((SIDE_T >= 0 ? SIDE_T : side) * nR + (qR - kQuietRmin)) * V.ny * V.nz
+                       : -1;
   if ((R.flags & ((TEX && kTexPad) ? 8 : 2)) == 0) {
     Sample<TEX, SIDE_T, true, DUMP> f{V, R, S, S.sc0, S.sc1, acc, side, dump_h, dump_fg, qoff};
     raster(R, V.nx, V.ny, loff, S, lane, f);
