@@ -30,6 +30,7 @@
 // Further sm_100a kernels: morea_sobol*.cuh (NEXT-1 Sobol sampler),
 // morea_repair.cuh (NEXT-2 fold repair), morea_mix.cuh (NEXT-3 optimal
 // mixing), morea_export.cuh (NEXT-4 object counts and DVF).
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -151,8 +152,11 @@ __device__ void build_side_ordered(const int Q[4][3], const int Qo[4][3], int nx
     // row crossing x*(y, z): 1024 (n0 x + n1 y + n2 z) = cst, evaluated in fp32 per row
     if (n0 != 0) {
       const i128 num = (i128)G.cst[k] - (i128)1024 * ((i128)n1 * G.lo[1] + (i128)n2 * G.lo[2]);
-      const double fa = (double)num / (1024.0 * (double)n0);
-      const double fb = -(double)n1 / (double)n0, fc = -(double)n2 / (double)n0;
+      // one fp64 reciprocal per face: the fp32 coefficients are within 2^-24 (1 + 2^-50)
+      // of the exact ratios, inside the crossing bound thr below (4x the fp32 worst case)
+      const double rn0 = 1.0 / (double)n0;
+      const double fa = (double)num * rn0 * (1.0 / 1024.0);
+      const double fb = -(double)n1 * rn0, fc = -(double)n2 * rn0;
       G.face[k].x = (float)fa;
       G.face[k].y = (float)fb;
       G.face[k].z = (float)fc;
@@ -181,9 +185,11 @@ __device__ void build_side_ordered(const int Q[4][3], const int Qo[4][3], int nx
     double Aab[3];
 #pragma unroll
     for (int b = 0; b < 3; b++) {
-      i128 num = 0;
+      // |n_kb| < 2^41, |U_ka| < 2^20 (Q.10 window): each product < 2^61, the sum of
+      // four < 2^63, so int64 is exact
+      i64 num = 0;
 #pragma unroll
-      for (int k = 0; k < 4; k++) num += (i128)G.nrm[k][b] * (i128)G.U[k][a];
+      for (int k = 0; k < 4; k++) num += G.nrm[k][b] * (i64)G.U[k][a];
       if (num != 0) exact = false;
       Aab[b] = (double)num * inv_det;
       G.A[a][b] = (float)Aab[b];
@@ -347,86 +353,117 @@ __device__ double magnitude(const int Q[2][4][3], double c, const double sp2[3],
 #include "morea_sobol_setup.cuh"
 
 // ---------------------------------------------------------------------------
-// k_setup: one thread per (version, canonical entry, solution).
+// k_setup: one thread per (version, canonical entry, solution).  The SideRecs are
+// built in a per-warp shared-memory stage (a 400-byte slot per lane: bank-conflict
+// free 16-byte stores) and copied out by the whole warp, side by side: the 32
+// records of one side of a warp's items land as 384-byte runs (coalesced) instead of
+// one thread storing 24 scattered 16-byte words.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128, 3) k_setup(const EvalArgs A) {
+constexpr int kSetupThreads = 128;
+constexpr int kStageVec = (int)(sizeof(SideRec) / 16) + 1;  // 25 int4 per lane slot
+constexpr size_t kSetupSmem = (size_t)kSetupThreads * kStageVec * 16;
+
+__global__ void __launch_bounds__(kSetupThreads, 3) k_setup(const EvalArgs A) {
+  extern __shared__ int4 setup_stage[];
+  const int lane = threadIdx.x & 31;
+  int4* stage = setup_stage + (threadIdx.x >> 5) * 32 * kStageVec;
+  SideRec& G = *reinterpret_cast<SideRec*>(stage + lane * kStageVec);
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long per_v = (long long)A.n_entries * A.P;
-  if (i >= per_v * A.n_setup_versions) return;
-  const int v = (int)(i / per_v);
-  const long long rem = i - (long long)v * per_v;
-  const int e = (int)(rem / A.P);
-  const int sol = (int)(rem - (long long)e * A.P);
-  const int tet = A.canon_tet ? A.canon_tet[e] : e;
-  const int4 none = make_int4(-1, -1, -1, -1);
-  const int4 slots = (v == 0 && A.canon_slots) ? A.canon_slots[e] : none;
   int Q[2][4][3];
-  Scal sc;
-  sc.m = sc.sev = 0.0;
-  sc.folds = sc.flags = 0;
-  sc.pad[0] = sc.pad[1] = 0;
-  const bool raster = v < A.n_raster_versions;
-  if (!load_tet(A, sol, A.mesh.tets[tet], slots, Q)) {
-    sc.flags = 1;  // domain: the tet contributes nothing
-    A.scal[i] = sc;
-    if (raster) {
-      if (A.sampler == 1) {
-        A.sgeom[2 * i].flags = 0;
-        A.sgeom[2 * i + 1].flags = 0;
-      } else {
-        A.geom[2 * i].flags = 0;
-        A.geom[2 * i + 1].flags = 0;
+  int mode = 0;  // SideRec path: 1 = build both sides, 2 = domain error (flags 0), 0 = none
+  if (i < per_v * A.n_setup_versions) {
+    const int v = (int)(i / per_v);
+    const long long rem = i - (long long)v * per_v;
+    const int e = (int)(rem / A.P);
+    const int sol = (int)(rem - (long long)e * A.P);
+    const int tet = A.canon_tet ? A.canon_tet[e] : e;
+    const int4 none = make_int4(-1, -1, -1, -1);
+    const int4 slots = (v == 0 && A.canon_slots) ? A.canon_slots[e] : none;
+    Scal sc;
+    sc.m = sc.sev = 0.0;
+    sc.folds = sc.flags = 0;
+    sc.pad[0] = sc.pad[1] = 0;
+    const bool raster = v < A.n_raster_versions;
+    if (!load_tet(A, sol, A.mesh.tets[tet], slots, Q)) {
+      sc.flags = 1;  // domain: the tet contributes nothing
+      A.scal[i] = sc;
+      if (raster) {
+        if (A.sampler == 1) {
+          A.sgeom[2 * i].flags = 0;
+          A.sgeom[2 * i + 1].flags = 0;
+        } else {
+          mode = 2;
+        }
       }
-    }
-    return;
-  }
-  const Volumes& V = A.vol;
-  const double sp2[3] = {V.sp[0] * V.sp[0], V.sp[1] * V.sp[1], V.sp[2] * V.sp[2]};
-  sc.m = magnitude(Q, (double)A.mesh.cdelta[tet], sp2, A.mesh.spoke_mode);
-  const int ref = A.mesh.ref[tet];
+    } else {
+      const Volumes& V = A.vol;
+      const double sp2[3] = {V.sp[0] * V.sp[0], V.sp[1] * V.sp[1], V.sp[2] * V.sp[2]};
+      sc.m = magnitude(Q, (double)A.mesh.cdelta[tet], sp2, A.mesh.spoke_mode);
+      const int ref = A.mesh.ref[tet];
 #pragma unroll
-  for (int s = 0; s < 2; s++) {
-    const i64 det = det3(Q[s]);
-    const int sg = (det > 0) - (det < 0);
-    if (sg != ref) {  // O2: sign change w.r.t. the reference sign; zero counts as a fold
-      sc.folds += 1;
-      const double vol = (double)(det < 0 ? -det : det) / (6.0 * 1073741824.0);
-      sc.sev += vol * V.sp[0] * V.sp[1] * V.sp[2];
+      for (int s = 0; s < 2; s++) {
+        const i64 det = det3(Q[s]);
+        const int sg = (det > 0) - (det < 0);
+        if (sg != ref) {  // O2: sign change w.r.t. the reference sign; zero counts as a fold
+          sc.folds += 1;
+          const double vol = (double)(det < 0 ? -det : det) / (6.0 * 1073741824.0);
+          sc.sev += vol * V.sp[0] * V.sp[1] * V.sp[2];
+        }
+      }
+      if (raster && A.sampler == 1) {
+#pragma unroll 1
+        for (int s = 0; s < 2; s++) {
+          SobolRec SG;
+          build_sobol(Q[s], Q[1 - s], V, A.rate, SG);
+          if (SG.N > 0x7fffffffLL) {  // beyond the 32-bit point counter: flagged like a domain
+            sc.flags = 1;             // error (objectives NaN), the side contributes nothing
+            SG.flags = 0;
+          }
+          const int4* src = reinterpret_cast<const int4*>(&SG);
+          int4* dst = reinterpret_cast<int4*>(&A.sgeom[2 * i + s]);
+#pragma unroll
+          for (int t = 0; t < (int)(sizeof(SobolRec) / 16); t++) dst[t] = src[t];
+        }
+      } else if (raster) {
+        mode = 1;
+      }
+      A.scal[i] = sc;
     }
   }
-  if (!raster) {
-    A.scal[i] = sc;
-    return;
-  }
+  if (A.sampler == 1) return;  // kernel-uniform
+  const unsigned wm = __ballot_sync(FULLMASK, mode != 0);
+  if (!wm) return;  // warp-uniform
+  const long long i0 = i - lane;  // the warp's first item
 #pragma unroll 1
   for (int s = 0; s < 2; s++) {
-    if (A.sampler == 1) {
-      SobolRec G;
-      build_sobol(Q[s], Q[1 - s], V, A.rate, G);
-      if (G.N > 0x7fffffffLL) {  // beyond the 32-bit point counter: flagged like a domain
-        sc.flags = 1;            // error (objectives NaN), the side contributes nothing
-        G.flags = 0;
-      }
-      const int4* src = reinterpret_cast<const int4*>(&G);
-      int4* dst = reinterpret_cast<int4*>(&A.sgeom[2 * i + s]);
-#pragma unroll
-      for (int t = 0; t < (int)(sizeof(SobolRec) / 16); t++) dst[t] = src[t];
-    } else {
-      SideRec G;
-      build_side(Q[s], Q[1 - s], V.nx, V.ny, V.nz, G);
-      const int4* src = reinterpret_cast<const int4*>(&G);
-      int4* dst = reinterpret_cast<int4*>(&A.geom[2 * i + s]);
-#pragma unroll
-      for (int t = 0; t < (int)(sizeof(SideRec) / 16); t++) dst[t] = src[t];
+    if (mode == 1) build_side(Q[s], Q[1 - s], A.vol.nx, A.vol.ny, A.vol.nz, G);
+    else if (mode == 2) G.flags = 0;
+    __syncwarp();
+    // record j of the stage -> A.geom[2 (i0 + j) + s], 24 int4 each, 32 lanes at a time
+    for (int m = lane; m < 32 * (kStageVec - 1); m += 32) {
+      const int j = m / (kStageVec - 1), t = m - j * (kStageVec - 1);
+      if (wm >> j & 1u) reinterpret_cast<int4*>(&A.geom[2 * (i0 + j) + s])[t] = stage[j * kStageVec + t];
     }
+    __syncwarp();
   }
-  A.scal[i] = sc;
 }
 
 cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s) {
   const long long n = (long long)a.n_setup_versions * a.n_entries * a.P;
   if (n == 0) return cudaSuccess;
-  k_setup<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(a);
+  // the 50 KB stage needs the opt-in above 48 KB, once per device
+  static std::atomic<unsigned long long> attr_set{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr_set.load() & bit)) {
+    e = cudaFuncSetAttribute(k_setup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSetupSmem);
+    if (e != cudaSuccess) return e;
+    attr_set.fetch_or(bit);
+  }
+  k_setup<<<(unsigned)((n + kSetupThreads - 1) / kSetupThreads), kSetupThreads, kSetupSmem, s>>>(a);
   return cudaGetLastError();
 }
 
