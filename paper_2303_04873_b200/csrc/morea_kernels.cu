@@ -440,10 +440,14 @@ __global__ void __launch_bounds__(kSetupThreads, 3) k_setup(const EvalArgs A) {
     if (mode == 1) build_side(Q[s], Q[1 - s], A.vol.nx, A.vol.ny, A.vol.nz, G);
     else if (mode == 2) G.flags = 0;
     __syncwarp();
-    // record j of the stage -> A.geom[2 (i0 + j) + s], 24 int4 each, 32 lanes at a time
+    // record j of the stage -> A.geom[2 (i0 + j) + s], 24 int4 each, 32 lanes at a time:
+    // word m = 24 j + t sits at stage[m + j] and at byte 16 m + 384 j from side s's
+    // first record (records of one side are 768 bytes apart)
+    char* const dst0 = reinterpret_cast<char*>(&A.geom[2 * i0 + s]);
+#pragma unroll 4
     for (int m = lane; m < 32 * (kStageVec - 1); m += 32) {
-      const int j = m / (kStageVec - 1), t = m - j * (kStageVec - 1);
-      if (wm >> j & 1u) reinterpret_cast<int4*>(&A.geom[2 * (i0 + j) + s])[t] = stage[j * kStageVec + t];
+      const int j = m / (kStageVec - 1);
+      if (wm >> j & 1u) *reinterpret_cast<int4*>(dst0 + (16 * m + 384 * j)) = stage[m + j];
     }
     __syncwarp();
   }
