@@ -1075,7 +1075,7 @@ struct Sample {
       dump_fg[q] = fg ? 1 : 0;
     }
     // a6: band entries go to the per-warp queue, evaluated 32 at a time
-    if (__reduce_or_sync(FULLMASK, bm)) enqueue(bm, lin, u, v, fx, fy, fz, SIDE);
+    if (__any_sync(FULLMASK, bm != 0u)) enqueue(bm, lin, u, v, fx, fy, fz, SIDE);
   }
 };
 
