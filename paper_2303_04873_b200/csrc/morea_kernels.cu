@@ -695,12 +695,12 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       }
       const int incl = warp_incl_scan(len, lane);
       const int total = __shfl_sync(FULLMASK, incl, 31);
-      const int tot_all = F::kQuiet ? (int)__reduce_add_sync(FULLMASK, (unsigned)len_all) : total;
-      if (F::kQuiet && lane == 0) f.count_quiet(tot_all - total);
-      if (total == 0) {
-        f.count_only(lane == 0 ? tot_all : 0);
-        continue;
-      }
+      // every sample counts (n), per lane: the item's warp reduction sums the lanes.
+      // Quiet samples (profiling) = the item's samples - the swept ones: -total here,
+      // +n at the item's end (k_raster)
+      f.count_only(len_all);
+      if (F::kQuiet && lane == 0) f.count_quiet(-total);
+      if (total == 0) continue;
       const unsigned ne = __ballot_sync(FULLMASK, len > 0);
       const int start = incl - len;
       __syncwarp();
@@ -725,7 +725,6 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
               "f"((float)y), "f"((float)z)
             : "memory");
       }
-      f.count_only(lane == 0 ? tot_all : 0);
       // Sweep in windows of 32 kStartWords samples.  The bitmap holds the row
       // starts of the window (bit s of word s/32); a lane's row is the number of
       // starts <= its sample index, minus one.  Past the end that is the last row
@@ -1267,6 +1266,7 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
       A.hgn[i] = out;
       S.stat[0] += out.n;
       S.stat[2] += 1;
+      S.stat[3] += out.n;  // quiet samples: the chunks subtracted the swept ones
       debug_count_item(A);
     }
   }
