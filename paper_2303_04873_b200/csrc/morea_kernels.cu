@@ -1019,7 +1019,7 @@ struct Sample {
     MOREA_CHECK(!valid || (lin >= (long long)SIDE * V.V && lin < (long long)(SIDE + 1) * V.V));
     const uint2 own = __ldg(&V.own[0][lin]);  // lin = SIDE V + q
     const float a = __uint_as_float(own.x);
-    const unsigned bm = valid ? (own.y & 0xffu) : 0u;
+    const unsigned bm = valid ? own.y : 0u;  // the band byte (k_own_records: upper bits 0)
     const float kf = (float)k;
     const float4 s0 = sc0;
     const float dx = fmaf(s0.x, kf, __int_as_float(ra.z)), dy = fmaf(s0.y, kf, __int_as_float(ra.w)),
