@@ -698,6 +698,11 @@ int morea_create(int cuda_device, void* cuda_stream, morea_ctx** out) {
     ctx->own_stream = true;
   }
   cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, cuda_device);
+  if (setup_prepare() != cudaSuccess) {
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return MOREA_ECUDA;
+  }
   ctx->blocks_per_sm = raster_blocks_per_sm(false);
   ctx->blocks_per_sm_tex = raster_blocks_per_sm(true);
   ctx->blocks_per_sm_sobol = sobol_blocks_per_sm(false);

@@ -195,6 +195,7 @@ cudaError_t launch_zero_radius(const float* I, int nx, int ny, int nz, unsigned 
 cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s);
 cudaError_t launch_raster(const EvalArgs& a, int grid, cudaStream_t s);
 int raster_blocks_per_sm(bool tex);
+cudaError_t setup_prepare();  // k_setup's dynamic shared-memory opt-in (current device)
 int raster_block_warps();
 cudaError_t launch_sobol(const EvalArgs& a, int grid, cudaStream_t s);
 int sobol_blocks_per_sm(bool tex);

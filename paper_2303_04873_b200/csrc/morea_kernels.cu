@@ -30,7 +30,6 @@
 // Further sm_100a kernels: morea_sobol*.cuh (NEXT-1 Sobol sampler),
 // morea_repair.cuh (NEXT-2 fold repair), morea_mix.cuh (NEXT-3 optimal
 // mixing), morea_export.cuh (NEXT-4 object counts and DVF).
-#include <atomic>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -453,20 +452,14 @@ __global__ void __launch_bounds__(kSetupThreads, 3) k_setup(const EvalArgs A) {
   }
 }
 
+// the 50 KB stage needs the opt-in above 48 KB (morea_create, per context's device)
+cudaError_t setup_prepare() {
+  return cudaFuncSetAttribute(k_setup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSetupSmem);
+}
+
 cudaError_t launch_setup(const EvalArgs& a, cudaStream_t s) {
   const long long n = (long long)a.n_setup_versions * a.n_entries * a.P;
   if (n == 0) return cudaSuccess;
-  // the 50 KB stage needs the opt-in above 48 KB, once per device
-  static std::atomic<unsigned long long> attr_set{0};
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  const unsigned long long bit = 1ull << (dev & 63);
-  if (!(attr_set.load() & bit)) {
-    e = cudaFuncSetAttribute(k_setup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSetupSmem);
-    if (e != cudaSuccess) return e;
-    attr_set.fetch_or(bit);
-  }
   k_setup<<<(unsigned)((n + kSetupThreads - 1) / kSetupThreads), kSetupThreads, kSetupSmem, s>>>(a);
   return cudaGetLastError();
 }
