@@ -28,6 +28,7 @@ struct LabelSample {
   const unsigned char* masks;
   int M;
   int* cnt;  // shared: M + 1 counters of this warp
+  __device__ __forceinline__ void steps_done(int) {}
   __device__ __forceinline__ void flush_h() {}
   __device__ __forceinline__ void count_only(int) {}
   __device__ __forceinline__ void sample(const int4& ra, const float4&, int k, bool valid) {
@@ -64,6 +65,7 @@ struct MinOwnerSample {
   __device__ __forceinline__ void quiet_row(int, int) {}
   int* owner;
   int tet;
+  __device__ __forceinline__ void steps_done(int) {}
   __device__ __forceinline__ void flush_h() {}
   __device__ __forceinline__ void count_only(int) {}
   __device__ __forceinline__ void sample(const int4& ra, const float4&, int k, bool valid) {
@@ -85,6 +87,7 @@ struct DvfSample {
   double sp0, sp1, sp2;
   float* dvf;
   unsigned char* cov;
+  __device__ __forceinline__ void steps_done(int) {}
   __device__ __forceinline__ void flush_h() {}
   __device__ __forceinline__ void count_only(int) {}
   __device__ __forceinline__ void sample(const int4& ra, const float4& rb, int k, bool valid) {

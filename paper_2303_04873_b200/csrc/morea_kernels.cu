@@ -721,8 +721,8 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       // Sweep in windows of 32 kStartWords samples.  The bitmap holds the row
       // starts of the window (bit s of word s/32); a lane's row is the number of
       // starts <= its sample index, minus one.  Past the end that is the last row
-      // (no starts there), evaluated with valid = false.  Blocks of 16 steps; the
-      // fp32 partial sums are flushed between blocks.
+      // (no starts there), evaluated with valid = false.  The fp32 partial sums
+      // are flushed once 16 or more steps accumulated (steps_done), across chunks.
       const unsigned le_mask = (2u << lane) - 1u;
       int rprev = -1;
       for (int base = 0; base < total; base += 32 * kStartWords) {
@@ -735,21 +735,18 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
         if (len > 0 && start >= base && start < base + 32 * kStartWords)
           atomicOr(&S.starts[(start - base) >> 5], 1u << (start & 31));
         __syncwarp();
-        for (int w0 = 0; w0 < nw; w0 += 16) {
-          const int wend = min(nw, w0 + 16);
-          for (int w = w0; w < wend; w++) {
-            MOREA_CHECK(w >= 0 && w < kStartWords);
-            const unsigned M = S.starts[w];
-            const int row = rprev + __popc(M & le_mask);
-            rprev += __popc(M);
-            const int idx = base + (w << 5) + lane;
-            const bool valid = idx < total;
-            MOREA_CHECK(row >= 0 && row < 32);
-            const int4 ra = S.row_a[row];
-            f.sample(ra, S.row_b[row], valid ? idx - ra.x : 0, valid);
-          }
-          f.flush_h();
+        for (int w = 0; w < nw; w++) {
+          MOREA_CHECK(w >= 0 && w < kStartWords);
+          const unsigned M = S.starts[w];
+          const int row = rprev + __popc(M & le_mask);
+          rprev += __popc(M);
+          const int idx = base + (w << 5) + lane;
+          const bool valid = idx < total;
+          MOREA_CHECK(row >= 0 && row < 32);
+          const int4 ra = S.row_a[row];
+          f.sample(ra, S.row_b[row], valid ? idx - ra.x : 0, valid);
         }
+        f.steps_done(nw);
       }
       __syncwarp();
     }
@@ -828,10 +825,11 @@ struct Acc {
   // once per flush): two fewer registers in the sweep, whose register pressure
   // otherwise spills the row-chunk state (1.2% measured)
   volatile double* hg;
-  float hf;     // fp32 partial sum of h over the last < 16 steps (flushed into h)
+  float hf;     // fp32 partial sum of h over at most 47 steps (flushed into h)
   float gf;     // fp32 partial sum of guidance terms since the last flush (into g)
   int n;        // samples
   int qn;       // band entries in the per-warp queue (warp-uniform)
+  int ns;       // sweep steps since the last flush (warp-uniform)
 };
 
 template <bool TEX, int SIDE_T, bool CLAMP, bool DUMP>
@@ -981,6 +979,16 @@ struct Sample {
       }
   }
 
+  // the fp32 partial sums are flushed into the fp64 lane sums once at least 16 steps
+  // have been added since the last flush (so at most 15 + 32 = 47 steps per fp32 sum)
+  __device__ __forceinline__ void steps_done(int n) {
+    acc.ns += n;
+    if (acc.ns >= 16) {
+      flush_h();
+      acc.ns = 0;
+    }
+  }
+
   __device__ __forceinline__ void flush_h() {
     const double h = acc.hg[0], g = acc.hg[1];
     acc.hg[0] = h + (double)acc.hf;
@@ -1058,8 +1066,8 @@ struct Sample {
     } else {
       h = (a == 0.f && !fg) ? 0.f : 1.f;
     }
-    // fp32 partial sum over at most 16 steps; raster() flushes it into the fp64
-    // lane sum (flush_h) every 16 steps
+    // fp32 partial sum over at most 47 steps; raster() flushes it into the fp64
+    // lane sum (steps_done / flush_h) once 16 or more steps accumulated
     acc.hf += valid ? h : 0.f;
     if (DUMP && valid) {  // the values just computed, at voxel q = lin - SIDE V
       const long long q = (long long)lin - (long long)SIDE * V.V;
@@ -1241,7 +1249,7 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
     MOREA_CHECK(e >= 0 && e < A.n_entries && v < A.n_raster_versions);
     const long long i = ((long long)v * A.n_entries + e) * A.P + sol;
     double hg_local[2] = {0.0, 0.0};
-    Acc acc{hg_local, 0.f, 0.f, 0, 0};
+    Acc acc{hg_local, 0.f, 0.f, 0, 0, 0};
     int n_side0 = 0;
 #pragma unroll 1
     for (int side = 0; side < 2; side++) {
@@ -1504,6 +1512,7 @@ struct OwnerSample {
   __device__ __forceinline__ short2 quiet_hull(int) const { return make_short2(0, -1); }
   __device__ __forceinline__ void count_quiet(int) {}
   __device__ __forceinline__ void quiet_row(int, int) {}
+  __device__ __forceinline__ void steps_done(int) {}
   __device__ __forceinline__ void flush_h() {}
   __device__ __forceinline__ void count_only(int) {}
   __device__ __forceinline__ void sample(const int4& ra, const float4&, int k, bool valid) {
