@@ -605,6 +605,7 @@ struct WarpSmem {
   float4 sc0, sc1;   // per-side sample constants (see Sample)
   int2 slices[32];   // non-empty z-slices of the current 32-slice chunk: (first row, ylo | slice << 16)
   unsigned long long stat[4];  // samples, band entries, items, skipped samples of this warp (profiling)
+  unsigned swept;  // samples swept in the current item (profiling; lane 0)
   // band-entry queue of the guidance term (a6): entries are evaluated 32 at a time
   float4 qa[kQueueCap];  // (u, v, fx, fy): footprint texel coordinates and weights
   int2 qb[kQueueCap];    // (fz bits, own linear index)
@@ -692,8 +693,8 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       // Quiet samples (profiling) = the item's samples - the swept ones: -total here,
       // +n at the item's end (k_raster)
       f.count_only(len_all);
-      if (F::kQuiet && lane == 0) f.count_quiet(-total);
       if (total == 0) continue;
+      if (F::kQuiet && lane == 0) f.count_quiet(total);
       const unsigned ne = __ballot_sync(FULLMASK, len > 0);
       const int start = incl - len;
       __syncwarp();
@@ -970,7 +971,7 @@ struct Sample {
     return __ldg(&V.qhull[0][idx]);  // qoff carries the side (qhull[1] follows qhull[0])
   }
   // samples of a chunk's quiet rows (profiling; lane 0, per-warp shared counter)
-  __device__ __forceinline__ void count_quiet(int n) { S.stat[3] += (unsigned long long)n; }
+  __device__ __forceinline__ void count_quiet(int n) { S.swept += (unsigned)n; }
   __device__ __forceinline__ void quiet_row(int q0, int n) {
     if (DUMP)
       for (int i = 0; i < n; i++) {
@@ -1236,7 +1237,10 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
   WarpSmem& S = smem[warp];
   const long long per_v = (long long)A.n_entries * A.P;
   const long long n_items = per_v * A.n_raster_versions;
-  if (lane == 0) S.stat[0] = S.stat[1] = S.stat[2] = S.stat[3] = 0ull;
+  if (lane == 0) {
+    S.stat[0] = S.stat[1] = S.stat[2] = S.stat[3] = 0ull;
+    S.swept = 0u;
+  }
   while (true) {
     unsigned long long item = 0;
     item = bq.claim(A.counter, lane, n_items, MOREA_CLAIM_CHUNK, MOREA_CLAIM_SPREAD);
@@ -1267,7 +1271,8 @@ __global__ void RASTER_BOUNDS k_raster(const EvalArgs A) {
       A.hgn[i] = out;
       S.stat[0] += out.n;
       S.stat[2] += 1;
-      S.stat[3] += out.n;  // quiet samples: the chunks subtracted the swept ones
+      S.stat[3] += (unsigned long long)(out.n - (long long)S.swept);  // quiet = samples - swept
+      S.swept = 0u;
       debug_count_item(A);
     }
   }
