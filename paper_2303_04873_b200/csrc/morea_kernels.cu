@@ -687,15 +687,15 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
         len = 0;
         f.quiet_row((z * ny + y) * nx + xl, len_all);  // 2 V < 2^31 (own-record index is an int)
       }
+      // every sample counts (n), per lane: the item's warp reduction sums the lanes.
+      // Quiet samples (profiling) = the item's samples - the swept ones (count_quiet
+      // adds the swept ones, k_raster takes the difference per item)
+      f.count_only(len_all);
+      const unsigned ne = __ballot_sync(FULLMASK, len > 0);
+      if (ne == 0u) continue;  // nothing to sweep: no prefix sum
       const int incl = warp_incl_scan(len, lane);
       const int total = __shfl_sync(FULLMASK, incl, 31);
-      // every sample counts (n), per lane: the item's warp reduction sums the lanes.
-      // Quiet samples (profiling) = the item's samples - the swept ones: -total here,
-      // +n at the item's end (k_raster)
-      f.count_only(len_all);
-      if (total == 0) continue;
       if (F::kQuiet && lane == 0) f.count_quiet(total);
-      const unsigned ne = __ballot_sync(FULLMASK, len > 0);
       const int start = incl - len;
       __syncwarp();
       {
