@@ -542,7 +542,6 @@ __device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, boo
   }
   const int lo = R.lo[0], hi = R.hi[0];
   const float dy = (float)(y - R.lo[1]), dz = (float)(z - R.lo[2]);
-  const float flo = (float)lo - 4.5f, fhi = (float)hi + 4.5f;
   // faces [0, nl) bound x from below, [nl, 4) from above (k_setup order, 1 <= nl <= 3):
   // owned x > max of the lower crossings and x < min of the upper ones.  Only the
   // binding crossing's rounding matters, so the ambiguity test is on the max / min
@@ -553,8 +552,10 @@ __device__ __forceinline__ void row_interval(const SideRec& R, int y, int z, boo
   const float x2 = fmaf(f2.z, dz, fmaf(f2.y, dy, f2.x)), x3 = fmaf(f3.z, dz, fmaf(f3.y, dy, f3.x));
   float ml = fmaxf(x0, fmaxf(nl > 1 ? x1 : x0, nl > 2 ? x2 : x0));
   float mh = fminf(x3, fminf(nl < 3 ? x2 : x3, nl < 2 ? x1 : x3));
-  ml = fminf(fmaxf(ml, flo), fhi);
-  mh = fminf(fmaxf(mh, flo), fhi);
+  // no clamp to the bbox: the fp32 error bound (thr) holds for every row of the
+  // item, |x*| < 2^19 for regular faces (thr < 1/4), and the max / min with lo, hi
+  // below bound the interval; a crossing far outside the bbox that happens to lie
+  // near an integer only sends the row to the exact routine
   bool amb = (fabsf(ml - rintf(ml)) <= f0.w) || (fabsf(mh - rintf(mh)) <= f3.w);
   // lower: smallest x > x*; upper: largest x < x* = ceil(x*) - 1
   xl = max(lo, __float2int_ru(ml));
