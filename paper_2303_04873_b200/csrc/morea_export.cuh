@@ -22,7 +22,7 @@ __device__ __forceinline__ int voxel_label(unsigned m, int M) {
 struct LabelSample {
   static constexpr bool kQuiet = false;
   __device__ __forceinline__ int quiet_off() const { return -1; }
-  __device__ __forceinline__ short2 quiet_hull(int) const { return make_short2(0, -1); }
+  __device__ __forceinline__ unsigned quiet_hull(int) const { return 0xffff0000u; }
   __device__ __forceinline__ void count_quiet(int) {}
   __device__ __forceinline__ void quiet_row(int, int) {}
   const unsigned char* masks;
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_label_counts(const EvalArgs 
 struct MinOwnerSample {
   static constexpr bool kQuiet = false;
   __device__ __forceinline__ int quiet_off() const { return -1; }
-  __device__ __forceinline__ short2 quiet_hull(int) const { return make_short2(0, -1); }
+  __device__ __forceinline__ unsigned quiet_hull(int) const { return 0xffff0000u; }
   __device__ __forceinline__ void count_quiet(int) {}
   __device__ __forceinline__ void quiet_row(int, int) {}
   int* owner;
@@ -78,7 +78,7 @@ struct MinOwnerSample {
 struct DvfSample {
   static constexpr bool kQuiet = false;
   __device__ __forceinline__ int quiet_off() const { return -1; }
-  __device__ __forceinline__ short2 quiet_hull(int) const { return make_short2(0, -1); }
+  __device__ __forceinline__ unsigned quiet_hull(int) const { return 0xffff0000u; }
   __device__ __forceinline__ void count_quiet(int) {}
   __device__ __forceinline__ void quiet_row(int, int) {}
   const SideRec* R;  // shared

@@ -674,9 +674,9 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       // the row's hull (quiet rows, below) is loaded before the interval is
       // computed, so its latency overlaps the interval arithmetic
       const int qo = F::kQuiet ? f.quiet_off() : -1;  // item-uniform; -1: radius beyond the hulls
-      short2 hb = make_short2(0, -1);
+      unsigned hbw = 0xffff0000u;  // packed hull (first | last << 16); (0, -1): empty
       if (F::kQuiet && qo >= 0)  // unconditional load (lanes past the chunk read the plane's first row)
-        hb = f.quiet_hull(qo + (rv ? z * ny + y : 0));
+        hbw = f.quiet_hull(qo + (rv ? z * ny + y : 0));
       row_interval(R, y, z, rv, xl, xh);  // every lane (warp-collective)
       const int len_all = rv ? max(0, xh - xl + 1) : 0;
       // quiet rows (empty space): every voxel of the row is background
@@ -684,7 +684,12 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       // each sample's h is exactly 0 -- counted, not swept.  The row is quiet when
       // [xl, xh] lies outside the hull of the image row's non-quiet voxels.
       int len = len_all;
-      if (F::kQuiet && qo >= 0 && len_all > 0 && (xh < hb.x || xl > hb.y)) {
+      // the hull's halves are sign-extended by PRMTs that also read xh / xl, so they
+      // are scheduled after the interval and the hull load's latency stays hidden
+      int hx, hy;
+      asm("prmt.b32 %0, %1, %2, 0x9910;" : "=r"(hx) : "r"(hbw), "r"(xh));
+      asm("prmt.b32 %0, %1, %2, 0xBB32;" : "=r"(hy) : "r"(hbw), "r"(xl));
+      if (F::kQuiet && qo >= 0 && len_all > 0 && (xh < hx || xl > hy)) {
         len = 0;
         f.quiet_row((z * ny + y) * nx + xl, len_all);  // 2 V < 2^31 (own-record index is an int)
       }
@@ -967,9 +972,9 @@ struct Sample {
   // quiet rows (raster): the side's row hulls at the item's radius R (SideRec flags)
   static constexpr bool kQuiet = true;
   __device__ __forceinline__ int quiet_off() const { return qoff; }
-  __device__ __forceinline__ short2 quiet_hull(int idx) const {
-    const int SIDE = SIDE_T >= 0 ? SIDE_T : side;
-    return __ldg(&V.qhull[0][idx]);  // qoff carries the side (qhull[1] follows qhull[0])
+  __device__ __forceinline__ unsigned quiet_hull(int idx) const {
+    // one 32-bit load of the packed short2 (first, last)
+    return __ldg(reinterpret_cast<const unsigned*>(V.qhull[0]) + idx);  // qoff carries the side
   }
   // samples of a chunk's quiet rows (profiling; lane 0, per-warp shared counter)
   __device__ __forceinline__ void count_quiet(int n) { S.swept += (unsigned)n; }
@@ -1515,7 +1520,7 @@ struct OwnerSample {
   int tet;
   static constexpr bool kQuiet = false;
   __device__ __forceinline__ int quiet_off() const { return -1; }
-  __device__ __forceinline__ short2 quiet_hull(int) const { return make_short2(0, -1); }
+  __device__ __forceinline__ unsigned quiet_hull(int) const { return 0xffff0000u; }
   __device__ __forceinline__ void count_quiet(int) {}
   __device__ __forceinline__ void quiet_row(int, int) {}
   __device__ __forceinline__ void steps_done(int) {}
