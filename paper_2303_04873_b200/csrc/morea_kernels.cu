@@ -657,14 +657,17 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
                    : "memory");
       __syncwarp();
     }
+    // the lane's slice start for the row lookup; empty slices never match (one
+    // value across the row loop instead of two)
+    const int zs = zne ? zstart : 0x7fffffff;
     const unsigned le_mask0 = (2u << lane) - 1u;
     for (int r0 = 0; r0 < nrows; r0 += 32) {
       const int r = r0 + lane;
       // the lane's slice: rank = (non-empty slices starting before r0) + (slice
       // starts in [r0, r]) - 1, from one OR-reduction of start bits and a ballot
-      const unsigned sb = __reduce_or_sync(
-          FULLMASK, (zne && zstart >= r0 && zstart < r0 + 32) ? (1u << (zstart - r0)) : 0u);
-      const int before = __popc(__ballot_sync(FULLMASK, zne && zstart < r0));
+      const unsigned sb =
+          __reduce_or_sync(FULLMASK, (zs >= r0 && zs < r0 + 32) ? (1u << (zs - r0)) : 0u);
+      const int before = __popc(__ballot_sync(FULLMASK, zs < r0));
       MOREA_CHECK(before + __popc(sb & le_mask0) - 1 >= 0 && before + __popc(sb & le_mask0) - 1 < 32);
       const int2 sl = S.slices[before + __popc(sb & le_mask0) - 1];
       int xl, xh;
