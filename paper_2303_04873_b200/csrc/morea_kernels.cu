@@ -931,12 +931,11 @@ struct Sample {
 
   // Band entries of this step's samples, one round per set bit, go to the
   // per-warp queue, evaluated 32 at a time (acc.qn: queued count, warp-uniform).
-  __device__ __forceinline__ void enqueue(unsigned bm, int lin, float u, float v, float fx, float fy,
-                                          float fz, int s) {
+  __device__ __forceinline__ void enqueue(unsigned bm, unsigned take, int lin, float u, float v, float fx,
+                                          float fy, float fz, int s) {
+    // take: the ballot of bm != 0 (non-zero: the caller's test)
     const int lane = threadIdx.x & 31;
-    while (true) {
-      const unsigned take = __ballot_sync(FULLMASK, bm != 0u);
-      if (!take) break;
+    do {
       {
         // computed by every lane, stored by lanes with a bit: predicated stores,
         // no divergent branch (no convergence barrier per round)
@@ -967,7 +966,8 @@ struct Sample {
         entry(ea.x, ea.y, ea.z, ea.w, __int_as_float(eb.x), eb.y, (int)S.qi[acc.qn + lane], s);
         __syncwarp();
       }
-    }
+      take = __ballot_sync(FULLMASK, bm != 0u);
+    } while (take);
   }
 
   __device__ __forceinline__ void count_only(int t) { acc.n += t; }
@@ -1085,7 +1085,8 @@ struct Sample {
       dump_fg[q] = fg ? 1 : 0;
     }
     // a6: band entries go to the per-warp queue, evaluated 32 at a time
-    if (__any_sync(FULLMASK, bm != 0u)) enqueue(bm, lin, u, v, fx, fy, fz, SIDE);
+    const unsigned take = __ballot_sync(FULLMASK, bm != 0u);
+    if (take) enqueue(bm, take, lin, u, v, fx, fy, fz, SIDE);
   }
 };
 
