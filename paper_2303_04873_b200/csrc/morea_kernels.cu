@@ -733,7 +733,6 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
       // starts <= its sample index, minus one.  Past the end that is the last row
       // (no starts there), evaluated with valid = false.  The fp32 partial sums
       // are flushed once 16 or more steps accumulated (steps_done), across chunks.
-      const unsigned le_mask = (2u << lane) - 1u;
       int rprev = -1;
       for (int base = 0; base < total; base += 32 * kStartWords) {
         const int nw = min(kStartWords, (total - base + 31) >> 5);
@@ -748,7 +747,9 @@ __device__ __forceinline__ void raster(const SideRec& R, int nx, int ny, int lof
         for (int w = 0; w < nw; w++) {
           MOREA_CHECK(w >= 0 && w < kStartWords);
           const unsigned M = S.starts[w];
-          const int row = rprev + __popc(M & le_mask);
+          unsigned lem;  // lanes <= this one (special register: no recomputation)
+          asm("mov.u32 %0, %%lanemask_le;" : "=r"(lem));
+          const int row = rprev + __popc(M & lem);
           rprev += __popc(M);
           const int idx = base + (w << 5) + lane;
           const bool valid = idx < total;
